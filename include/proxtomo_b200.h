@@ -1,0 +1,226 @@
+/*
+ * proxtomo_b200.h -- C ABI of the B200-native ProxSkip-VR CT hot path.
+ *
+ * The reference (`proxtomo`, arxiv/paper_2602_09527) is pure Python; its seam
+ * for this path is a duck-typed projector object plus plain functions.  Each
+ * entry point below replaces one reference call; the reference symbol it
+ * stands in for is cited as pkg/src/proxtomo/<file>:<lines>.
+ *
+ * Conventions
+ *  - Every array argument is a caller-owned DEVICE pointer (float32, row-major,
+ *    contiguous) unless its name starts with `host_`.
+ *  - Images are (n_slices, height, width); n_slices == 1 is the 2D case.
+ *    Sinograms are (n_angles, n_slices, n_bins) (angle-major, so a subset is a
+ *    set of whole angle blocks); a selection's output is (n_sel, n_slices, n_bins).
+ *  - Every compute call is stream-ordered on `stream` (a cudaStream_t passed
+ *    as void*), performs no allocation and no host synchronisation unless
+ *    documented ("syncs").
+ *  - Return value: PT_OK (0) or a negative PT_E* code; pt_last_error() gives
+ *    the message of the calling thread's last failure.  PT_EINVAL maps to the
+ *    reference's ValueError, PT_ECUDA / PT_ENCCL to RuntimeError.
+ *  - A plan is immutable after creation (selections are added under a lock)
+ *    and may be shared by threads using distinct sessions / streams.
+ */
+#ifndef PROXTOMO_B200_H
+#define PROXTOMO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PT_OK 0
+#define PT_EINVAL -1
+#define PT_ECUDA -2
+#define PT_EUNSUPPORTED -3
+#define PT_ENCCL -4
+
+typedef struct pt_plan pt_plan;
+typedef struct pt_selection pt_selection;
+typedef struct pt_session pt_session;
+
+/* Scan geometry + image grid.  Replaces ParallelGeometry
+ * (pkg/src/proxtomo/geometry.py:9-47) bound to a grid by Projector
+ * (pkg/src/proxtomo/projector.py:143-153).  `host_angles` are radians,
+ * validated like the reference (strictly increasing, in [0, pi)). */
+typedef struct {
+    int32_t height, width;   /* image grid (H, W) */
+    int32_t n_slices;        /* >= 1; > 1 = slice-stacked 3D (rotation about z) */
+    int32_t n_angles, n_bins;
+    double bin_spacing, pixel_size;
+    const double* host_angles;
+} pt_geometry_desc;
+
+const char* pt_last_error(void);
+const char* pt_version(void);
+/* Process-wide number of kernels this library has launched (evidence that
+ * the native path, not a fallback, ran). */
+int64_t pt_launch_count(void);
+
+/* Plan lifecycle: uploads the per-angle Joseph tables (computed on the host
+ * in float64 from the reference's expressions, projector.py:26-61). */
+int pt_plan_create(const pt_geometry_desc* desc, pt_plan** out);
+int pt_plan_destroy(pt_plan* plan);
+
+/* An angle selection (a subset, projector.py:86-97 `pair(subset)`); NULL
+ * host_idx with n == -1 means all angles in order.  Index validation as
+ * projector.py:105-111.  Selections live as long as the plan. */
+int pt_selection_create(pt_plan* plan, const int32_t* host_idx, int32_t n, pt_selection** out);
+int32_t pt_selection_size(const pt_selection* sel);
+/* Sum over the selection of the number of nonzero Joseph weights (the
+ * reference's CSR nnz of A_S, projector.py:55-60), host-side count. */
+int64_t pt_selection_nnz(pt_plan* plan, const pt_selection* sel);
+
+/* y = A_S (x - x2) [- b_S].  Replaces forward_project (projector.py:114-126)
+ * and the residual of _subset_gradient (estimators.py:29-31).
+ * x2 (may be NULL) is subtracted before projection (SVRG: A_i(x - x_snap));
+ * data (may be NULL) is the FULL sinogram (n_angles, n_slices, n_bins) whose
+ * selected rows are subtracted; sumsq (may be NULL, device double[1]) receives
+ * sum(y^2) (objective, solvers.py:271-277).  Uses the plan's workspace:
+ * standalone calls on one plan must be serialised on one stream. */
+int pt_forward(pt_plan* plan, const pt_selection* sel, const float* x, const float* x2,
+               const float* data, float* y, double* sumsq, void* stream);
+
+/* x_out = alpha * A_S^T y (+ beta * x_out when accumulate != 0).  Replaces
+ * back_project (projector.py:129-140); a per-pixel gather, no atomics,
+ * deterministic. */
+int pt_adjoint(pt_plan* plan, const pt_selection* sel, const float* y, float* x_out,
+               float alpha, int32_t accumulate, void* stream);
+
+/* Estimator kinds (estimators.py:24). */
+#define PT_EST_FULL 0
+#define PT_EST_SGD 1
+#define PT_EST_SAGA 2
+#define PT_EST_SVRG 3
+#define PT_EST_LSVRG 4
+
+/* Fused adjoint + estimator + ProxSkip gradient half-step, one pass:
+ *   g    = A_S^T r                              (estimators.py:32)
+ *   est  = g | N g | N g + (S - N T_i) | N g + G (full/sgd/saga/svrg)
+ *          (estimators.py:55,92,146); SAGA also S <- (S - T_i) + g, T_i <- g
+ *          (estimators.py:93-94)
+ *   base = x - gamma est; x_hat = base + gamma h (solvers.py:236-237)
+ *   theta == 0: x_out = x_hat                   (solvers.py:246)
+ *   theta == 1: v_out = base + hcoef h, xhat_out = x_hat, hcoef = gamma - gamma/p
+ *               (solvers.py:242)
+ * A non-finite x_out sets *bad_iter = min(*bad_iter, iteration) (device int64;
+ * DivergenceError, solvers.py:247-248).  For SVRG, r must be A_i(x - x_snap)
+ * (b cancels) and aux0 = full_grad; for SAGA aux0 = table_i, aux1 = sum. */
+typedef struct {
+    int32_t estimator;
+    int32_t theta;
+    float n_scale;       /* N */
+    float gamma;
+    float hcoef;
+    int64_t iteration;
+    const float* x;
+    const float* h;
+    float* aux0;
+    float* aux1;
+    float* x_out;
+    float* v_out;
+    float* xhat_out;
+    int64_t* bad_iter;
+} pt_step_epilogue;
+
+int pt_adjoint_step(pt_plan* plan, const pt_selection* sel, const float* r,
+                    const pt_step_epilogue* ep, void* stream);
+/* The same epilogue applied to an already-reduced gradient g (multi-GPU path:
+ * partial A^T r per angle sector -> allreduce -> this). */
+int pt_step_epilogue_apply(pt_plan* plan, const float* g, const pt_step_epilogue* ep,
+                           void* stream);
+
+/* FGP TV prox (regularizers.py:90-133), temporally blocked.  v: prox input;
+ * lam = tau * alpha; p, q (and w in 3D) are the warm duals in/out (zeros =
+ * cold start; the caller applies the reference's reuse rule, :102-106);
+ * x_out = max(v - lam D^T(p,q), 0 if nonneg).  When h != NULL the ProxSkip
+ * control-variate update h += p_over_gamma (x_out - xhat) is fused into the
+ * last launch (solvers.py:249-250) and non-finite x_out raises *bad_iter.
+ * `work` is a device buffer of pt_fgp_workspace_floats() floats. */
+int64_t pt_fgp_workspace_floats(pt_plan* plan);
+int pt_tv_prox(pt_plan* plan, const float* v, double lam, int32_t inner_iterations,
+               int32_t nonneg, float* p, float* q, float* w, float* x_out, const float* xhat,
+               float* h, float p_over_gamma, int64_t iteration, int64_t* bad_iter, float* work,
+               void* stream);
+
+/* Reductions into device doubles (deterministic: fixed grid and combine
+ * order, float64 accumulation).  `out` must hold PT_RED_DOUBLES doubles:
+ * out[0] (and out[1] for pt_diff_norms) is the result, the rest scratch. */
+#define PT_RED_DOUBLES 1025
+int pt_dot(const float* a, const float* b, int64_t n, double* out, void* stream);
+/* isotropic TV, forward differences (regularizers.py:79-82; 3D adds z) */
+int pt_tv_value(pt_plan* plan, const float* x, double* out, void* stream);
+/* out[0] = sum((x - ref)^2), out[1] = sum(ref^2)   (metrics.py:19-27) */
+int pt_diff_norms(const float* x, const float* ref, int64_t n, double* out, void* stream);
+
+/* Squared operator norm by the reference's Rayleigh power method
+ * (projector.py:170-197); v0 is the host-drawn start vector (device copy,
+ * overwritten).  Syncs; returns the estimate in *host_out. */
+int pt_operator_norm_sq(pt_plan* plan, float* v0, int32_t iterations, double* host_out,
+                        void* stream);
+
+/* ------------------------------------------------------------------ */
+/* Native executor for the ProxSkip loop (solvers.py:159-324).          */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    int32_t estimator;       /* PT_EST_* */
+    int32_t n_subsets;
+    double gamma;
+    double skip_probability; /* p */
+    int32_t prox_kind;       /* 0 identity, 1 TV (FGP) */
+    double tv_alpha;
+    int32_t tv_inner;
+    int32_t tv_warm_start;
+    int32_t tv_nonneg;
+} pt_solver_desc;
+
+/* data: full sinogram (device, n_angles x n_slices x n_bins), must outlive the
+ * session.  x0 may be NULL (zeros, solvers.py:161). */
+int pt_session_create(pt_plan* plan, const pt_solver_desc* desc, const float* data,
+                      const float* x0, pt_session** out, void* stream);
+int pt_session_destroy(pt_session* s);
+/* SVRG/LSVRG initial snapshot + full gradient (estimators.py:117-123). */
+int pt_session_init(pt_session* s, void* stream);
+/* Enqueue n_steps iterations k0 .. k0+n_steps-1 of proxskip_step
+ * (solvers.py:230-254).  host_subset[j]: drawn subset index (ignored for
+ * full); host_theta[j]: Bernoulli(p) outcome; host_refresh[j]: SVRG snapshot
+ * refresh before step j (estimators.py:149-162).  No host sync. */
+int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
+                   const uint8_t* host_theta, const uint8_t* host_refresh, int64_t k0,
+                   void* stream);
+/* Device pointers of the live state (valid until the next run call). */
+float* pt_session_x(pt_session* s);
+float* pt_session_h(pt_session* s);
+float* pt_session_buffer(pt_session* s, int32_t which); /* 0 snapshot 1 full_grad 2 saga sum 3 saga table 4 dual p 5 dual q */
+int64_t* pt_session_bad_iter(pt_session* s);            /* device int64, INT64_MAX = finite */
+
+/* Per-kernel-category device time inside pt_session_run / _init (CUDA events
+ * on the session stream around each launch; off by default). */
+#define PT_PROF_FWD_BAND 0   /* forward band-partial kernel (per-step subset) */
+#define PT_PROF_FWD_REDUCE 1 /* forward band reduction (+ residual)           */
+#define PT_PROF_GATHER 2     /* fused gather + estimator + ProxSkip epilogue  */
+#define PT_PROF_FGP 3        /* one TV prox call (all its launches)           */
+#define PT_PROF_SNAPSHOT 4   /* SVRG snapshot full gradient (fwd + adj)       */
+#define PT_PROF_OTHER 5      /* copies, identity prox, allreduce              */
+#define PT_PROF_N 6
+int pt_session_set_profiling(pt_session* s, int32_t on);
+/* Syncs the session stream; returns accumulated ms and call counts per
+ * category since the last collection, then resets them. */
+int pt_session_profile(pt_session* s, double* host_ms, int64_t* host_calls);
+
+/* Multi-GPU (angle sectors).  The NCCL library is dlopen'ed from `nccl_path`
+ * (the torch-bundled libnccl.so.2), so this .so has no link-time NCCL.
+ * unique_id: 128 bytes from pt_nccl_unique_id on rank 0, broadcast by the
+ * caller.  After attach, the session's per-step subset gradients cover only
+ * angles [rank*A/world, (rank+1)*A/world) and are summed by ncclAllReduce on
+ * the session stream before the epilogue. */
+int pt_nccl_unique_id(const char* nccl_path, uint8_t* host_out128);
+int pt_session_attach_nccl(pt_session* s, const char* nccl_path, const uint8_t* host_id128,
+                           int32_t rank, int32_t world);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PROXTOMO_B200_H */

@@ -1,0 +1,368 @@
+// C ABI: plan / selection lifecycle, standalone operator entry points.
+// See include/proxtomo_b200.h for the contract of every function.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <vector>
+
+#include "pt_internal.cuh"
+
+namespace pt {
+
+static thread_local char g_err[1024] = "";
+std::atomic<long long> g_launches{0};
+
+void set_error(const char* fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int workspace_alloc(const pt_plan* plan, Workspace* ws)
+{
+    ws->partial_floats =
+        (size_t)plan->n_bands * plan->Z * plan->B * (size_t)plan->max_angles_per_launch;
+    size_t chunks = (plan->A + plan->max_angles_per_launch - 1) / plan->max_angles_per_launch;
+    ws->red_doubles = ((size_t)plan->A * plan->Z * plan->B + 255) / 256 + chunks + 16;
+    PT_CHECK_CUDA(cudaMalloc(&ws->partial, ws->partial_floats * sizeof(float)));
+    PT_CHECK_CUDA(cudaMalloc(&ws->red, ws->red_doubles * sizeof(double)));
+    return PT_OK;
+}
+
+void workspace_free(Workspace* ws)
+{
+    if (ws->partial) cudaFree(ws->partial);
+    if (ws->red) cudaFree(ws->red);
+    ws->partial = nullptr;
+    ws->red = nullptr;
+}
+
+static AngleTab make_tab(double theta, int H, int W, int B, double ds, double h)
+{
+    AngleTab t;
+    const double c = cos(theta), s = sin(theta);
+    const double cB = (B - 1) / 2.0, cH = (H - 1) / 2.0, cW = (W - 1) / 2.0;
+    if (fabs(c) >= fabs(s)) {  // projector.py:32
+        t.branch = 0;
+        t.sigma = ds / (h * c);
+        t.m = -(s / c);
+        t.a0 = -cB * t.sigma + cH * (s / c) + cW;
+        t.step_len = (float)(h / fabs(c));
+    } else {
+        t.branch = 1;
+        t.sigma = ds / (h * s);
+        t.m = -(c / s);
+        t.a0 = -cB * t.sigma + cW * (c / s) + cH;
+        t.step_len = (float)(h / fabs(s));
+    }
+    return t;
+}
+
+static int selection_build(pt_plan* plan, const int32_t* idx, int32_t n, pt_selection** out)
+{
+    pt_selection* sel = new pt_selection();
+    sel->n = n;
+    sel->h_angle.resize(n);
+    std::vector<int32_t> br[2];
+    for (int k = 0; k < n; ++k) {
+        const int a = idx ? idx[k] : k;
+        if (a < 0 || a >= plan->A) {
+            delete sel;
+            set_error("angle index out of range [0, %d)", plan->A);
+            return PT_EINVAL;
+        }
+        sel->h_angle[k] = a;
+        br[plan->h_tab[a].branch].push_back(k);
+    }
+    auto up = [&](int32_t** d, const std::vector<int32_t>& v) -> int {
+        PT_CHECK_CUDA(cudaMalloc(d, std::max<size_t>(1, v.size()) * sizeof(int32_t)));
+        if (!v.empty())
+            PT_CHECK_CUDA(cudaMemcpy(*d, v.data(), v.size() * sizeof(int32_t),
+                                     cudaMemcpyHostToDevice));
+        return PT_OK;
+    };
+    int rc = up(&sel->d_angle, sel->h_angle);
+    for (int b = 0; b < 2 && rc == PT_OK; ++b) {
+        sel->n_branch[b] = (int32_t)br[b].size();
+        rc = up(&sel->d_branch_pos[b], br[b]);
+    }
+    if (rc != PT_OK) {
+        delete sel;
+        return rc;
+    }
+    {
+        std::lock_guard<std::mutex> g(plan->mu);
+        plan->selections.push_back(sel);
+    }
+    *out = sel;
+    return PT_OK;
+}
+
+}  // namespace pt
+
+using namespace pt;
+
+extern "C" {
+
+const char* pt_last_error(void) { return g_err; }
+const char* pt_version(void) { return "proxtomo_b200 0.1.0 sm_100a"; }
+int64_t pt_launch_count(void) { return g_launches.load(); }
+
+int pt_plan_create(const pt_geometry_desc* d, pt_plan** out)
+{
+    if (!d || !out) { set_error("null argument"); return PT_EINVAL; }
+    if (d->height < 1 || d->width < 1 || d->n_slices < 1) { set_error("grid must be positive"); return PT_EINVAL; }
+    if (d->n_angles < 1) { set_error("geometry needs at least one projection angle"); return PT_EINVAL; }
+    if (d->n_bins < 1) { set_error("n_bins must be >= 1"); return PT_EINVAL; }
+    if (!(d->bin_spacing > 0.0) || !(d->pixel_size > 0.0)) {
+        set_error("bin_spacing and pixel_size must be positive");
+        return PT_EINVAL;
+    }
+    for (int a = 0; a < d->n_angles; ++a) {
+        if (a && !(d->host_angles[a] > d->host_angles[a - 1])) { set_error("angles must be strictly increasing"); return PT_EINVAL; }
+    }
+    if (d->host_angles[0] < 0.0 || d->host_angles[d->n_angles - 1] >= M_PI) { set_error("angles must lie in [0, pi)"); return PT_EINVAL; }
+
+    pt_plan* p = new pt_plan();
+    p->H = d->height; p->W = d->width; p->Z = d->n_slices;
+    p->A = d->n_angles; p->B = d->n_bins;
+    p->ds = d->bin_spacing; p->h = d->pixel_size;
+    p->angles.assign(d->host_angles, d->host_angles + d->n_angles);
+    p->h_tab.resize(p->A);
+    double max_br = 0, max_bc = 0, min_abs_sigma = 1e300;
+    for (int a = 0; a < p->A; ++a) {
+        const AngleTab t = make_tab(p->angles[a], p->H, p->W, p->B, p->ds, p->h);
+        p->h_tab[a] = t;
+        const double ar = t.branch ? -1.0 : t.m, ac = t.branch ? t.m : -1.0;
+        max_br = std::max(max_br, fabs(ar / t.sigma));
+        max_bc = std::max(max_bc, fabs(ac / t.sigma));
+        min_abs_sigma = std::min(min_abs_sigma, fabs(t.sigma));
+    }
+    p->cand_half = std::max(1, (int)ceil(1.0 / min_abs_sigma - 1e-12));
+    p->gather_slot = (int)ceil(31 * max_br + 63 * max_bc) + 2 * p->cand_half + 8;
+    const int mn = std::min(p->H, p->W);
+    p->fwd_ty = mn >= 512 ? 64 : (mn >= 128 ? 32 : 16);
+    p->fwd_tx = mn >= 512 ? 256 : (mn >= 128 ? 128 : 64);
+    p->n_bands = (std::max(p->H, p->W) + p->fwd_ty - 1) / p->fwd_ty;
+    const size_t per_angle = (size_t)p->n_bands * p->Z * p->B;
+    const size_t cap_floats = (size_t)1 << 28;  // 1 GiB of band partials
+    p->max_angles_per_launch = (int)std::max<size_t>(1, std::min<size_t>(p->A, cap_floats / per_angle));
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) { set_error("cudaGetDevice: %s", cudaGetErrorString(e)); delete p; return PT_ECUDA; }
+    if (cudaMalloc(&p->d_tab, sizeof(AngleTab) * p->A) != cudaSuccess ||
+        cudaMemcpy(p->d_tab, p->h_tab.data(), sizeof(AngleTab) * p->A, cudaMemcpyHostToDevice) != cudaSuccess) {
+        set_error("angle table upload failed");
+        delete p;
+        return PT_ECUDA;
+    }
+    int rc = workspace_alloc(p, &p->ws);
+    if (rc == PT_OK) rc = selection_build(p, nullptr, p->A, &p->all);
+    if (rc != PT_OK) { pt_plan_destroy(p); return rc; }
+    *out = p;
+    return PT_OK;
+}
+
+int pt_plan_destroy(pt_plan* p)
+{
+    if (!p) return PT_OK;
+    for (pt_selection* s : p->selections) {
+        cudaFree(s->d_angle);
+        cudaFree(s->d_branch_pos[0]);
+        cudaFree(s->d_branch_pos[1]);
+        delete s;
+    }
+    workspace_free(&p->ws);
+    if (p->d_tab) cudaFree(p->d_tab);
+    delete p;
+    return PT_OK;
+}
+
+int pt_selection_create(pt_plan* plan, const int32_t* host_idx, int32_t n, pt_selection** out)
+{
+    if (!plan || !out) { set_error("null argument"); return PT_EINVAL; }
+    if (!host_idx && n == -1) { *out = plan->all; return PT_OK; }
+    if (n < 0 || (!host_idx && n > 0)) { set_error("bad selection"); return PT_EINVAL; }
+    return selection_build(plan, host_idx, n, out);
+}
+
+int32_t pt_selection_size(const pt_selection* sel) { return sel ? sel->n : -1; }
+
+int64_t pt_selection_nnz(pt_plan* plan, const pt_selection* sel)
+{
+    if (!plan || !sel) return -1;
+    if (sel->nnz >= 0) return sel->nnz;
+    // exact count of kept COO entries (projector.py:55-60), float64 as the reference
+    int64_t total = 0;
+    const int H = plan->H, W = plan->W, B = plan->B;
+    for (int k = 0; k < sel->n; ++k) {
+        const double th = plan->angles[sel->h_angle[k]];
+        const double c = cos(th), s = sin(th), h = plan->h;
+        const bool rows = fabs(c) >= fabs(s);
+        const int n_steps = rows ? H : W, n_lanes = rows ? W : H;
+        const double step_len = rows ? h / fabs(c) : h / fabs(s);
+        int64_t cnt = 0;
+#pragma omp parallel for reduction(+ : cnt)
+        for (int b = 0; b < B; ++b) {
+            const double sb = ((double)b - (B - 1) / 2.0) * plan->ds;
+            for (int st = 0; st < n_steps; ++st) {
+                double cross;
+                if (rows) cross = (sb - (((double)st - (H - 1) / 2.0) * h) * s) / c;
+                else cross = (sb - (((double)st - (W - 1) / 2.0) * h) * c) / s;
+                const double pos = cross / h + (n_lanes - 1) / 2.0;
+                const double fl = floor(pos);
+                const double fr = pos - fl;
+                const long long l0 = (long long)fl;
+                if (l0 >= 0 && l0 < n_lanes && (1.0 - fr) * step_len > 0.0) ++cnt;
+                if (l0 + 1 >= 0 && l0 + 1 < n_lanes && fr * step_len > 0.0) ++cnt;
+            }
+        }
+        total += cnt;
+    }
+    const_cast<pt_selection*>(sel)->nnz = total * plan->Z;
+    return sel->nnz;
+}
+
+int pt_forward(pt_plan* plan, const pt_selection* sel, const float* x, const float* x2,
+               const float* data, float* y, double* sumsq, void* stream)
+{
+    if (!plan || !sel || !x || !y) { set_error("null argument"); return PT_EINVAL; }
+    return launch_forward(plan, &plan->ws, sel, x, x2, data, y, sumsq, (cudaStream_t)stream);
+}
+
+int pt_adjoint(pt_plan* plan, const pt_selection* sel, const float* y, float* x_out, float alpha,
+               int32_t accumulate, void* stream)
+{
+    if (!plan || !sel || !y || !x_out) { set_error("null argument"); return PT_EINVAL; }
+    if (sel->n == 0) {
+        if (!accumulate)
+            PT_CHECK_CUDA(cudaMemsetAsync(x_out, 0, sizeof(float) * (size_t)plan->Z * plan->H * plan->W,
+                                          (cudaStream_t)stream));
+        return PT_OK;
+    }
+    return launch_adjoint(plan, sel, y, x_out, alpha, accumulate, nullptr, (cudaStream_t)stream);
+}
+
+static int check_ep(const pt_step_epilogue* ep)
+{
+    if (!ep || !ep->x || !ep->h) { set_error("epilogue needs x and h"); return PT_EINVAL; }
+    if (ep->estimator < PT_EST_FULL || ep->estimator > PT_EST_LSVRG) { set_error("unknown estimator"); return PT_EINVAL; }
+    if (ep->estimator == PT_EST_SAGA && (!ep->aux0 || !ep->aux1)) { set_error("saga needs table and sum"); return PT_EINVAL; }
+    if ((ep->estimator == PT_EST_SVRG || ep->estimator == PT_EST_LSVRG) && !ep->aux0) { set_error("svrg needs full_grad"); return PT_EINVAL; }
+    if (ep->theta ? (!ep->v_out || !ep->xhat_out) : !ep->x_out) { set_error("missing epilogue output"); return PT_EINVAL; }
+    return PT_OK;
+}
+
+int pt_adjoint_step(pt_plan* plan, const pt_selection* sel, const float* r,
+                    const pt_step_epilogue* ep, void* stream)
+{
+    if (!plan || !sel || !r) { set_error("null argument"); return PT_EINVAL; }
+    int rc = check_ep(ep);
+    if (rc) return rc;
+    return launch_adjoint(plan, sel, r, nullptr, 1.f, 0, ep, (cudaStream_t)stream);
+}
+
+int pt_step_epilogue_apply(pt_plan* plan, const float* g, const pt_step_epilogue* ep, void* stream)
+{
+    if (!plan || !g) { set_error("null argument"); return PT_EINVAL; }
+    int rc = check_ep(ep);
+    if (rc) return rc;
+    return launch_epilogue(plan, g, ep, (cudaStream_t)stream);
+}
+
+int64_t pt_fgp_workspace_floats(pt_plan* plan) { return plan ? fgp_workspace_floats(plan) : -1; }
+
+int pt_tv_prox(pt_plan* plan, const float* v, double lam, int32_t inner_iterations, int32_t nonneg,
+               float* p, float* q, float* w, float* x_out, const float* xhat, float* h,
+               float p_over_gamma, int64_t iteration, int64_t* bad_iter, float* work, void* stream)
+{
+    if (!plan || !v || !p || !q || !x_out || !work) { set_error("null argument"); return PT_EINVAL; }
+    if (plan->Z > 1 && !w) { set_error("3D prox needs the third dual"); return PT_EINVAL; }
+    if (!(lam > 0.0)) { set_error("tau must be positive"); return PT_EINVAL; }
+    if (h && !xhat) { set_error("h update needs x_hat"); return PT_EINVAL; }
+    return launch_tv_prox(plan, v, lam, inner_iterations, nonneg, p, q, w, x_out, xhat, h,
+                          p_over_gamma, iteration, bad_iter, work, (cudaStream_t)stream);
+}
+
+int pt_dot(const float* a, const float* b, int64_t n, double* out, void* stream)
+{
+    if (!a || !b || !out || n < 0) { set_error("bad argument"); return PT_EINVAL; }
+    return launch_dot(a, b, n, out, (cudaStream_t)stream);
+}
+
+int pt_tv_value(pt_plan* plan, const float* x, double* out, void* stream)
+{
+    if (!plan || !x || !out) { set_error("null argument"); return PT_EINVAL; }
+    return launch_tv_value(plan, x, out, (cudaStream_t)stream);
+}
+
+int pt_diff_norms(const float* x, const float* ref, int64_t n, double* out, void* stream)
+{
+    if (!x || !ref || !out || n < 0) { set_error("bad argument"); return PT_EINVAL; }
+    return launch_diff_norms(x, ref, n, out, (cudaStream_t)stream);
+}
+
+int pt_operator_norm_sq(pt_plan* plan, float* v0, int32_t iterations, double* host_out, void* stream)
+{
+    if (!plan || !v0 || !host_out) { set_error("null argument"); return PT_EINVAL; }
+    if (iterations < 1) { set_error("iterations must be >= 1"); return PT_EINVAL; }
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = (size_t)plan->Z * plan->H * plan->W;
+    const size_t m = (size_t)plan->A * plan->Z * plan->B;
+    float *y = nullptr, *u = nullptr;
+    double* red = nullptr;
+    double* hist = nullptr;
+    int rc = PT_OK;
+    std::vector<double> h(3 * (size_t)iterations);
+    if (cudaMalloc(&y, m * 4) != cudaSuccess || cudaMalloc(&u, n * 4) != cudaSuccess ||
+        cudaMalloc(&red, 3 * PT_RED_DOUBLES * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&hist, 3 * (size_t)iterations * sizeof(double)) != cudaSuccess) {
+        set_error("operator_norm_sq: allocation failed");
+        rc = PT_ECUDA;
+    }
+    for (int it = 0; it < iterations && rc == PT_OK; ++it) {
+        rc = launch_forward(plan, &plan->ws, plan->all, v0, nullptr, nullptr, y, nullptr, st);
+        if (!rc) rc = launch_adjoint(plan, plan->all, y, u, 1.f, 0, nullptr, st);
+        if (!rc) rc = launch_dot(v0, u, n, red, st);
+        if (!rc) rc = launch_dot(v0, v0, n, red + PT_RED_DOUBLES, st);
+        if (!rc) rc = launch_dot(u, u, n, red + 2 * PT_RED_DOUBLES, st);
+        if (!rc) {
+            for (int j = 0; j < 3; ++j)
+                if (cudaMemcpyAsync(hist + 3 * it + j, red + j * PT_RED_DOUBLES, 8,
+                                    cudaMemcpyDeviceToDevice, st) != cudaSuccess) rc = PT_ECUDA;
+        }
+        if (!rc) rc = launch_scale_by_rsqrt(v0, u, red + 2 * PT_RED_DOUBLES, n, st);
+    }
+    if (rc == PT_OK) {
+        if (cudaMemcpyAsync(h.data(), hist, h.size() * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess) {
+            set_error("operator_norm_sq: %s", cudaGetErrorString(cudaGetLastError()));
+            rc = PT_ECUDA;
+        }
+    }
+    if (rc == PT_OK) {
+        // projector.py:170-180, replayed on the recorded scalars
+        double est = 0.0;
+        for (int it = 0; it < iterations; ++it) {
+            est = h[3 * it] / h[3 * it + 1];
+            if (sqrt(h[3 * it + 2]) == 0.0) { est = 0.0; break; }
+        }
+        *host_out = est;
+    }
+    cudaStreamSynchronize(st);
+    if (y) cudaFree(y);
+    if (u) cudaFree(u);
+    if (red) cudaFree(red);
+    if (hist) cudaFree(hist);
+    return rc;
+}
+
+}  // extern "C"

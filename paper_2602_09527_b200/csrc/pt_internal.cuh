@@ -1,0 +1,146 @@
+// Internal declarations shared by the sm_100a kernels and the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/proxtomo_b200.h"
+
+namespace pt {
+
+// Per-angle Joseph parameters, computed on the host in float64 from the
+// reference expressions (pkg/src/proxtomo/projector.py:28-51):
+//   pos(b, step) = a0 + b * sigma + step * m     (in lane units)
+// branch 0: |cos| >= |sin|, one sample per image row, lanes = columns
+//           sigma = ds/(h cos), m = -tan, a0 = -cB sigma + cH tan + cW
+// branch 1: one sample per image column, lanes = rows
+//           sigma = ds/(h sin), m = -cot, a0 = -cB sigma + cW cot + cH
+// with cB = (B-1)/2, cH = (H-1)/2, cW = (W-1)/2; step_len = h/max(|cos|,|sin|).
+struct AngleTab {
+    double sigma, m, a0;
+    float step_len;
+    int branch;
+};
+
+void set_error(const char* fmt, ...);
+
+#define PT_CHECK_CUDA(call)                                                          \
+    do {                                                                             \
+        cudaError_t e_ = (call);                                                     \
+        if (e_ != cudaSuccess) {                                                     \
+            ::pt::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,               \
+                            cudaGetErrorString(e_));                                 \
+            return PT_ECUDA;                                                         \
+        }                                                                            \
+    } while (0)
+
+extern std::atomic<long long> g_launches;  // kernels launched by this library
+
+#define PT_CHECK_LAUNCH()      \
+    do {                       \
+        ::pt::g_launches++;    \
+        PT_CHECK_CUDA(cudaGetLastError()); \
+    } while (0)
+
+}  // namespace pt
+
+struct pt_selection {
+    int32_t n = 0;
+    std::vector<int32_t> h_angle;       // geometry angle index per selection slot
+    int32_t* d_angle = nullptr;         // [n]
+    int32_t n_branch[2] = {0, 0};
+    int32_t* d_branch_pos[2] = {nullptr, nullptr};  // selection slots per branch
+    int64_t nnz = -1;
+};
+
+namespace pt {
+// Per-caller scratch for the forward band partials and reductions.  The plan
+// owns one (used by the standalone C-ABI calls, which must therefore be
+// stream-serialised per plan, like a cuFFT plan); every session owns its own.
+// Optional per-kernel device timing (CUDA events around launches on the
+// caller's stream), used by bench.py for the live roofline.
+struct Profiler {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    struct Rec { int cat; size_t ev0; };
+    std::vector<Rec> recs;
+    int depth = 0;  // nested scopes: only the outermost one records
+    double ms[PT_PROF_N] = {0};
+    long long calls[PT_PROF_N] = {0};
+    cudaEvent_t ev();
+    void begin(int cat, cudaStream_t st);  // pairs: begin, then end
+    void end(cudaStream_t st);
+    int collect();
+    ~Profiler();
+};
+struct Workspace {
+    float* partial = nullptr;
+    size_t partial_floats = 0;
+    double* red = nullptr;
+    size_t red_doubles = 0;
+    Profiler* prof = nullptr;
+};
+struct ProfScope {
+    Profiler* p;
+    cudaStream_t st;
+    ProfScope(Workspace* ws, int cat, cudaStream_t s) : p(ws && ws->prof && ws->prof->on ? ws->prof : nullptr), st(s)
+    {
+        if (p) p->begin(cat, st);
+    }
+    ~ProfScope() { if (p) p->end(st); }
+};
+int workspace_alloc(const pt_plan* plan, Workspace* ws);
+void workspace_free(Workspace* ws);
+}  // namespace pt
+
+struct pt_plan {
+    int32_t H = 0, W = 0, Z = 1, A = 0, B = 0;
+    double ds = 1.0, h = 1.0;
+    std::vector<double> angles;
+    std::vector<pt::AngleTab> h_tab;
+    pt::AngleTab* d_tab = nullptr;
+    int32_t cand_half = 1;     // gather candidates per side: ceil(h/ds) (1 = two-tap)
+    int32_t gather_slot = 0;   // floats of staged sinogram per angle in the gather
+    int32_t fwd_ty = 64, fwd_tx = 256;
+    int32_t n_bands = 0;
+    int32_t max_angles_per_launch = 0;
+    pt::Workspace ws;
+    int sm_count = 148;
+    std::mutex mu;
+    std::vector<pt_selection*> selections;
+    pt_selection* all = nullptr;
+};
+
+namespace pt {
+// kernels (projector.cu)
+int launch_forward(pt_plan* plan, Workspace* ws, const pt_selection* sel, const float* x,
+                   const float* x2, const float* data, float* y, double* sumsq, cudaStream_t st);
+int launch_adjoint(pt_plan* plan, const pt_selection* sel, const float* y, float* x_out,
+                   float alpha, int accumulate, const pt_step_epilogue* ep, cudaStream_t st,
+                   Workspace* ws = nullptr, int cat = PT_PROF_GATHER);
+int launch_epilogue(pt_plan* plan, const float* g, const pt_step_epilogue* ep, cudaStream_t st);
+// fgp.cu
+int64_t fgp_workspace_floats(const pt_plan* plan);
+int launch_tv_prox(pt_plan* plan, const float* v, double lam, int inner, int nonneg, float* p,
+                   float* q, float* w, float* x_out, const float* xhat, float* h,
+                   float p_over_gamma, int64_t iteration, int64_t* bad_iter, float* work,
+                   cudaStream_t st);
+// reduce.cu  (out: device doubles, out[0] = result, out[1 .. PT_RED_DOUBLES) scratch)
+int launch_dot(const float* a, const float* b, int64_t n, double* out, cudaStream_t st);
+int launch_tv_value(const pt_plan* plan, const float* x, double* out, cudaStream_t st);
+int launch_diff_norms(const float* x, const float* ref, int64_t n, double* out, cudaStream_t st);
+int launch_sum_doubles(const double* in, int64_t n, double* out, int accumulate, cudaStream_t st);
+int launch_identity_prox(const float* v, const float* xhat, float* x_out, float* h,
+                         float p_over_gamma, int64_t n, int64_t iteration, int64_t* bad_iter,
+                         cudaStream_t st);
+int launch_scale_by_rsqrt(float* v, const float* u, const double* sumsq, int64_t n,
+                          cudaStream_t st);
+int launch_fill_i64(int64_t* p, int64_t value, cudaStream_t st);
+int launch_sub(const float* a, const float* b, float* out, int64_t n, cudaStream_t st);
+}  // namespace pt

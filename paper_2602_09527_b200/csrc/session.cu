@@ -1,0 +1,471 @@
+// Native executor for the ProxSkip loop: owns the solver state in HBM and
+// enqueues whole segments of iterations with no host synchronisation.
+//
+// One iteration k (pkg/src/proxtomo/solvers.py:189-254):
+//   [refresh]  x_snap <- x; G <- A^T(A x_snap - b)           (estimators.py:126-130)
+//   forward    r = A_i x - b_i   |   r = A_i (x - x_snap) (SVRG: b cancels)
+//   gather     g = A_i^T r, est, base, x_hat, v / x+         (one fused kernel)
+//   [theta]    x+ = prox_{(gamma/p) alpha TV}(v), h += (p/gamma)(x+ - x_hat)
+// The subset / theta / refresh sequences are drawn on the host with the
+// reference's own PCG64 streams (solvers.py:164,174-176) and passed in.
+//
+// Multi-GPU (angle sectors): rank g owns angles [g A/G, (g+1) A/G); its
+// forward/gather cover only those rows of subset i; the partial A_i^T r is
+// summed with ncclAllReduce on the session stream; every rank then applies the
+// identical epilogue and prox, so the replicas stay bitwise equal.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <climits>
+#include <vector>
+
+#include "pt_internal.cuh"
+
+namespace {
+
+// Minimal NCCL ABI (nccl.h, 2.x): resolved at run time from the
+// torch-bundled libnccl.so.2 so this library never links a second NCCL.
+typedef struct { char internal[128]; } nccl_uid;
+typedef void* nccl_comm;
+typedef int (*fn_get_uid)(nccl_uid*);
+typedef int (*fn_init_rank)(nccl_comm*, int, nccl_uid, int);
+typedef int (*fn_allreduce)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t);
+typedef int (*fn_destroy)(nccl_comm);
+typedef const char* (*fn_errstr)(int);
+constexpr int kNcclFloat32 = 7;
+constexpr int kNcclSum = 0;
+
+struct NcclApi {
+    void* so = nullptr;
+    fn_get_uid get_uid = nullptr;
+    fn_init_rank init_rank = nullptr;
+    fn_allreduce allreduce = nullptr;
+    fn_destroy destroy = nullptr;
+    fn_errstr errstr = nullptr;
+};
+
+int nccl_load(const char* path, NcclApi* api)
+{
+    api->so = dlopen(path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!api->so) {
+        pt::set_error("dlopen(%s): %s", path ? path : "libnccl.so.2", dlerror());
+        return PT_ENCCL;
+    }
+    api->get_uid = (fn_get_uid)dlsym(api->so, "ncclGetUniqueId");
+    api->init_rank = (fn_init_rank)dlsym(api->so, "ncclCommInitRank");
+    api->allreduce = (fn_allreduce)dlsym(api->so, "ncclAllReduce");
+    api->destroy = (fn_destroy)dlsym(api->so, "ncclCommDestroy");
+    api->errstr = (fn_errstr)dlsym(api->so, "ncclGetErrorString");
+    if (!api->get_uid || !api->init_rank || !api->allreduce || !api->destroy) {
+        pt::set_error("libnccl is missing symbols");
+        return PT_ENCCL;
+    }
+    return PT_OK;
+}
+
+}  // namespace
+
+namespace pt {
+
+cudaEvent_t Profiler::ev()
+{
+    if (used == pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        pool.push_back(e);
+    }
+    return pool[used++];
+}
+
+void Profiler::begin(int cat, cudaStream_t st)
+{
+    if (depth++ > 0) return;
+    Rec r{cat, used};
+    cudaEventRecord(ev(), st);
+    ev();  // reserve the end event
+    recs.push_back(r);
+}
+
+void Profiler::end(cudaStream_t st)
+{
+    if (--depth > 0) return;
+    cudaEventRecord(pool[recs.back().ev0 + 1], st);
+}
+
+int Profiler::collect()
+{
+    for (const Rec& r : recs) {
+        cudaEventSynchronize(pool[r.ev0 + 1]);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, pool[r.ev0], pool[r.ev0 + 1]);
+        ms[r.cat] += t;
+        calls[r.cat] += 1;
+    }
+    recs.clear();
+    used = 0;
+    return PT_OK;
+}
+
+Profiler::~Profiler()
+{
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
+}
+
+}  // namespace pt
+
+struct pt_session {
+    pt_plan* plan = nullptr;
+    pt_solver_desc d{};
+    const float* data = nullptr;
+    size_t n = 0;
+    float* x[2] = {nullptr, nullptr};
+    int cur = 0;
+    float *h = nullptr, *v = nullptr, *xhat = nullptr;
+    float *snap = nullptr, *fg = nullptr;
+    float *saga_table = nullptr, *saga_sum = nullptr;
+    float *dp = nullptr, *dq = nullptr, *dw = nullptr;
+    float* fgp_work = nullptr;
+    float* r = nullptr;  // residual rows (largest selection)
+    float* g = nullptr;  // partial gradient (multi-GPU)
+    int64_t* bad = nullptr;
+    pt::Workspace ws;
+    pt::Profiler prof;
+    bool have_duals = false;
+    double dual_weight = 0.0;
+    std::vector<pt_selection*> subsets;  // (own rows of) subset i
+    pt_selection* own_all = nullptr;     // all (own) angles
+    // NCCL
+    NcclApi nccl;
+    nccl_comm comm = nullptr;
+    int rank = 0, world = 1;
+};
+
+namespace {
+
+int alloc_f(float** p, size_t n)
+{
+    PT_CHECK_CUDA(cudaMalloc(p, std::max<size_t>(1, n) * sizeof(float)));
+    return PT_OK;
+}
+
+// Selections of this rank: subset k = {k, k+N, ...} (geometry.py:75-82)
+// restricted to the owned angle sector.
+int build_selections(pt_session* s)
+{
+    pt_plan* P = s->plan;
+    const int A = P->A;
+    const int lo = (int)((long long)A * s->rank / s->world);
+    const int hi = (int)((long long)A * (s->rank + 1) / s->world);
+    std::vector<int32_t> own;
+    for (int a = lo; a < hi; ++a) own.push_back(a);
+    int rc;
+    if (s->world == 1) {
+        s->own_all = P->all;
+    } else {
+        rc = pt_selection_create(P, own.data(), (int32_t)own.size(), &s->own_all);
+        if (rc) return rc;
+    }
+    s->subsets.clear();
+    if (s->d.estimator != PT_EST_FULL) {
+        const int N = s->d.n_subsets;
+        for (int k = 0; k < N; ++k) {
+            std::vector<int32_t> idx;
+            for (int a = k; a < A; a += N)
+                if (a >= lo && a < hi) idx.push_back(a);
+            pt_selection* sel = nullptr;
+            rc = pt_selection_create(P, idx.data(), (int32_t)idx.size(), &sel);
+            if (rc) return rc;
+            s->subsets.push_back(sel);
+        }
+    }
+    return PT_OK;
+}
+
+int allreduce(pt_session* s, float* buf, cudaStream_t st)
+{
+    if (s->world == 1) return PT_OK;
+    int e = s->nccl.allreduce(buf, buf, s->n, kNcclFloat32, kNcclSum, s->comm, st);
+    if (e != 0) {
+        pt::set_error("ncclAllReduce: %s", s->nccl.errstr ? s->nccl.errstr(e) : "error");
+        return PT_ENCCL;
+    }
+    return PT_OK;
+}
+
+// G = A^T (A x - b) over the owned angles, summed over ranks (estimators.py:40-48)
+int full_gradient(pt_session* s, const float* x, float* out, cudaStream_t st)
+{
+    pt::ProfScope ps(&s->ws, PT_PROF_SNAPSHOT, st);
+    pt_plan* P = s->plan;
+    int rc = pt::launch_forward(P, &s->ws, s->own_all, x, nullptr, s->data, s->r, nullptr, st);
+    if (rc) return rc;
+    if (s->own_all->n == 0) {
+        PT_CHECK_CUDA(cudaMemsetAsync(out, 0, s->n * 4, st));
+    } else {
+        rc = pt::launch_adjoint(P, s->own_all, s->r, out, 1.f, 0, nullptr, st);
+        if (rc) return rc;
+    }
+    return allreduce(s, out, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+int pt_session_create(pt_plan* plan, const pt_solver_desc* desc, const float* data,
+                      const float* x0, pt_session** out, void* stream)
+{
+    if (!plan || !desc || !data || !out) { pt::set_error("null argument"); return PT_EINVAL; }
+    if (!(desc->gamma > 0.0)) { pt::set_error("gamma must be positive"); return PT_EINVAL; }
+    if (!(desc->skip_probability > 0.0 && desc->skip_probability <= 1.0)) {
+        pt::set_error("skip_probability must be in (0, 1]");
+        return PT_EINVAL;
+    }
+    if (desc->estimator < PT_EST_FULL || desc->estimator > PT_EST_LSVRG) { pt::set_error("unknown estimator"); return PT_EINVAL; }
+    if (desc->estimator != PT_EST_FULL && (desc->n_subsets < 1 || desc->n_subsets > plan->A)) {
+        pt::set_error("n_subsets must be in [1, n_angles], got %d for %d angles", desc->n_subsets, plan->A);
+        return PT_EINVAL;
+    }
+    if (desc->prox_kind == 1 && (!(desc->tv_alpha > 0.0) || desc->tv_inner < 1)) {
+        pt::set_error("bad TV configuration");
+        return PT_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    pt_session* s = new pt_session();
+    s->plan = plan;
+    s->d = *desc;
+    s->data = data;
+    s->n = (size_t)plan->Z * plan->H * plan->W;
+    const size_t n = s->n;
+    int rc = PT_OK;
+    auto A = [&](float** p, size_t cnt) { if (rc == PT_OK) rc = alloc_f(p, cnt); };
+    A(&s->x[0], n); A(&s->x[1], n); A(&s->h, n); A(&s->v, n); A(&s->xhat, n);
+    if (desc->estimator == PT_EST_SVRG || desc->estimator == PT_EST_LSVRG) { A(&s->snap, n); A(&s->fg, n); }
+    if (desc->estimator == PT_EST_SAGA) { A(&s->saga_table, n * desc->n_subsets); A(&s->saga_sum, n); }
+    if (desc->prox_kind == 1) {
+        A(&s->dp, n); A(&s->dq, n);
+        if (plan->Z > 1) A(&s->dw, n);
+        A(&s->fgp_work, (size_t)pt::fgp_workspace_floats(plan));
+    }
+    A(&s->r, (size_t)plan->A * plan->Z * plan->B);
+    A(&s->g, n);
+    if (rc == PT_OK && cudaMalloc(&s->bad, sizeof(int64_t)) != cudaSuccess) rc = PT_ECUDA;
+    if (rc == PT_OK) rc = pt::workspace_alloc(plan, &s->ws);
+    s->ws.prof = &s->prof;
+    if (rc == PT_OK) rc = build_selections(s);
+    if (rc == PT_OK) {
+        // solvers.py:161,172,178-179: x0 (or zeros), h = 0, SAGA table/sum = 0
+        if (x0) rc = cudaMemcpyAsync(s->x[0], x0, n * 4, cudaMemcpyDeviceToDevice, st) ? PT_ECUDA : PT_OK;
+        else rc = cudaMemsetAsync(s->x[0], 0, n * 4, st) ? PT_ECUDA : PT_OK;
+        if (!rc) rc = cudaMemsetAsync(s->h, 0, n * 4, st) ? PT_ECUDA : PT_OK;
+        if (!rc && s->saga_table) rc = cudaMemsetAsync(s->saga_table, 0, n * 4 * desc->n_subsets, st) ? PT_ECUDA : PT_OK;
+        if (!rc && s->saga_sum) rc = cudaMemsetAsync(s->saga_sum, 0, n * 4, st) ? PT_ECUDA : PT_OK;
+        if (!rc) rc = pt::launch_fill_i64(s->bad, INT64_MAX, st);
+    }
+    if (rc != PT_OK) {
+        pt_session_destroy(s);
+        return rc;
+    }
+    *out = s;
+    return PT_OK;
+}
+
+int pt_session_destroy(pt_session* s)
+{
+    if (!s) return PT_OK;
+    cudaDeviceSynchronize();
+    float* bufs[] = {s->x[0], s->x[1], s->h, s->v, s->xhat, s->snap, s->fg, s->saga_table,
+                     s->saga_sum, s->dp, s->dq, s->dw, s->fgp_work, s->r, s->g};
+    for (float* b : bufs)
+        if (b) cudaFree(b);
+    if (s->bad) cudaFree(s->bad);
+    pt::workspace_free(&s->ws);
+    if (s->comm && s->nccl.destroy) s->nccl.destroy(s->comm);
+    delete s;
+    return PT_OK;
+}
+
+int pt_session_init(pt_session* s, void* stream)
+{
+    if (!s) { pt::set_error("null session"); return PT_EINVAL; }
+    if (s->d.estimator != PT_EST_SVRG && s->d.estimator != PT_EST_LSVRG) return PT_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    // init_svrg_state (estimators.py:117-123): snapshot = x0, G = full gradient
+    PT_CHECK_CUDA(cudaMemcpyAsync(s->snap, s->x[s->cur], s->n * 4, cudaMemcpyDeviceToDevice, st));
+    return full_gradient(s, s->snap, s->fg, st);
+}
+
+int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
+                   const uint8_t* host_theta, const uint8_t* host_refresh, int64_t k0, void* stream)
+{
+    if (!s || n_steps < 0) { pt::set_error("bad argument"); return PT_EINVAL; }
+    cudaStream_t st = (cudaStream_t)stream;
+    pt_plan* P = s->plan;
+    const pt_solver_desc& d = s->d;
+    const bool vr = (d.estimator == PT_EST_SVRG || d.estimator == PT_EST_LSVRG);
+    const double gamma = d.gamma, p = d.skip_probability;
+    for (int j = 0; j < n_steps; ++j) {
+        const int64_t k = k0 + j;
+        int rc = PT_OK;
+        if (vr && host_refresh && host_refresh[j]) {
+            // refresh_svrg_state (estimators.py:126-130)
+            {
+                pt::ProfScope ps(&s->ws, PT_PROF_OTHER, st);
+                PT_CHECK_CUDA(cudaMemcpyAsync(s->snap, s->x[s->cur], s->n * 4, cudaMemcpyDeviceToDevice, st));
+            }
+            rc = full_gradient(s, s->snap, s->fg, st);
+            if (rc) return rc;
+        }
+        const pt_selection* sel = s->own_all;
+        int i = 0;
+        if (d.estimator != PT_EST_FULL) {
+            i = host_subset ? host_subset[j] : 0;
+            if (i < 0 || i >= d.n_subsets) {
+                pt::set_error("subset index %d out of range [0, %d)", i, d.n_subsets);
+                return PT_EINVAL;
+            }
+            sel = s->subsets[i];
+        }
+        const float* xc = s->x[s->cur];
+        float* xn = s->x[1 - s->cur];
+        const int theta = (p >= 1.0) ? 1 : (host_theta ? host_theta[j] : 0);
+
+        // forward: residual rows of the (own part of the) selection
+        if (vr) rc = pt::launch_forward(P, &s->ws, sel, xc, s->snap, nullptr, s->r, nullptr, st);
+        else rc = pt::launch_forward(P, &s->ws, sel, xc, nullptr, s->data, s->r, nullptr, st);
+        if (rc) return rc;
+
+        pt_step_epilogue ep;
+        memset(&ep, 0, sizeof(ep));
+        ep.estimator = d.estimator;
+        ep.theta = theta;
+        ep.n_scale = (float)d.n_subsets;
+        ep.gamma = (float)gamma;
+        ep.hcoef = (float)(gamma - gamma / p);  // solvers.py:242, exactly 0 at p = 1
+        ep.iteration = k;
+        ep.x = xc;
+        ep.h = s->h;
+        if (d.estimator == PT_EST_SAGA) {
+            ep.aux0 = s->saga_table + (size_t)i * s->n;
+            ep.aux1 = s->saga_sum;
+        } else if (vr) {
+            ep.aux0 = s->fg;
+        }
+        ep.x_out = xn;
+        ep.v_out = s->v;
+        ep.xhat_out = s->xhat;
+        ep.bad_iter = s->bad;
+        if (s->world == 1) {
+            rc = pt::launch_adjoint(P, sel, s->r, nullptr, 1.f, 0, &ep, st, &s->ws);
+        } else {
+            if (sel->n == 0) {
+                PT_CHECK_CUDA(cudaMemsetAsync(s->g, 0, s->n * 4, st));
+            } else {
+                rc = pt::launch_adjoint(P, sel, s->r, s->g, 1.f, 0, nullptr, st, &s->ws);
+            }
+            pt::ProfScope ps(&s->ws, PT_PROF_OTHER, st);
+            if (!rc) rc = allreduce(s, s->g, st);
+            if (!rc) rc = pt::launch_epilogue(P, s->g, &ep, st);
+        }
+        if (rc) return rc;
+
+        if (theta) {
+            const float pog = (float)(p / gamma);
+            if (d.prox_kind == 1) {
+                // _apply_prox -> tv_prox with tau = gamma/p (solvers.py:217-223,242-243)
+                const double lam = (gamma / p) * d.tv_alpha;
+                const bool warm = d.tv_warm_start && s->have_duals &&
+                                  fabs(s->dual_weight - lam) <= 1e-12 * fabs(lam);
+                pt::ProfScope ps(&s->ws, PT_PROF_FGP, st);
+                if (!warm) {
+                    PT_CHECK_CUDA(cudaMemsetAsync(s->dp, 0, s->n * 4, st));
+                    PT_CHECK_CUDA(cudaMemsetAsync(s->dq, 0, s->n * 4, st));
+                    if (s->dw) PT_CHECK_CUDA(cudaMemsetAsync(s->dw, 0, s->n * 4, st));
+                }
+                rc = pt::launch_tv_prox(P, s->v, lam, d.tv_inner, d.tv_nonneg, s->dp, s->dq,
+                                        s->dw, xn, s->xhat, s->h, pog, k, s->bad, s->fgp_work, st);
+                s->have_duals = true;
+                s->dual_weight = lam;
+            } else {
+                pt::ProfScope ps(&s->ws, PT_PROF_OTHER, st);
+                rc = pt::launch_identity_prox(s->v, s->xhat, xn, s->h, pog, (int64_t)s->n, k,
+                                              s->bad, st);
+            }
+            if (rc) return rc;
+        }
+        s->cur = 1 - s->cur;
+    }
+    return PT_OK;
+}
+
+int pt_session_set_profiling(pt_session* s, int32_t on)
+{
+    if (!s) { pt::set_error("null session"); return PT_EINVAL; }
+    s->prof.on = on != 0;
+    return PT_OK;
+}
+
+int pt_session_profile(pt_session* s, double* host_ms, int64_t* host_calls)
+{
+    if (!s || !host_ms || !host_calls) { pt::set_error("null argument"); return PT_EINVAL; }
+    s->prof.collect();
+    for (int c = 0; c < PT_PROF_N; ++c) {
+        host_ms[c] = s->prof.ms[c];
+        host_calls[c] = s->prof.calls[c];
+        s->prof.ms[c] = 0.0;
+        s->prof.calls[c] = 0;
+    }
+    return PT_OK;
+}
+
+float* pt_session_x(pt_session* s) { return s ? s->x[s->cur] : nullptr; }
+float* pt_session_h(pt_session* s) { return s ? s->h : nullptr; }
+int64_t* pt_session_bad_iter(pt_session* s) { return s ? s->bad : nullptr; }
+
+float* pt_session_buffer(pt_session* s, int32_t which)
+{
+    if (!s) return nullptr;
+    switch (which) {
+        case 0: return s->snap;
+        case 1: return s->fg;
+        case 2: return s->saga_sum;
+        case 3: return s->saga_table;
+        case 4: return s->dp;
+        case 5: return s->dq;
+        case 6: return s->dw;
+        default: return nullptr;
+    }
+}
+
+int pt_nccl_unique_id(const char* nccl_path, uint8_t* host_out128)
+{
+    NcclApi api;
+    int rc = nccl_load(nccl_path, &api);
+    if (rc) return rc;
+    nccl_uid id;
+    int e = api.get_uid(&id);
+    if (e != 0) { pt::set_error("ncclGetUniqueId failed (%d)", e); return PT_ENCCL; }
+    memcpy(host_out128, id.internal, 128);
+    return PT_OK;
+}
+
+int pt_session_attach_nccl(pt_session* s, const char* nccl_path, const uint8_t* host_id128,
+                           int32_t rank, int32_t world)
+{
+    if (!s || !host_id128 || world < 1 || rank < 0 || rank >= world) { pt::set_error("bad argument"); return PT_EINVAL; }
+    if (world == 1) return PT_OK;
+    int rc = nccl_load(nccl_path, &s->nccl);
+    if (rc) return rc;
+    nccl_uid id;
+    memcpy(id.internal, host_id128, 128);
+    int e = s->nccl.init_rank(&s->comm, world, id, rank);
+    if (e != 0) { pt::set_error("ncclCommInitRank failed (%d)", e); return PT_ENCCL; }
+    s->rank = rank;
+    s->world = world;
+    return build_selections(s);
+}
+
+}  // extern "C"

@@ -1,0 +1,66 @@
+"""Multi-GPU angle-sector data parallelism (one process per GPU).
+
+Rank g of G owns the contiguous sinogram rows of angles
+[g*A/G, (g+1)*A/G) (geometry.angle_sector).  Staggered subsets therefore
+split across all ranks, so every stochastic step is parallel; the per-step
+partial gradient A_i^T r (4 * n_px bytes) and the snapshot full gradient are
+summed by ncclAllReduce inside the native executor on the solver stream; the
+image, control variate, SAGA/SVRG state and the TV prox stay replicated and
+bitwise identical on every rank (deterministic kernels, identical reduced
+bytes).  torch.distributed is only the bootstrap: it ships NCCL's unique id
+from rank 0; the library dlopens the same libnccl torch uses.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import glob
+import os
+
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+
+
+def nccl_library_path() -> str:
+    """The libnccl.so.2 torch is using (nvidia-nccl wheel), else the system one."""
+    try:
+        import nvidia.nccl  # type: ignore
+        base = list(nvidia.nccl.__path__)[0]
+        hits = glob.glob(os.path.join(base, "lib", "libnccl.so*"))
+        if hits:
+            return sorted(hits)[0]
+    except Exception:
+        pass
+    return "libnccl.so.2"
+
+
+def attach(session, rank: int | None = None, world: int | None = None,
+           group=None) -> None:
+    """Attach a native solver session to an NCCL communicator over the
+    torch.distributed process group (the ranks of one node, one GPU each)."""
+    rank = dist.get_rank(group) if rank is None else rank
+    world = dist.get_world_size(group) if world is None else world
+    if world == 1:
+        return
+    path = nccl_library_path().encode()
+    uid = (ctypes.c_uint8 * 128)()
+    if rank == 0:
+        N.check(N.lib().pt_nccl_unique_id(path, uid), "ncclGetUniqueId")
+    payload = [bytes(uid)]
+    dist.broadcast_object_list(payload, src=0, group=group)
+    uid = (ctypes.c_uint8 * 128)(*payload[0])
+    N.check(N.lib().pt_session_attach_nccl(session.handle, path, uid, rank, world),
+            "attach_nccl")
+
+
+def replicas_identical(x: torch.Tensor, group=None) -> bool:
+    """Replica check: every rank's iterate has the same bytes (max == min of a
+    bit-pattern checksum over ranks)."""
+    v = x.contiguous().view(torch.int32).to(torch.int64)
+    chk = torch.stack([v.sum(), (v * torch.arange(v.numel(), device=v.device) % 1000003).sum()])
+    lo, hi = chk.clone(), chk.clone()
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
+    return bool(torch.equal(lo, hi))

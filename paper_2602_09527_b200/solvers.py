@@ -1,0 +1,646 @@
+"""ProxSkip driver with variance-reduced estimators, executed natively.
+
+Drop-in for pkg/src/proxtomo/solvers.py (``SolverConfig``, ``TomoProblem``,
+``IterateState``, ``RunRecord``, ``DivergenceError``, ``proxskip_step``,
+``run``, ``run_ista``, ``run_fista``, ``composite_objective``,
+``default_gamma``, ``fista_gamma``, ``optimal_p``).
+
+Division of labour:
+  * host (this file): the reference's control flow, bit-exact -- the three
+    PCG64 streams from SeedSequence(seed).spawn(3) (:164,174-176), the subset /
+    skip / refresh draws (:198-214,238; estimators.py:149-162), float64 data
+    pass accounting and the log-row schedule (:302-322);
+  * device (csrc/session.cu): the whole iteration -- forward, fused
+    gather + estimator + ProxSkip step, FGP prox with the h update -- for a
+    whole segment of iterations between two log rows, with no host sync.
+Timing: ``wall_seconds`` is device time of the step segments measured with
+CUDA events on the solver stream; metric evaluation at rows is excluded, as
+the reference's perf_counter brackets only the steps (:304-313).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import estimators as est
+from .geometry import SubsetPartition, build_staggered_partition
+from .metrics import psnr as _psnr
+from .metrics import relative_error_sq as _relative_error_sq
+from .metrics import ssim as _ssim
+from .projector import Projector, as_device
+from .regularizers import TvDualState, TvProxConfig, tv_prox, tv_value
+
+RUN_COLUMNS = ("data_passes", "wall_seconds", "rel_err", "psnr", "ssim",
+               "prox_calls", "objective")
+INT64_MAX = 2**63 - 1
+
+
+class DivergenceError(RuntimeError):
+    """Iterate became non-finite; carries the partial run record (:42-51)."""
+
+    def __init__(self, iteration: int, gamma: float, record=None):
+        super().__init__(f"non-finite iterate at iteration {iteration} (gamma={gamma:g})")
+        self.iteration = iteration
+        self.gamma = gamma
+        self.record = record
+
+
+@dataclass(frozen=True)
+class SolverConfig:
+    """One solver run: step size, skipping probability, estimator, budgets (:54-80)."""
+
+    gamma: float
+    skip_probability: float = 1.0
+    n_subsets: int = 1
+    estimator: str = "full"
+    max_data_passes: float = 200.0
+    tolerance: float | None = None
+    time_budget: float | None = None
+    mu: float | None = None
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.gamma <= 0.0:
+            raise ValueError("gamma must be positive")
+        if not 0.0 < self.skip_probability <= 1.0:
+            raise ValueError("skip_probability must be in (0, 1]")
+        if self.estimator not in est.ESTIMATOR_KINDS:
+            raise ValueError(f"unknown estimator {self.estimator!r}")
+        if self.n_subsets < 1:
+            raise ValueError("n_subsets must be >= 1")
+        if self.max_data_passes <= 0.0:
+            raise ValueError("max_data_passes must be positive")
+        if self.time_budget is not None and self.time_budget <= 0.0:
+            raise ValueError("time_budget must be positive")
+
+
+@dataclass
+class TomoProblem:
+    """Measured sinogram, its projector and the regulariser (:83-105).
+
+    ``data`` may be a host array or a CUDA tensor; it is moved to the device
+    (float32) on first use by a solver, so a host sinogram's H2D copy is part
+    of the solve.  Plug-and-play ``denoiser`` problems are out of scope."""
+
+    projector: Projector
+    data: object
+    tv: TvProxConfig | None = None
+    denoiser: object | None = None
+
+    def __post_init__(self):
+        geometry = self.projector.geometry
+        shape = tuple(self.data.shape)
+        nz = getattr(self.projector, "n_slices", 1)
+        want = ((geometry.n_angles, geometry.n_bins) if nz == 1
+                else (geometry.n_angles, nz, geometry.n_bins))
+        if shape != want:
+            raise ValueError(f"data shape {shape} does not match geometry {want}")
+        if self.tv is not None and self.denoiser is not None:
+            raise ValueError("choose either tv or denoiser, not both")
+        self._device_data = None
+
+    def device_data(self) -> torch.Tensor:
+        if self._device_data is None:
+            if isinstance(self.data, torch.Tensor):
+                self._device_data = self.data.to(device="cuda", dtype=torch.float32,
+                                                 non_blocking=True).contiguous()
+            else:
+                self._device_data = as_device(self.data)
+        return self._device_data
+
+
+class _Session:
+    """Owner of a native pt_session (device-resident solver state)."""
+
+    def __init__(self, config: SolverConfig, problem: TomoProblem, x0, stream):
+        if problem.denoiser is not None:
+            raise NotImplementedError("plug-and-play denoisers are out of scope (DESIGN.md)")
+        lib = N.lib()
+        self.plan = problem.projector.plan
+        self.data = problem.device_data()
+        self.stream = stream
+        tv = problem.tv
+        desc = N.SolverDesc(N.EST_CODES[config.estimator], int(config.n_subsets),
+                            float(config.gamma), float(config.skip_probability),
+                            1 if tv is not None else 0, float(tv.alpha) if tv else 0.0,
+                            int(tv.inner_iterations) if tv else 0,
+                            int(bool(tv.warm_start)) if tv else 0,
+                            int(bool(tv.nonneg)) if tv else 0)
+        self.x0 = None if x0 is None else as_device(x0)
+        handle = ctypes.c_void_p()
+        N.check(lib.pt_session_create(self.plan.handle, ctypes.byref(desc), N.ptr(self.data),
+                                      N.ptr(self.x0), ctypes.byref(handle),
+                                      N.stream_handle(stream)), "session")
+        self.handle = handle
+        self.shape = problem.projector.shape
+        self.n = int(np.prod(self.shape))
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None) and N._lib is not None:
+                N._lib.pt_session_destroy(self.handle)
+        except Exception:
+            pass
+
+    def init(self):
+        N.check(N.lib().pt_session_init(self.handle, N.stream_handle(self.stream)), "init")
+
+    def run(self, subs: np.ndarray, thetas: np.ndarray, refresh: np.ndarray, k0: int):
+        n = len(subs)
+        if n == 0:
+            return
+        s = np.ascontiguousarray(subs, dtype=np.int32)
+        t = np.ascontiguousarray(thetas, dtype=np.uint8)
+        r = np.ascontiguousarray(refresh, dtype=np.uint8)
+        N.check(N.lib().pt_session_run(
+            self.handle, n, s.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+            t.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
+            r.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), int(k0),
+            N.stream_handle(self.stream)), "run")
+
+    def view(self, address) -> torch.Tensor:
+        return N.device_view(address, self.shape)
+
+    @property
+    def x(self) -> torch.Tensor:
+        return self.view(N.lib().pt_session_x(self.handle))
+
+    @property
+    def h(self) -> torch.Tensor:
+        return self.view(N.lib().pt_session_h(self.handle))
+
+    def buffer(self, which: int) -> torch.Tensor | None:
+        addr = N.lib().pt_session_buffer(self.handle, which)
+        return None if not addr else self.view(addr)
+
+    def bad_iteration(self) -> int | None:
+        t = N.device_view(N.lib().pt_session_bad_iter(self.handle), (1,), torch.int64)
+        v = int(t.item())
+        return None if v == INT64_MAX else v
+
+
+@dataclass
+class IterateState:
+    """Loop state (:108-125).  x, h and the estimator/prox state live in the
+    native session; the views below alias its device buffers."""
+
+    session: _Session
+    partition: SubsetPartition | None
+    rng_subset: np.random.Generator
+    rng_theta: np.random.Generator
+    rng_refresh: np.random.Generator
+    svrg_period: int | None = None
+    svrg_probability: float | None = None
+    iterations_since_refresh: int = 0
+    k: int = 0
+    data_passes: float = 0.0
+    prox_calls: int = 0
+    denoiser_calls: int = 0
+    work_seconds: float = 0.0
+
+    @property
+    def x(self) -> torch.Tensor:
+        return self.session.x
+
+    @property
+    def h(self) -> torch.Tensor:
+        return self.session.h
+
+    @property
+    def saga(self):
+        t = self.session.buffer(3)
+        if t is None:
+            return None
+        n = self.partition.n_subsets
+        table = N.device_view(N.lib().pt_session_buffer(self.session.handle, 3),
+                              (n,) + tuple(self.session.shape))
+        return est.SagaState(table=table, running_sum=self.session.buffer(2))
+
+    @property
+    def svrg(self):
+        snap = self.session.buffer(0)
+        if snap is None:
+            return None
+        return est.SvrgState(snapshot=snap, full_grad=self.session.buffer(1),
+                             iterations_since_refresh=self.iterations_since_refresh,
+                             refresh_period=self.svrg_period,
+                             refresh_probability=self.svrg_probability)
+
+    @property
+    def tv_warm(self):
+        p = self.session.buffer(4)
+        if p is None or self.prox_calls == 0:
+            return None
+        return TvDualState(p=p, q=self.session.buffer(5), weight=float("nan"),
+                           w=self.session.buffer(6))
+
+
+@dataclass
+class RunRecord:
+    """Per-logging-event rows plus the final iterate (:128-156)."""
+
+    rows: list = field(default_factory=list)
+    iterations: list = field(default_factory=list)
+    image: torch.Tensor | None = None
+
+    def column(self, name: str) -> np.ndarray:
+        j = RUN_COLUMNS.index(name)
+        return np.array([math.nan if r[j] is None else float(r[j]) for r in self.rows])
+
+    @property
+    def final_rel_err(self) -> float:
+        return float(self.rows[-1][RUN_COLUMNS.index("rel_err")]) if self.rows else math.nan
+
+    def to_csv(self, path) -> None:
+        with open(path, "w", encoding="utf-8") as handle:
+            handle.write(",".join(RUN_COLUMNS) + "\n")
+            for row in self.rows:
+                handle.write(",".join("" if v is None else repr(float(v))
+                                      if isinstance(v, float) else str(v)
+                                      for v in row) + "\n")
+
+
+def _init_state(config: SolverConfig, problem: TomoProblem, x0, stream=None) -> IterateState:
+    """solvers.py:159-186: x0 (or zeros), h = 0, three PCG64 streams, the
+    staggered partition, SAGA zeros, SVRG initial snapshot (+1 pass)."""
+    shape = problem.projector.shape
+    if x0 is not None and tuple(x0.shape) != tuple(shape):
+        raise ValueError(f"x0 shape {tuple(x0.shape)} does not match grid {shape}")
+    streams = np.random.SeedSequence(config.seed).spawn(3)
+    partition = None
+    if config.estimator != "full":
+        partition = build_staggered_partition(problem.projector.geometry.n_angles,
+                                              config.n_subsets)
+    stream = stream if stream is not None else torch.cuda.current_stream()
+    session = _Session(config, problem, x0, stream)
+    state = IterateState(session=session, partition=partition,
+                         rng_subset=np.random.default_rng(streams[0]),
+                         rng_theta=np.random.default_rng(streams[1]),
+                         rng_refresh=np.random.default_rng(streams[2]))
+    if config.estimator in ("svrg", "lsvrg"):
+        if config.estimator == "svrg":
+            state.svrg_period = config.n_subsets
+        else:
+            state.svrg_probability = 1.0 / config.n_subsets
+        session.init()
+        state.data_passes += 1.0
+    return state
+
+
+def _draw_one(state: IterateState, config: SolverConfig):
+    """The reference's per-step draws and pass charge (:189-214,238)."""
+    kind = config.estimator
+    refresh = False
+    i = 0
+    if kind == "full":
+        passes = 1.0
+    else:
+        n = state.partition.n_subsets
+        if kind in ("sgd", "saga"):
+            i = int(state.rng_subset.integers(n))
+            passes = 1.0 / n
+        else:
+            passes = 0.0
+            if state.svrg_period is not None:
+                refresh = state.iterations_since_refresh >= state.svrg_period
+            elif state.svrg_probability >= 1.0:
+                refresh = True
+            else:
+                refresh = bool(state.rng_refresh.random() < state.svrg_probability)
+            if refresh:
+                state.iterations_since_refresh = 0
+                passes += 1.0
+            i = int(state.rng_subset.integers(n))
+            state.iterations_since_refresh += 1
+            passes = passes + 2.0 / n
+    p = config.skip_probability
+    theta = True if p >= 1.0 else bool(state.rng_theta.random() < p)
+    return i, theta, refresh, passes
+
+
+def _plan_segment(state: IterateState, config: SolverConfig, last_floor: int,
+                  max_steps: int | None = None):
+    """Steps up to and including the next log event (pass-floor crossing or
+    exhaustion, :314-318).  Subset and skip draws are vectorised -- a vector
+    draw consumes a PCG64 stream exactly like the same number of scalar draws
+    (tests/test_host.py pins this against the reference)."""
+    kind = config.estimator
+    if kind == "lsvrg":
+        subs, thetas, refr = [], [], []
+        passes = state.data_passes
+        while True:
+            i, th, rf, ch = _draw_one(state, config)
+            subs.append(i); thetas.append(th); refr.append(rf)
+            passes += ch
+            exhausted = passes >= config.max_data_passes - 1e-9
+            crossed = math.floor(passes + 1e-12) > last_floor
+            if crossed or exhausted or (max_steps and len(subs) >= max_steps):
+                break
+        return (np.array(subs), np.array(thetas), np.array(refr), passes,
+                exhausted)
+    n = state.partition.n_subsets if state.partition else 1
+    passes = state.data_passes
+    since = state.iterations_since_refresh
+    charges, refr = [], []
+    while True:
+        rf = False
+        if kind == "full":
+            ch = 1.0
+        elif kind in ("sgd", "saga"):
+            ch = 1.0 / n
+        else:
+            c = 0.0
+            if since >= state.svrg_period:
+                rf = True
+                since = 0
+                c += 1.0
+            since += 1
+            ch = c + 2.0 / n
+        passes += ch
+        refr.append(rf)
+        charges.append(ch)
+        exhausted = passes >= config.max_data_passes - 1e-9
+        crossed = math.floor(passes + 1e-12) > last_floor
+        if crossed or exhausted or (max_steps and len(refr) >= max_steps):
+            break
+    L = len(refr)
+    state.iterations_since_refresh = since
+    subs = (state.rng_subset.integers(n, size=L) if kind != "full"
+            else np.zeros(L, dtype=np.int64))
+    p = config.skip_probability
+    thetas = (np.ones(L, dtype=bool) if p >= 1.0 else state.rng_theta.random(L) < p)
+    return subs, thetas, np.array(refr), passes, exhausted
+
+
+def proxskip_step(state: IterateState, config: SolverConfig, problem: TomoProblem) -> IterateState:
+    """One iteration of the skip-capable loop (:230-254), on the device."""
+    i, theta, refresh, passes = _draw_one(state, config)
+    state.session.run(np.array([i]), np.array([theta]), np.array([refresh]), state.k)
+    bad = state.session.bad_iteration()
+    if bad is not None:
+        raise DivergenceError(bad, config.gamma)
+    if theta:
+        state.prox_calls += 1
+    state.k += 1
+    state.data_passes += passes
+    return state
+
+
+def composite_objective(x, problem: TomoProblem) -> float:
+    """0.5 ||A x - b||^2 + alpha TV(x) (:271-277): fused forward + residual +
+    sum of squares on the device, then the TV reduction."""
+    plan = problem.projector.plan
+    xd = as_device(x)
+    y = torch.empty(plan.sino_shape(problem.projector.geometry.n_angles), device="cuda",
+                    dtype=torch.float32)
+    sq = torch.empty(1, device="cuda", dtype=torch.float64)
+    plan.forward_into(xd, y, None, data=problem.device_data(), sumsq=sq)
+    value = 0.5 * float(sq.item())
+    if problem.tv is not None:
+        value += problem.tv.alpha * tv_value(xd)
+    return value
+
+
+def _metrics_row(passes, wall, x, reference, ground_truth, prox_calls, problem,
+                 record_objective):
+    rel = psnr_val = ssim_val = obj = None
+    if reference is not None:
+        rel = _relative_error_sq(x, reference)
+    if ground_truth is not None:
+        gt = as_device(ground_truth)
+        rng_val = float(gt.max() - gt.min())
+        psnr_val = _psnr(x, gt, rng_val if rng_val > 0 else 1.0)
+        ssim_val = _ssim(x, gt)
+    if record_objective:
+        obj = composite_objective(x, problem)
+    return (passes, wall, rel, psnr_val, ssim_val, prox_calls, obj)
+
+
+def run(config: SolverConfig, problem: TomoProblem, x0=None, reference=None,
+        ground_truth=None, record_objective: bool = False, stream=None) -> RunRecord:
+    """Run the skip-capable loop until tolerance or budget exhaustion (:327-336).
+
+    Rows are logged at every data-pass boundary exactly as :280-324; the
+    iterations between two rows are one native segment.  The host syncs only
+    at rows that need a metric (or for a time budget) and at the end."""
+    stream = stream if stream is not None else torch.cuda.current_stream()
+    with torch.cuda.stream(stream):
+        state = _init_state(config, problem, x0, stream)
+        return _run_loop(state, config, problem, reference, ground_truth, record_objective,
+                         stream)
+
+
+def _run_loop(state: IterateState, config, problem, reference, ground_truth,
+              record_objective, stream) -> RunRecord:
+    record = RunRecord()
+    need_metrics = reference is not None or ground_truth is not None or record_objective
+    pending = []  # (row index, event-end index) for deferred wall time
+    events = [torch.cuda.Event(enable_timing=True)]
+    events[0].record(stream)
+
+    def log_row(wall):
+        x = state.x
+        row = _metrics_row(state.data_passes, wall, x, reference, ground_truth,
+                           state.prox_calls, problem, record_objective)
+        record.rows.append(row)
+        record.iterations.append(state.k)
+        return row
+
+    def satisfied(row):
+        rel = row[RUN_COLUMNS.index("rel_err")]
+        return config.tolerance is not None and rel is not None and rel < config.tolerance
+
+    row = log_row(0.0)
+    if satisfied(row):
+        record.image = state.x.clone()
+        return record
+    last_floor = math.floor(state.data_passes + 1e-12)
+    budget = config.time_budget
+    while True:
+        subs, thetas, refr, passes, exhausted = _plan_segment(
+            state, config, last_floor, max_steps=1 if budget is not None else None)
+        state.session.run(subs, thetas, refr, state.k)
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        events.append(ev)
+        state.k += len(subs)
+        state.prox_calls += int(np.count_nonzero(thetas))
+        state.data_passes = passes
+        if budget is not None or need_metrics:
+            ev.synchronize()
+            state.work_seconds = (state.work_seconds
+                                  + events[-2].elapsed_time(events[-1]) / 1e3)
+            if budget is not None:
+                exhausted = exhausted or state.work_seconds >= budget
+            bad = state.session.bad_iteration()
+            if bad is not None:
+                raise _diverged(bad, config, record)
+        crossed = math.floor(state.data_passes + 1e-12) > last_floor
+        if crossed or exhausted:
+            last_floor = math.floor(state.data_passes + 1e-12)
+            if need_metrics or budget is not None:
+                row = log_row(state.work_seconds)
+            else:
+                row = (state.data_passes, None, None, None, None, state.prox_calls, None)
+                record.rows.append(row)
+                record.iterations.append(state.k)
+                pending.append((len(record.rows) - 1, len(events) - 1))
+            if satisfied(row) or exhausted:
+                break
+    if pending:
+        # wall_seconds of deferred rows: cumulative device time of segments
+        stream.synchronize()
+        cum = [0.0]
+        for j in range(1, len(events)):
+            cum.append(cum[-1] + events[j - 1].elapsed_time(events[j]) / 1e3)
+        for ri, ei in pending:
+            r = record.rows[ri]
+            record.rows[ri] = (r[0], cum[ei]) + tuple(r[2:])
+        state.work_seconds = cum[-1]
+    bad = state.session.bad_iteration()
+    if bad is not None:
+        raise _diverged(bad, config, record)
+    record.image = state.x.clone()
+    record.state = state
+    return record
+
+
+def _diverged(bad: int, config: SolverConfig, record: RunRecord) -> DivergenceError:
+    keep = [j for j, it in enumerate(record.iterations) if it <= bad]
+    record.rows = [record.rows[j] for j in keep]
+    record.iterations = [record.iterations[j] for j in keep]
+    record.image = None
+    return DivergenceError(bad, config.gamma, record)
+
+
+# ----------------------------------------------------------------------------
+# Deterministic reference solvers (solvers.py:339-392) built from the same
+# native operators.  They keep the reference's loop and logging semantics.
+# ----------------------------------------------------------------------------
+
+def _apply_prox_simple(target, tau, problem, warm):
+    if problem.tv is not None:
+        w = warm if problem.tv.warm_start else None
+        return tv_prox(target, tau, problem.tv, w)
+    if problem.denoiser is not None:
+        raise NotImplementedError("plug-and-play denoisers are out of scope (DESIGN.md)")
+    return target, warm
+
+
+def _full_loop(config, problem, x0, reference, ground_truth, record_objective, step_fn):
+    """_run_loop semantics (:280-324) for the full-gradient solvers (1 pass/iteration)."""
+    record = RunRecord()
+    shape = problem.projector.shape
+    x = torch.zeros(shape, device="cuda") if x0 is None else as_device(x0).clone()
+    ctx = {"x": x, "warm": None, "k": 0, "passes": 0.0, "prox": 0, "work": 0.0}
+
+    def log_row():
+        row = _metrics_row(ctx["passes"], ctx["work"], ctx["x"], reference, ground_truth,
+                           ctx["prox"], problem, record_objective)
+        record.rows.append(row)
+        record.iterations.append(ctx["k"])
+        return row
+
+    def satisfied(row):
+        rel = row[2]
+        return config.tolerance is not None and rel is not None and rel < config.tolerance
+
+    row = log_row()
+    if satisfied(row):
+        record.image = ctx["x"].clone()
+        return record
+    last_floor = math.floor(ctx["passes"] + 1e-12)
+    while True:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        step_fn(ctx)
+        torch.cuda.synchronize()
+        ctx["work"] += time.perf_counter() - t0
+        if not bool(torch.isfinite(ctx["x"]).all()):
+            record.image = None
+            raise DivergenceError(ctx["k"] - 1, config.gamma, record)
+        exhausted = ctx["passes"] >= config.max_data_passes - 1e-9
+        if config.time_budget is not None:
+            exhausted = exhausted or ctx["work"] >= config.time_budget
+        crossed = math.floor(ctx["passes"] + 1e-12) > last_floor
+        if crossed or exhausted:
+            last_floor = math.floor(ctx["passes"] + 1e-12)
+            row = log_row()
+            if satisfied(row) or exhausted:
+                break
+    record.image = ctx["x"].clone()
+    return record
+
+
+def run_ista(config: SolverConfig, problem: TomoProblem, x0=None, reference=None,
+             ground_truth=None, record_objective: bool = False) -> RunRecord:
+    """x+ = prox_gamma(x - gamma grad f(x)) (:339-364)."""
+    gamma = config.gamma
+
+    def step(ctx):
+        grad = est.full_gradient(ctx["x"], problem.projector, problem.device_data())
+        ctx["x"], ctx["warm"] = _apply_prox_simple(ctx["x"] - gamma * grad, gamma, problem,
+                                                   ctx["warm"])
+        ctx["prox"] += 1
+        ctx["k"] += 1
+        ctx["passes"] += 1.0
+
+    return _full_loop(config, problem, x0, reference, ground_truth, record_objective, step)
+
+
+def run_fista(config: SolverConfig, problem: TomoProblem, x0=None, reference=None,
+              ground_truth=None, record_objective: bool = False) -> RunRecord:
+    """Accelerated variant, prox every iteration (:367-392)."""
+    gamma = config.gamma
+    aux = {"y": None, "t": 1.0}
+
+    def step(ctx):
+        if aux["y"] is None:
+            aux["y"] = ctx["x"].clone()
+        grad = est.full_gradient(aux["y"], problem.projector, problem.device_data())
+        x_next, ctx["warm"] = _apply_prox_simple(aux["y"] - gamma * grad, gamma, problem,
+                                                 ctx["warm"])
+        ctx["prox"] += 1
+        t_next = (1.0 + math.sqrt(1.0 + 4.0 * aux["t"] * aux["t"])) / 2.0
+        aux["y"] = x_next + ((aux["t"] - 1.0) / t_next) * (x_next - ctx["x"])
+        aux["t"] = t_next
+        ctx["x"] = x_next
+        ctx["k"] += 1
+        ctx["passes"] += 1.0
+
+    return _full_loop(config, problem, x0, reference, ground_truth, record_objective, step)
+
+
+def optimal_p(mu: float, lipschitz: float) -> float:
+    """sqrt(mu / L) clamped into (0, 1] (:458-465)."""
+    if mu <= 0.0 or lipschitz <= 0.0:
+        raise ValueError("mu and L must be positive")
+    if mu > lipschitz:
+        raise ValueError("mu cannot exceed L")
+    return min(1.0, math.sqrt(mu / lipschitz))
+
+
+def default_gamma(estimator: str, lipschitz: float) -> float:
+    """1.99/L full, 1/(3L) saga, 1/L otherwise (:468-479)."""
+    if lipschitz <= 0.0:
+        raise ValueError("L must be positive")
+    if estimator == "full":
+        return 1.99 / lipschitz
+    if estimator == "saga":
+        return 1.0 / (3.0 * lipschitz)
+    if estimator in ("sgd", "svrg", "lsvrg"):
+        return 1.0 / lipschitz
+    raise ValueError(f"unknown estimator {estimator!r}")
+
+
+def fista_gamma(lipschitz: float) -> float:
+    if lipschitz <= 0.0:
+        raise ValueError("L must be positive")
+    return 1.0 / lipschitz

@@ -1,0 +1,94 @@
+"""GPU parity of the temporally blocked FGP TV prox (regularizers.py:90-133).
+
+float32 on the device vs the reference's float64: tolerance 1e-4 relative L2
+(the north_star's iterate tolerance); the blocked kernel is also checked
+against an unblocked run of itself (T = 1 per launch is what the oracle
+does) through many launch splits."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_l2
+from paper_2602_09527_b200 import TvProxConfig, nonneg_prox, tv_prox, tv_value
+
+pytestmark = pytest.mark.gpu
+
+
+def cpu(t):
+    return t.detach().double().cpu().numpy()
+
+
+@pytest.mark.parametrize("nn", [0, 1])
+def test_fgp_matches_reference_goldens(units, nn):
+    u = units["fgp_u"]
+    cfg = TvProxConfig(alpha=0.5, inner_iterations=37, nonneg=bool(nn))
+    x, st = tv_prox(u, 0.8, cfg)
+    assert rel_l2(cpu(x), units[f"fgp_x_nn{nn}"]) <= 1e-5
+    assert rel_l2(cpu(st.p), units[f"fgp_p_nn{nn}"]) <= 1e-4
+    xw, _ = tv_prox(u, 0.8, cfg, warm=st)
+    assert rel_l2(cpu(xw), units[f"fgp_xw_nn{nn}"]) <= 1e-5
+
+
+def test_fgp_config_size_case(units):
+    v = units["fgp128_v"]
+    cfg = TvProxConfig(alpha=0.02, inner_iterations=50)
+    x, st = tv_prox(v, 1.0, cfg)
+    assert rel_l2(cpu(x), units["fgp128_x"]) <= 1e-5
+    x2, _ = tv_prox(v, 1.0, cfg, warm=st)
+    assert rel_l2(cpu(x2), units["fgp128_x_warm"]) <= 1e-5
+
+
+@pytest.mark.parametrize("shape,inner", [((512, 512), 100), ((300, 701), 13), ((2048, 2048), 100),
+                                         ((7, 5), 9)])
+def test_fgp_matches_oracle_large_and_ragged(oracle, shape, inner):
+    rng = np.random.default_rng(sum(shape))
+    v = rng.standard_normal(shape).cumsum(axis=1) * 0.05 + 0.3
+    lam = 0.05
+    xo, sto = oracle.tv_prox(v, 1.0, lam, inner, True)
+    x, st = tv_prox(v, 1.0, TvProxConfig(alpha=lam, inner_iterations=inner))
+    assert rel_l2(cpu(x), xo) <= 1e-5
+    assert rel_l2(cpu(st.p), sto.p) <= 1e-4
+    assert rel_l2(xo, v) > 1e-3  # the prox does something
+
+
+def test_fgp_3d_matches_oracle(oracle):
+    rng = np.random.default_rng(3)
+    v = rng.standard_normal((9, 20, 24))
+    for nn in (False, True):
+        xo, _ = oracle.tv_prox(v, 1.0, 0.3, 25, nn)
+        x, st = tv_prox(v, 1.0, TvProxConfig(alpha=0.3, inner_iterations=25, nonneg=nn))
+        assert rel_l2(cpu(x), xo) <= 1e-5
+        assert st.w is not None
+
+
+def test_fgp_properties():
+    rng = np.random.default_rng(5)
+    u = rng.standard_normal((40, 40))
+    for inner in (1, 2, 7, 15):
+        _, st = tv_prox(u, 1.0, TvProxConfig(alpha=0.8, inner_iterations=inner))
+        assert float((st.p ** 2 + st.q ** 2).max()) <= 1.0 + 1e-5
+    a, _ = tv_prox(u, 0.7, TvProxConfig(alpha=0.3, inner_iterations=40))
+    b, _ = tv_prox(u, 1.0, TvProxConfig(alpha=0.7 * 0.3, inner_iterations=40))
+    assert torch.equal(a, b)  # scaling law (reference asserts bitwise)
+    c = np.full((9, 9), 3.0)
+    out, _ = tv_prox(c, 1.0, TvProxConfig(alpha=10.0, inner_iterations=60))
+    assert np.allclose(cpu(out), c, atol=1e-6)
+    with pytest.raises(ValueError):
+        tv_prox(np.zeros((3, 3)), 0.0, TvProxConfig(alpha=1.0))
+    cold, st = tv_prox(u, 1.0, TvProxConfig(alpha=0.5, inner_iterations=15))
+    warm, _ = tv_prox(u, 1.0, TvProxConfig(alpha=0.5, inner_iterations=15), warm=st)
+    assert not torch.equal(cold, warm)
+    reset, _ = tv_prox(u, 2.0, TvProxConfig(alpha=0.5, inner_iterations=15), warm=st)
+    cold2, _ = tv_prox(u, 2.0, TvProxConfig(alpha=0.5, inner_iterations=15))
+    assert torch.equal(reset, cold2)
+
+
+def test_tv_value_and_nonneg(oracle):
+    rng = np.random.default_rng(0)
+    img = rng.standard_normal((33, 47))
+    assert tv_value(img) == pytest.approx(oracle.tv_value(img), rel=1e-6)
+    vol = rng.standard_normal((4, 8, 9))
+    assert tv_value(vol) == pytest.approx(oracle.tv_value(vol), rel=1e-6)
+    assert tv_value(np.full((6, 6), 2.5)) == 0.0
+    assert np.array_equal(cpu(nonneg_prox(np.array([-1.0, 2.0, 0.0]))), [0.0, 2.0, 0.0])

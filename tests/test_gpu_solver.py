@@ -1,0 +1,167 @@
+"""End-to-end parity of the native ProxSkip executor (csrc/session.cu).
+
+* subset / skip / refresh sequences: bit-exact (prox-call counts, rows,
+  iterations identical to the reference's);
+* final iterate and objective after K epochs: relative L2 <= 1e-4 against
+  the reference's own runs (tests/golden) -- config 0 whole, and the 16^2
+  problem for every estimator."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_l2
+from paper_2602_09527_b200 import (DivergenceError, ParallelGeometry, Projector, SolverConfig,
+                                   TomoProblem, TvProxConfig, composite_objective, default_gamma,
+                                   proxskip_step, run, run_fista, run_ista)
+from paper_2602_09527_b200 import estimators as E
+from paper_2602_09527_b200 import problems
+from paper_2602_09527_b200.solvers import _init_state
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+def cpu(t):
+    return t.detach().double().cpu().numpy()
+
+
+def small_problem(small_runs):
+    g = ParallelGeometry.uniform(10, 23)
+    proj = Projector(g, 16, 16)
+    tv = TvProxConfig(alpha=0.5, inner_iterations=10)
+    return TomoProblem(proj, small_runs["small_data"], tv=tv), float(small_runs["small_L"])
+
+
+@pytest.mark.parametrize("est,p,passes,seed", [("full", 1.0, 20, 1), ("sgd", 0.4, 30, 17),
+                                               ("saga", 0.4, 30, 3), ("svrg", 0.4, 30, 23),
+                                               ("lsvrg", 0.5, 30, 4), ("svrg", 1.0, 15, 5)])
+def test_small_runs_match_reference(small_runs, est, p, passes, seed):
+    problem, lip = small_problem(small_runs)
+    cfg = SolverConfig(gamma=default_gamma(est, lip), skip_probability=p,
+                       n_subsets=5 if est != "full" else 1, estimator=est,
+                       max_data_passes=passes, seed=seed)
+    rec = run(cfg, problem, record_objective=True)
+    tag = f"small_{est}_p{p}_s{seed}"
+    assert rel_l2(cpu(rec.image), small_runs[tag + "_image"]) <= TOL
+    assert np.array_equal(rec.column("data_passes"), small_runs[tag + "_passes"])
+    assert np.array_equal(rec.column("prox_calls"), small_runs[tag + "_prox"])
+    assert rec.iterations == list(small_runs[tag + "_iters"])
+    obj = rec.column("objective")
+    assert np.allclose(obj, small_runs[tag + "_obj"], rtol=TOL)
+
+
+def test_config0_whole_run_matches_reference(c0_ref):
+    """BASELINE config 0: 128^2, 180x192, SVRG N=10, p=0.1, FGP 50, 50 epochs."""
+    cfg = problems.CONFIGS["c0"]
+    g = ParallelGeometry.uniform(cfg.n_angles, cfg.n_bins)
+    proj = Projector(g, cfg.size, cfg.size)
+    tv = TvProxConfig(alpha=float(c0_ref["c0_alpha"]), inner_iterations=cfg.fgp_inner)
+    problem = TomoProblem(proj, c0_ref["c0_b"], tv=tv)
+    scfg = SolverConfig(gamma=float(c0_ref["c0_gamma"]), skip_probability=cfg.p,
+                        n_subsets=cfg.n_subsets, estimator=cfg.estimator,
+                        max_data_passes=cfg.max_data_passes, seed=cfg.solver_seed)
+    rec = run(scfg, problem, record_objective=True)
+    assert rel_l2(cpu(rec.image), c0_ref["c0_image"]) <= TOL
+    assert np.array_equal(rec.column("data_passes"), c0_ref["c0_passes"])
+    assert np.array_equal(rec.column("prox_calls"), c0_ref["c0_prox"])
+    assert rec.iterations == list(c0_ref["c0_iters"])
+    assert np.allclose(rec.column("objective"), c0_ref["c0_obj"], rtol=TOL)
+    walls = rec.column("wall_seconds")
+    assert np.all(np.diff(walls) >= 0) and walls[-1] > 0
+
+
+def test_config0_setup_constants_match_reference(c0_ref):
+    """L (50 power iterations, seed 0) and alpha from the device operator."""
+    cfg = problems.CONFIGS["c0"]
+    g = ParallelGeometry.uniform(cfg.n_angles, cfg.n_bins)
+    proj = Projector(g, cfg.size, cfg.size)
+    assert proj.norm_sq(50, 0) == pytest.approx(float(c0_ref["c0_L"]), rel=1e-5)
+    atb = proj.adjoint(c0_ref["c0_b"])
+    alpha = problems.alpha_from_backprojection(float(atb.abs().max()), cfg.n_pixels)
+    assert alpha == pytest.approx(float(c0_ref["c0_alpha"]), rel=1e-5)
+
+
+def test_proxskip_step_api_matches_run(small_runs):
+    problem, lip = small_problem(small_runs)
+    cfg = SolverConfig(gamma=1.0 / lip, skip_probability=0.4, n_subsets=5, estimator="svrg",
+                       max_data_passes=1e9, seed=23)
+    st = _init_state(cfg, problem, None)
+    for _ in range(40):
+        proxskip_step(st, cfg, problem)
+    cfg2 = SolverConfig(gamma=1.0 / lip, skip_probability=0.4, n_subsets=5, estimator="svrg",
+                        max_data_passes=st.data_passes, seed=23)
+    rec = run(cfg2, problem)
+    assert rec.iterations[-1] == st.k == 40
+    assert torch.equal(rec.image, st.x)
+
+
+def test_estimator_api_against_oracle(oracle):
+    g = ParallelGeometry.uniform(6, 7)
+    proj = Projector(g, 4, 4)
+    oproj = oracle.OracleProjector(g, 4, 4)
+    rng = np.random.default_rng(0)
+    x, data = rng.standard_normal((4, 4)), rng.standard_normal((6, 7))
+    full_ref = oproj.adjoint(oproj.forward(x) - data)
+    assert rel_l2(cpu(E.full_gradient(x, proj, data)), full_ref) <= 1e-5
+    from paper_2602_09527_b200 import build_staggered_partition
+    for n in (2, 3, 6):
+        part = build_staggered_partition(6, n)
+        sgd = np.mean([cpu(E.sgd_estimate(x, i, proj, data, part)) for i in range(n)], axis=0)
+        assert rel_l2(sgd, full_ref) <= 1e-5
+        st = E.init_svrg_state(rng.standard_normal((4, 4)), proj, data, refresh_period=n)
+        svrg = np.mean([cpu(E.svrg_estimate(x, i, st, proj, data, part)) for i in range(n)], axis=0)
+        assert rel_l2(svrg, full_ref) <= 1e-4
+        table = rng.standard_normal((n, 4, 4))
+        saga = np.mean([cpu(E.saga_estimate_update(
+            x, i, E.SagaState(torch.tensor(table, device="cuda", dtype=torch.float32),
+                              torch.tensor(table.sum(0), device="cuda", dtype=torch.float32)),
+            proj, data, part)) for i in range(n)], axis=0)
+        assert rel_l2(saga, full_ref) <= 1e-4
+
+
+def test_divergence_raises_with_partial_record():
+    g = ParallelGeometry((0.0,), 1, bin_spacing=1.0, pixel_size=1.0)
+    problem = TomoProblem(Projector(g, 1, 1), np.array([[1.0]]))
+    cfg = SolverConfig(gamma=1e6, max_data_passes=2000, seed=0)
+    with pytest.raises(DivergenceError) as info:
+        run(cfg, problem)
+    assert info.value.gamma == 1e6
+    assert info.value.iteration > 0
+    assert info.value.record is not None and len(info.value.record.rows) >= 1
+
+
+def test_scalar_contraction_any_p():
+    """f = x^2/2, g = 0: x <- (1 - gamma) x exactly (reference test_solvers.py:23-34)."""
+    g = ParallelGeometry((0.0,), 1, bin_spacing=1.0, pixel_size=1.0)
+    problem = TomoProblem(Projector(g, 1, 1), np.array([[0.0]]))
+    for p in (1.0, 0.4, 0.05):
+        cfg = SolverConfig(gamma=0.3, skip_probability=p, max_data_passes=1e9, seed=5)
+        st = _init_state(cfg, problem, np.array([[2.0]]))
+        value = 2.0
+        for _ in range(40):
+            proxskip_step(st, cfg, problem)
+            value *= 0.7
+            assert float(st.x[0, 0]) == pytest.approx(value, rel=1e-5)
+
+
+def test_ista_fista(small_runs):
+    problem, lip = small_problem(small_runs)
+    cfg = SolverConfig(gamma=1.0 / lip, max_data_passes=1, seed=0)
+    a = run_fista(cfg, problem)
+    b = run_ista(cfg, problem)
+    assert torch.equal(a.image, b.image)
+    cfg = SolverConfig(gamma=1.99 / lip, skip_probability=1.0, estimator="full",
+                       max_data_passes=20, seed=1)
+    ista = run_ista(cfg, problem)
+    assert rel_l2(cpu(ista.image), small_runs["small_full_p1.0_s1_image"]) <= TOL
+
+
+def test_objective(small_runs):
+    problem, lip = small_problem(small_runs)
+    x = np.random.default_rng(1).random((16, 16))
+    from oracle.solver import objective
+    import oracle as O
+    oproj = O.OracleProjector(ParallelGeometry.uniform(10, 23), 16, 16)
+    want = objective(oproj, small_runs["small_data"], x, 0.5)
+    assert composite_objective(x, problem) == pytest.approx(want, rel=1e-5)
