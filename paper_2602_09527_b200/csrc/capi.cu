@@ -7,6 +7,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <vector>
 
@@ -31,8 +32,10 @@ int workspace_alloc(const pt_plan* plan, Workspace* ws)
         (size_t)plan->n_bands * plan->Z * plan->B * (size_t)plan->max_angles_per_launch;
     size_t chunks = (plan->A + plan->max_angles_per_launch - 1) / plan->max_angles_per_launch;
     ws->red_doubles = ((size_t)plan->A * plan->Z * plan->B + 255) / 256 + chunks + 16;
+    ws->image_floats = (size_t)plan->Z * plan->H * plan->W;
     PT_CHECK_CUDA(cudaMalloc(&ws->partial, ws->partial_floats * sizeof(float)));
     PT_CHECK_CUDA(cudaMalloc(&ws->red, ws->red_doubles * sizeof(double)));
+    PT_CHECK_CUDA(cudaMalloc(&ws->image, ws->image_floats * sizeof(float)));
     return PT_OK;
 }
 
@@ -40,8 +43,10 @@ void workspace_free(Workspace* ws)
 {
     if (ws->partial) cudaFree(ws->partial);
     if (ws->red) cudaFree(ws->red);
+    if (ws->image) cudaFree(ws->image);
     ws->partial = nullptr;
     ws->red = nullptr;
+    ws->image = nullptr;
 }
 
 static AngleTab make_tab(double theta, int H, int W, int B, double ds, double h)
@@ -62,6 +67,8 @@ static AngleTab make_tab(double theta, int H, int W, int B, double ds, double h)
         t.a0 = -cB * t.sigma + cW * (c / s) + cH;
         t.step_len = (float)(h / fabs(s));
     }
+    t.isig = 1.0 / t.sigma;
+    t.im = fabs(t.m) < 1e-300 ? 0.0 : 1.0 / t.m;
     return t;
 }
 
@@ -148,8 +155,15 @@ int pt_plan_create(const pt_geometry_desc* d, pt_plan** out)
     p->cand_half = std::max(1, (int)ceil(1.0 / min_abs_sigma - 1e-12));
     p->gather_slot = (int)ceil(31 * max_br + 63 * max_bc) + 2 * p->cand_half + 8;
     const int mn = std::min(p->H, p->W);
-    p->fwd_ty = mn >= 512 ? 64 : (mn >= 128 ? 32 : 16);
-    p->fwd_tx = mn >= 512 ? 256 : (mn >= 128 ? 128 : 64);
+    // forward tile configuration (band height TY x lane tile TX), see projector.cu
+    static const int cfg_env = [] {
+        const char* e = getenv("PT_FWD_CFG");
+        return e ? atoi(e) : -1;
+    }();
+    if (mn >= 512) p->fwd_cfg = cfg_env >= 0 ? cfg_env : 3;
+    else if (mn >= 128) p->fwd_cfg = 100;
+    else p->fwd_cfg = 101;
+    pt::forward_config(p->fwd_cfg, &p->fwd_ty, &p->fwd_tx);
     p->n_bands = (std::max(p->H, p->W) + p->fwd_ty - 1) / p->fwd_ty;
     const size_t per_angle = (size_t)p->n_bands * p->Z * p->B;
     const size_t cap_floats = (size_t)1 << 28;  // 1 GiB of band partials

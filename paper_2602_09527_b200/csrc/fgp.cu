@@ -48,14 +48,77 @@ struct FgpArgs {
     long long* bad_iter;
 };
 
-template <int RW, int RH, int STRIP>
-__global__ void __launch_bounds__(RW*(RH / STRIP)) fgp2d_kernel(FgpArgs P)
+// One FGP inner iteration on the register strips.  EDGE = the region touches
+// the image border (masks needed); interior regions skip every boundary test.
+template <int RW, int RH, int STRIP, bool EDGE>
+__device__ __forceinline__ void fgp2d_iteration(
+    float (&v)[STRIP], float (&p)[STRIP], float (&q)[STRIP], float (&r)[STRIP],
+    float (&s)[STRIP], float (&u)[STRIP], float (*S_s)[RW + 1], float (*S_u)[RW + 1],
+    float (*S_r)[RW], float (*S_ut)[RW], int tx, int ty, int i0, int H, bool not_last_col,
+    unsigned in_mask, float lam, float eta, float beta, int nonneg)
 {
     constexpr int NS = RH / STRIP;
+    const int row0 = ty * STRIP;
+#pragma unroll
+    for (int k = 0; k < STRIP; ++k) S_s[row0 + k][tx] = s[k];
+    S_r[ty][tx] = r[STRIP - 1];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < STRIP; ++k) {
+        const float r_up = k ? r[k - 1] : (ty ? S_r[ty - 1][tx] : 0.f);
+        const float s_left = tx ? S_s[row0 + k][tx - 1] : 0.f;
+        // _diff_adjoint (regularizers.py:70-76), numpy statement order
+        float o;
+        if (EDGE) {
+            const int gi = i0 + row0 + k;
+            o = (gi < H - 1) ? -r[k] : 0.f;
+            o += r_up;
+            o = not_last_col ? o - s[k] : o;
+        } else {
+            o = -r[k];
+            o += r_up;
+            o = o - s[k];
+        }
+        o += s_left;
+        float uu = v[k] - lam * o;
+        if (nonneg) uu = (uu < 0.f) ? 0.f : uu;
+        if (EDGE) uu = ((in_mask >> k) & 1u) ? uu : 0.f;
+        u[k] = uu;
+        S_u[row0 + k][tx] = uu;
+    }
+    S_ut[ty][tx] = u[0];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < STRIP; ++k) {
+        const float u_down = (k < STRIP - 1) ? u[k + 1] : (ty < NS - 1 ? S_ut[ty + 1][tx] : 0.f);
+        const float u_right = (tx < RW - 1) ? S_u[row0 + k][tx + 1] : 0.f;
+        float gv = u_down - u[k], gh = u_right - u[k];
+        if (EDGE) {
+            const int gi = i0 + row0 + k;
+            gv = (gi < H - 1) ? gv : 0.f;
+            gh = not_last_col ? gh : 0.f;
+        }
+        const float ph = r[k] + eta * gv;
+        const float qh = s[k] + eta * gh;
+        const float n2 = ph * ph + qh * qh;
+        const float inv = (n2 > 1.f) ? rsqrtf(n2) : 1.f;
+        const float pn = ph * inv, qn = qh * inv;
+        if (!EDGE || ((in_mask >> k) & 1u)) {
+            r[k] = pn + beta * (pn - p[k]);
+            s[k] = qn + beta * (qn - q[k]);
+            p[k] = pn;
+            q[k] = qn;
+        }
+    }
+}
+
+template <int RW, int RH, int STRIP>
+__global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
+{
     __shared__ float S_s[RH][RW + 1];
     __shared__ float S_u[RH][RW + 1];
-    __shared__ float S_r[NS][RW];
-    __shared__ float S_ut[NS][RW];
+    __shared__ float S_r[RH / STRIP][RW];
+    __shared__ float S_ut[RH / STRIP][RW];
 
     const int tid = threadIdx.x;
     const int tx = tid % RW;
@@ -67,6 +130,8 @@ __global__ void __launch_bounds__(RW*(RH / STRIP)) fgp2d_kernel(FgpArgs P)
     const int row0 = ty * STRIP;
     const bool col_in = (gj >= 0 && gj < P.W);
     const bool not_last_col = (gj < P.W - 1);
+    // the whole region, and one point beyond it, strictly inside the image
+    const bool edge = !(i0 >= 0 && j0 >= 0 && i0 + RH < P.H && j0 + RW < P.W);
 
     float v[STRIP], p[STRIP], q[STRIP], r[STRIP], s[STRIP], u[STRIP];
     unsigned in_mask = 0;
@@ -83,53 +148,19 @@ __global__ void __launch_bounds__(RW*(RH / STRIP)) fgp2d_kernel(FgpArgs P)
         s[k] = in ? (P.s_in ? P.s_in[o] : q[k]) : 0.f;
         u[k] = 0.f;
     }
-    const float lam = P.lam, eta = P.eta;
-
     for (int it = 0; it < P.n_iter; ++it) {
-        const float beta = P.beta[it];
-#pragma unroll
-        for (int k = 0; k < STRIP; ++k) S_s[row0 + k][tx] = s[k];
-        S_r[ty][tx] = r[STRIP - 1];
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < STRIP; ++k) {
-            const int gi = i0 + row0 + k;
-            const float r_up = k ? r[k - 1] : (ty ? S_r[ty - 1][tx] : 0.f);
-            const float s_left = tx ? S_s[row0 + k][tx - 1] : 0.f;
-            // _diff_adjoint (regularizers.py:70-76), numpy statement order
-            float o = (gi < P.H - 1) ? -r[k] : 0.f;
-            o += r_up;
-            o = not_last_col ? o - s[k] : o;
-            o += s_left;
-            float uu = v[k] - lam * o;
-            if (P.nonneg) uu = (uu < 0.f) ? 0.f : uu;
-            u[k] = ((in_mask >> k) & 1u) ? uu : 0.f;
-            S_u[row0 + k][tx] = u[k];
-        }
-        S_ut[ty][tx] = u[0];
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < STRIP; ++k) {
-            const int gi = i0 + row0 + k;
-            const float u_down = (k < STRIP - 1) ? u[k + 1] : (ty < NS - 1 ? S_ut[ty + 1][tx] : 0.f);
-            const float u_right = (tx < RW - 1) ? S_u[row0 + k][tx + 1] : 0.f;
-            const float gv = (gi < P.H - 1) ? u_down - u[k] : 0.f;
-            const float gh = not_last_col ? u_right - u[k] : 0.f;
-            const float ph = r[k] + eta * gv;
-            const float qh = s[k] + eta * gh;
-            const float n2 = ph * ph + qh * qh;
-            const float inv = (n2 > 1.f) ? rsqrtf(n2) : 1.f;
-            const float pn = ph * inv, qn = qh * inv;
-            if ((in_mask >> k) & 1u) {
-                r[k] = pn + beta * (pn - p[k]);
-                s[k] = qn + beta * (qn - q[k]);
-                p[k] = pn;
-                q[k] = qn;
-            }
-        }
+        if (edge)
+            fgp2d_iteration<RW, RH, STRIP, true>(v, p, q, r, s, u, S_s, S_u, S_r, S_ut, tx, ty, i0,
+                                                 P.H, not_last_col, in_mask, P.lam, P.eta,
+                                                 P.beta[it], P.nonneg);
+        else
+            fgp2d_iteration<RW, RH, STRIP, false>(v, p, q, r, s, u, S_s, S_u, S_r, S_ut, tx, ty, i0,
+                                                  P.H, not_last_col, in_mask, P.lam, P.eta,
+                                                  P.beta[it], P.nonneg);
     }
 
     const bool col_inner = tx >= P.halo && tx < RW - P.halo;
+    const float lam = P.lam;
     if (P.final_) {
         // x = max(v - lam D^T(p, q), 0), then the ProxSkip h update
         __syncthreads();
@@ -387,8 +418,8 @@ int launch_tv_prox(pt_plan* plan, const float* v, double lam, int inner, int non
         return launch_fgp3d(plan, v, lam, inner, nonneg, p, q, w, x_out, xhat, h, p_over_gamma,
                             iteration, bad_iter, work, st);
     if (std::min(plan->H, plan->W) >= 256)
-        return run_fgp2d<64, 64, 16>(plan, v, lam, inner, nonneg, p, q, x_out, xhat, h,
-                                     p_over_gamma, iteration, bad_iter, work, st, 6);
+        return run_fgp2d<64, 64, 8>(plan, v, lam, inner, nonneg, p, q, x_out, xhat, h,
+                                    p_over_gamma, iteration, bad_iter, work, st, 6);
     return run_fgp2d<32, 32, 8>(plan, v, lam, inner, nonneg, p, q, x_out, xhat, h,
                                 p_over_gamma, iteration, bad_iter, work, st, 3);
 }

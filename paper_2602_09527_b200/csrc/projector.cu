@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "pt_internal.cuh"
 
@@ -19,21 +20,118 @@ namespace pt {
 static constexpr float kMagic = 12582912.0f;
 static constexpr int kMagicBits = 0x4B400000;
 
+// Packed float32x2 arithmetic (sm_100a FFMA2 / FADD2): two Joseph samples or
+// two pixels per instruction, halving the FP issue slots of the hot loops.
+struct f2 {
+    unsigned long long v;
+};
+__device__ __forceinline__ f2 pk(float a, float b)
+{
+    f2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk(f2 r, float& a, float& b)
+{
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r.v));
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c)
+{
+    f2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+    return r;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b)
+{
+    f2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ f2 add2_rm(f2 a, f2 b)
+{
+    f2 r;
+    asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b)
+{
+    f2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ uint32_t smem_u32(const void* p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ float lds(uint32_t a)
+{
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+// (x[a], x[a+1]) of a shared-memory address: one IMAD-formed address, two
+// loads with an immediate offset
+__device__ __forceinline__ void lds_pair(uint32_t a, float& v0, float& v1)
+{
+    asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+4];"
+                 : "=f"(v0), "=f"(v1)
+                 : "r"(a));
+}
+// a*4 + base as one IMAD; `base` is made opaque so the compiler cannot
+// re-associate the folded constants back out of it
+__device__ __forceinline__ uint32_t mad4(uint32_t a, uint32_t base)
+{
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(r) : "r"(a), "r"(base));
+    return r;
+}
+__device__ __forceinline__ uint32_t opaque(uint32_t v)
+{
+    asm volatile("" : "+r"(v));
+    return v;
+}
+
 // ---------------------------------------------------------------------------
-// Forward: one CTA = one band of TY consecutive steps (image rows for
+// Forward: a work item = one band of TY consecutive steps (image rows for
 // row-stepping angles, image columns for column-stepping ones) x one tile of
-// TX lanes, staged once in shared memory (transposed for the column branch so
-// both branches read lanes contiguously).  The CTA then walks every selected
-// angle of its branch and, for each ray it owns (ray position at the band's
-// middle step inside [l0, l0+TX); the edge tiles also own the rays beyond),
-// sums the <= TY Joseph samples of that ray inside the band.  Each
-// (band, ray) partial is written exactly once, so the band reduction that
-// follows is deterministic and needs no atomics.  Partial sums of <= 64
-// samples are combined in float64 (blocked fp32 sums).
+// TX lanes (+ halo), for one group of the selection's angles of that branch.
+// Persistent CTAs walk the items round-robin; each item's tile is staged in
+// shared memory by cp.async (LDGSTS, zero-filled outside the image) one item
+// ahead, so the copy of item i+1 overlaps the samples of item i.  Both
+// branches keep the image's row-major orientation in shared memory (the
+// column branch reads lanes with an odd pitch -> conflict-free).  For each ray
+// it owns (ray position at the band's middle step inside [l0, l0+TX); the edge
+// tiles also own the rays beyond), a thread sums the <= TY Joseph samples of
+// that ray inside the band.  Each (band, ray) partial is written exactly once,
+// so the band reduction that follows is deterministic and needs no atomics.
+// Partial sums of <= 64 samples are combined in float64.
 // ---------------------------------------------------------------------------
+// Forward tile configurations: (id, band height TY, lane tile TX, threads, min CTAs/SM)
+#define PT_FWD_CONFIGS(X)        \
+    X(0, 64, 256, 256, 2)        \
+    X(1, 64, 128, 256, 4)        \
+    X(2, 32, 256, 256, 4)        \
+    X(3, 64, 256, 512, 2)        \
+    X(4, 32, 512, 256, 3)        \
+    X(5, 16, 256, 256, 4)        \
+    X(6, 32, 256, 128, 8)        \
+    X(7, 32, 128, 128, 8)        \
+    X(100, 32, 128, 256, 4)      \
+    X(101, 16, 64, 128, 8)
+
+void forward_config(int cfg, int32_t* ty, int32_t* tx)
+{
+    switch (cfg) {
+#define PT_FWD_TT(id, TY, TX, NT, MB) \
+    case id: *ty = TY; *tx = TX; return;
+        PT_FWD_CONFIGS(PT_FWD_TT)
+#undef PT_FWD_TT
+        default: *ty = 32; *tx = 256; return;
+    }
+}
+
 struct FwdArgs {
     const float* x;
-    const float* x2;
     float* partial;
     const AngleTab* tab;
     const int32_t* sel_angle;
@@ -43,18 +141,157 @@ struct FwdArgs {
     int32_t k_begin, n_k;
     int32_t H, W, Z, B;
     int32_t n_groups;
-    int32_t n_bands;  // bands per slice in grid.y (max over branches)
+    int32_t n_bands;  // bands per slice (max over branches)
+    int32_t n_tiles;  // lane tiles (max over branches)
+    int32_t n_items;
 };
 
 template <int TY, int TX>
 struct FwdTile {
     static constexpr int HL = TY / 2 + 3;
-    static constexpr int PITCH = ((TX + 2 * HL) | 1);
-    static constexpr int SMEM = TY * PITCH * 4;
+    static constexpr int NL = TX + 2 * HL;                 // lanes staged per band
+    static constexpr int PITCH_R = NL | 1;                  // row branch: [TY][PITCH_R]
+    static constexpr int PITCH_C = TY + 1;                  // column branch: [NL][PITCH_C]
+    static constexpr int BUF = (TY * PITCH_R > NL * PITCH_C) ? TY * PITCH_R : NL * PITCH_C;
+    static constexpr int SMEM = BUF * 4;
 };
 
+__device__ __forceinline__ void cp_async4(uint32_t dst, const float* src, bool valid)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src),
+                 "r"(valid ? 4 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_one() { asm volatile("cp.async.wait_group 1;"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;"); }
+
+struct FwdItem {
+    int z, branch, band, tile, group;
+};
+
+__device__ __forceinline__ FwdItem decode_item(const FwdArgs& P, int item)
+{
+    FwdItem it;
+    it.tile = item % P.n_tiles;
+    int t = item / P.n_tiles;
+    it.band = t % P.n_bands;
+    t /= P.n_bands;
+    it.group = t % P.n_groups;
+    t /= P.n_groups;
+    it.branch = t & 1;
+    it.z = t >> 1;
+    return it;
+}
+
+// true when the item has work (band / tile inside the branch's extent, angles in the group)
+__device__ __forceinline__ bool item_valid(const FwdArgs& P, const FwdItem& it, int TY, int TX)
+{
+    const int n_steps = it.branch ? P.W : P.H;
+    const int n_lanes = it.branch ? P.H : P.W;
+    if (it.band * TY >= n_steps || it.tile * TX >= n_lanes) return false;
+    const int bb = it.branch ? P.bbeg[1] : P.bbeg[0];
+    const int nb = (it.branch ? P.bend[1] : P.bend[0]) - bb;
+    const long long lo = (long long)nb * it.group / P.n_groups;
+    const long long hi = (long long)nb * (it.group + 1) / P.n_groups;
+    return hi > lo;
+}
+
 template <int TY, int TX, int NT>
-__global__ void __launch_bounds__(NT) fwd_band_kernel(FwdArgs P)
+__device__ __forceinline__ void stage_tile(const FwdArgs& P, const FwdItem& it, uint32_t buf)
+{
+    using T = FwdTile<TY, TX>;
+    constexpr int NW = NT / 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s0 = it.band * TY;
+    const int lane_org = it.tile * TX - T::HL;
+    const float* img = P.x + (size_t)it.z * P.H * P.W;
+    if (it.branch == 0) {
+        // [st][ll] = img[s0 + st][lane_org + ll]: a warp per tile row
+        for (int st = warp; st < TY; st += NW) {
+            const int r = s0 + st;
+            const bool rin = r < P.H;
+            const float* src = img + (size_t)(rin ? r : 0) * P.W;
+            const uint32_t dst = buf + (uint32_t)(st * T::PITCH_R) * 4u;
+#pragma unroll 4
+            for (int ll = lane; ll < T::NL; ll += 32) {
+                const int c = lane_org + ll;
+                const bool ok = rin && c >= 0 && c < P.W;
+                cp_async4(dst + (uint32_t)ll * 4u, src + (ok ? c : 0), ok);
+            }
+        }
+    } else {
+        // [ll][st] = img[lane_org + ll][s0 + st]: a warp per image-row segment
+        for (int ll = warp; ll < T::NL; ll += NW) {
+            const int r = lane_org + ll;
+            const bool rin = r >= 0 && r < P.H;
+            const float* src = img + (size_t)(rin ? r : 0) * P.W + s0;
+            const uint32_t dst = buf + (uint32_t)(ll * T::PITCH_C) * 4u;
+#pragma unroll
+            for (int st = lane; st < TY; st += 32) {
+                const bool ok = rin && s0 + st < P.W;
+                cp_async4(dst + (uint32_t)st * 4u, src + (ok ? st : 0), ok);
+            }
+        }
+    }
+}
+
+// Sum of the Joseph samples st in [st_a, st_b) of one ray inside the tile.
+// LS / SS: byte strides of one lane / one step in the staged tile.
+template <int LS, int SS>
+__device__ __forceinline__ float ray_band_sum(uint32_t tile_u32, int st_a, int st_b, float pl,
+                                              float mf)
+{
+    // shared byte address of lane 0 at step st_a, minus the floor-trick
+    // magic offset folded in (mod 2^32)
+    uint32_t sbase = tile_u32 + (uint32_t)(st_a * SS) - (uint32_t)kMagicBits * (uint32_t)LS;
+    const f2 pl2 = pk(pl, pl), m2 = pk(mf, mf), mg2 = pk(kMagic, kMagic);
+    const f2 two2 = pk(2.f, 2.f);
+    f2 st2 = pk((float)st_a, (float)st_a + 1.f);
+    f2 acc2 = pk(0.f, 0.f);
+    const int n = st_b - st_a;
+    int i = 0;
+    for (; i + 8 <= n; i += 8) {  // 8 samples per trip: 4 packed pairs
+        const uint32_t sb = opaque(sbase);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const f2 pos = fma2(st2, m2, pl2);
+            const f2 t = add2_rm(pos, mg2);
+            const f2 fr = sub2(pos, sub2(t, mg2));
+            float ta, tb, a0, a1, b0, b1;
+            upk(t, ta, tb);
+            const uint32_t aa = __float_as_uint(ta) * (uint32_t)LS + sb + (2 * u) * SS;
+            const uint32_t ab = __float_as_uint(tb) * (uint32_t)LS + sb + (2 * u + 1) * SS;
+            asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+%3];"
+                         : "=f"(a0), "=f"(a1) : "r"(aa), "n"(LS));
+            asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+%3];"
+                         : "=f"(b0), "=f"(b1) : "r"(ab), "n"(LS));
+            const f2 x0 = pk(a0, b0), x1 = pk(a1, b1);
+            acc2 = add2(acc2, fma2(fr, sub2(x1, x0), x0));
+            st2 = add2(st2, two2);
+        }
+        sbase += 8 * SS;
+    }
+    float acc0, acc1;
+    upk(acc2, acc0, acc1);
+    float sa, sb_;
+    upk(st2, sa, sb_);
+    for (; i < n; ++i) {
+        const float pa = fmaf(sa, mf, pl);
+        const float ta = __fadd_rd(pa, kMagic);
+        const float fa = pa - (ta - kMagic);
+        const uint32_t aa = __float_as_uint(ta) * (uint32_t)LS + opaque(sbase);
+        float a0, a1;
+        asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+%3];"
+                     : "=f"(a0), "=f"(a1) : "r"(aa), "n"(LS));
+        acc0 += fmaf(fa, a1 - a0, a0);
+        sa += 1.f;
+        sbase += SS;
+    }
+    return acc0 + acc1;
+}
+
+template <int TY, int TX, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
 {
     using T = FwdTile<TY, TX>;
     extern __shared__ float sm[];
@@ -62,65 +299,35 @@ __global__ void __launch_bounds__(NT) fwd_band_kernel(FwdArgs P)
     __shared__ int s_pref[CH + 1];
     __shared__ int s_blo[CH];
     __shared__ int s_k[CH];
-    __shared__ double s_a0[CH], s_sig[CH], s_m[CH];
-
-    const int branch = blockIdx.z & 1;
-    const int group = blockIdx.z >> 1;
-    const int band = blockIdx.y % P.n_bands;
-    const int z = blockIdx.y / P.n_bands;
-    const int n_steps = branch ? P.W : P.H;
-    const int n_lanes = branch ? P.H : P.W;
-    const int s0 = band * TY;
-    const int l0 = blockIdx.x * TX;
-    if (s0 >= n_steps || l0 >= n_lanes) return;
-    const int bb = branch ? P.bbeg[1] : P.bbeg[0];
-    const int nb = (branch ? P.bend[1] : P.bend[0]) - bb;
-    const int a_begin = bb + (int)(((long long)nb * group) / P.n_groups);
-    const int a_end = bb + (int)(((long long)nb * (group + 1)) / P.n_groups);
-    if (a_begin >= a_end) return;
-    const int32_t* bpos = branch ? P.bpos1 : P.bpos0;
+    __shared__ double s_a0[CH], s_sig[CH], s_m[CH], s_im[CH];
 
     const int tid = threadIdx.x;
+    const FwdItem it = decode_item(P, blockIdx.x);
+    if (!item_valid(P, it, TY, TX)) return;
+    const uint32_t tile_u32 = smem_u32(sm);
+    stage_tile<TY, TX, NT>(P, it, tile_u32);
+    cp_async_commit();
+
+    const int branch = it.branch;
+    const int n_steps = branch ? P.W : P.H;
+    const int n_lanes = branch ? P.H : P.W;
+    const int s0 = it.band * TY;
+    const int l0 = it.tile * TX;
     const int lane_org = l0 - T::HL;
     const int ty_valid = min(TY, n_steps - s0);
-    const size_t plane = (size_t)P.H * P.W;
-    const float* img = P.x + (size_t)z * plane;
-    const float* img2 = P.x2 ? P.x2 + (size_t)z * plane : nullptr;
-
-    // ---- stage the tile (zero outside the image) ----
-    if (branch == 0) {
-        for (int idx = tid; idx < TY * T::PITCH; idx += NT) {
-            int st = idx / T::PITCH, ll = idx - st * T::PITCH;
-            int r = s0 + st, c = lane_org + ll;
-            float v = 0.f;
-            if (r < P.H && c >= 0 && c < P.W) {
-                size_t o = (size_t)r * P.W + c;
-                v = __ldg(img + o);
-                if (img2) v -= __ldg(img2 + o);
-            }
-            sm[idx] = v;
-        }
-    } else {
-        for (int idx = tid; idx < TY * T::PITCH; idx += NT) {
-            int ll = idx / TY, st = idx - ll * TY;
-            int r = lane_org + ll, c = s0 + st;
-            float v = 0.f;
-            if (c < P.W && r >= 0 && r < P.H) {
-                size_t o = (size_t)r * P.W + c;
-                v = __ldg(img + o);
-                if (img2) v -= __ldg(img2 + o);
-            }
-            sm[st * T::PITCH + ll] = v;
-        }
-    }
-    __syncthreads();
-
+    const int bb = branch ? P.bbeg[1] : P.bbeg[0];
+    const int nb = (branch ? P.bend[1] : P.bend[0]) - bb;
+    const int a_begin = bb + (int)(((long long)nb * it.group) / P.n_groups);
+    const int a_end = bb + (int)(((long long)nb * (it.group + 1)) / P.n_groups);
+    const int32_t* bpos = branch ? P.bpos1 : P.bpos0;
     const bool first_tile = (l0 == 0);
     const bool last_tile = (l0 + TX >= n_lanes);
     const double smid = s0 + 0.5 * (ty_valid - 1);
+    bool waited = false;
 
     for (int cbeg = a_begin; cbeg < a_end; cbeg += CH) {
         const int nc = min(CH, a_end - cbeg);
+        // per-angle ray ranges (overlaps the tile copy on the first chunk)
         if (tid < CH) {
             int cnt = 0;
             if (tid < nc) {
@@ -130,11 +337,11 @@ __global__ void __launch_bounds__(NT) fwd_band_kernel(FwdArgs P)
                 const double base = t.a0 + smid * t.m;
                 long long blo, bhi;
                 if (t.sigma > 0) {
-                    blo = first_tile ? 0 : (long long)ceil(((double)l0 - base) / t.sigma);
-                    bhi = last_tile ? P.B : (long long)ceil(((double)(l0 + TX) - base) / t.sigma);
+                    blo = first_tile ? 0 : (long long)ceil(((double)l0 - base) * t.isig);
+                    bhi = last_tile ? P.B : (long long)ceil(((double)(l0 + TX) - base) * t.isig);
                 } else {
-                    blo = last_tile ? 0 : (long long)floor(((double)(l0 + TX) - base) / t.sigma) + 1;
-                    bhi = first_tile ? P.B : (long long)floor(((double)l0 - base) / t.sigma) + 1;
+                    blo = last_tile ? 0 : (long long)floor(((double)(l0 + TX) - base) * t.isig) + 1;
+                    bhi = first_tile ? P.B : (long long)floor(((double)l0 - base) * t.isig) + 1;
                 }
                 blo = max(blo, 0LL);
                 bhi = min(bhi, (long long)P.B);
@@ -144,9 +351,9 @@ __global__ void __launch_bounds__(NT) fwd_band_kernel(FwdArgs P)
                 s_a0[tid] = t.a0;
                 s_sig[tid] = t.sigma;
                 s_m[tid] = t.m;
+                s_im[tid] = t.im;
             }
-            // inclusive warp scan of counts
-            int v = cnt;
+            int v = cnt;  // inclusive warp scan of the ray counts
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 int n = __shfl_up_sync(0xffffffffu, v, o);
@@ -155,6 +362,10 @@ __global__ void __launch_bounds__(NT) fwd_band_kernel(FwdArgs P)
             s_pref[tid + 1] = v;
             if (tid == 0) s_pref[0] = 0;
         }
+        if (!waited) {
+            cp_async_wait_all();
+            waited = true;
+        }
         __syncthreads();
         const int total = s_pref[nc];
         int j = 0;
@@ -162,35 +373,36 @@ __global__ void __launch_bounds__(NT) fwd_band_kernel(FwdArgs P)
             while (w >= s_pref[j + 1]) ++j;
             const int b = s_blo[j] + (w - s_pref[j]);
             const double m = s_m[j];
-            // global lane position at st = 0, then local (tile) coordinate
+            // global lane position at st = 0
             const double P0 = s_a0[j] + (double)b * s_sig[j] + (double)s0 * m;
             // steps where pos in [-1.5, n_lanes + 0.5]: outside, both taps are zero
             int st_a = 0, st_b = ty_valid;
-            if (fabs(m) < 1e-300) {
+            if (s_im[j] == 0.0) {
                 if (P0 < -1.5 || P0 > n_lanes + 0.5) st_b = 0;
             } else {
-                double e1 = (-1.5 - P0) / m, e2 = ((double)n_lanes + 0.5 - P0) / m;
-                double lo = fmin(e1, e2), hi = fmax(e1, e2);
+                const double im = s_im[j];
+                const double e1 = (-1.5 - P0) * im, e2 = ((double)n_lanes + 0.5 - P0) * im;
+                const double lo = fmin(e1, e2), hi = fmax(e1, e2);
                 st_a = max(st_a, (int)ceil(fmin(fmax(lo, -1.0), (double)TY + 1.0)));
                 st_b = min(st_b, (int)floor(fmin(fmax(hi, -2.0), (double)TY + 1.0)) + 1);
             }
-            const float pl = (float)(P0 - (double)lane_org);
+            const float pl = (float)(P0 - (double)lane_org);  // tile-local lane position
             const float mf = (float)m;
-            float acc = 0.f;
-            for (int st = st_a; st < st_b; ++st) {
-                const float pos = fmaf((float)st, mf, pl);
-                const float tt = __fadd_rd(pos, kMagic);
-                const int l = __float_as_int(tt) - kMagicBits;
-                const float fr = pos - (tt - kMagic);
-                const float* row = sm + st * T::PITCH + l;
-                const float x0 = row[0], x1 = row[1];
-                acc += fmaf(fr, x1 - x0, x0);
-            }
+            const float acc = branch == 0
+                ? ray_band_sum<4, T::PITCH_R * 4>(tile_u32, st_a, st_b, pl, mf)
+                : ray_band_sum<T::PITCH_C * 4, 4>(tile_u32, st_a, st_b, pl, mf);
             const size_t kk = (size_t)(s_k[j] - P.k_begin);
-            P.partial[(((size_t)band * P.n_k + kk) * P.Z + z) * P.B + b] = acc;
+            P.partial[(((size_t)it.band * P.n_k + kk) * P.Z + it.z) * P.B + b] = acc;
         }
         __syncthreads();
     }
+}
+
+__global__ void sub_images_kernel(const float* a, const float* b, float* out, size_t n)
+{
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        out[i] = a[i] - b[i];
 }
 
 struct RedArgs {
@@ -200,6 +412,7 @@ struct RedArgs {
     int32_t k_begin, n_k, Z, B;
     int32_t nb_row, nb_col;
     const float* data;
+    const float* data2;
     float* y;
     double* block_sums;
 };
@@ -221,8 +434,10 @@ __global__ void __launch_bounds__(256) fwd_reduce_kernel(RedArgs P)
         const size_t stride = (size_t)P.n_k * P.Z * P.B;
         double s = 0.0;
         for (int band = 0; band < nb; ++band) s += (double)P.partial[band * stride + idx];
-        float yv = (float)(s * (double)at.step_len);
-        if (P.data) yv -= P.data[((size_t)ang * P.Z + z) * P.B + b];
+        double yd = s * (double)at.step_len;
+        if (P.data) yd -= (double)P.data[((size_t)ang * P.Z + z) * P.B + b];
+        if (P.data2) yd -= (double)P.data2[((size_t)ang * P.Z + z) * P.B + b];
+        const float yv = (float)yd;
         P.y[((size_t)k * P.Z + z) * P.B + b] = yv;
         sq = (double)yv * (double)yv;
     }
@@ -240,17 +455,27 @@ __global__ void __launch_bounds__(256) fwd_reduce_kernel(RedArgs P)
     }
 }
 
-template <int TY, int TX, int NT>
+template <int TY, int TX, int NT, int MINB>
 static int run_forward_cfg(pt_plan* plan, Workspace* ws, const pt_selection* sel,
                            const float* x, const float* x2, const float* data, float* y,
-                           double* sumsq, cudaStream_t st)
+                           double* sumsq, cudaStream_t st, const float* data2)
 {
     using T = FwdTile<TY, TX>;
     static bool attr_set = false;
     if (!attr_set) {
-        PT_CHECK_CUDA(cudaFuncSetAttribute(fwd_band_kernel<TY, TX, NT>,
+        PT_CHECK_CUDA(cudaFuncSetAttribute(fwd_band_kernel<TY, TX, NT, MINB>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM));
         attr_set = true;
+    }
+    if (x2) {
+        // A (x - x2): difference image first (standalone API path; the solver
+        // session never projects a difference, see session.cu)
+        const size_t n = (size_t)plan->Z * plan->H * plan->W;
+        if (ws->image_floats < n) { set_error("workspace image too small"); return PT_EINVAL; }
+        sub_images_kernel<<<(int)std::min<size_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(
+            x, x2, ws->image, n);
+        PT_CHECK_LAUNCH();
+        x = ws->image;
     }
     const int nb_row = (plan->H + TY - 1) / TY;
     const int nb_col = (plan->W + TY - 1) / TY;
@@ -259,7 +484,6 @@ static int run_forward_cfg(pt_plan* plan, Workspace* ws, const pt_selection* sel
     const int n_chunk = std::max(1, plan->max_angles_per_launch);
     const size_t per_angle = (size_t)n_bands * plan->Z * plan->B;
     const int n_sel = sel->n;
-    // prefix counts of branch members per selection slot, to slice the lists
     int n_blocks_red_total = 0;
     for (int kb = 0; kb < n_sel; kb += n_chunk) {
         int ke = std::min(n_sel, kb + n_chunk);
@@ -269,6 +493,10 @@ static int run_forward_cfg(pt_plan* plan, Workspace* ws, const pt_selection* sel
         set_error("reduction scratch too small");
         return PT_EINVAL;
     }
+    static const int waves = [] {
+        const char* e = getenv("PT_FWD_WAVES");
+        return e ? std::max(1, atoi(e)) : 3;
+    }();
     int red_off = 0;
     int bi0 = 0, bi1 = 0;  // running positions in the branch lists
     for (int kb = 0; kb < n_sel; kb += n_chunk) {
@@ -279,39 +507,36 @@ static int run_forward_cfg(pt_plan* plan, Workspace* ws, const pt_selection* sel
         }
         FwdArgs a;
         a.x = x;
-        a.x2 = x2;
         a.partial = ws->partial;
         a.tab = plan->d_tab;
         a.sel_angle = sel->d_angle;
         a.bpos0 = sel->d_branch_pos[0];
         a.bpos1 = sel->d_branch_pos[1];
-        int e0 = bi0, e1 = bi1;
-        // the branch lists are ascending in selection slot: slice [kb, ke)
-        {
-            int c0 = 0, c1 = 0;
-            for (int k = kb; k < ke; ++k) {
-                if (plan->h_tab[sel->h_angle[k]].branch) ++c1; else ++c0;
-            }
-            e0 = bi0 + c0;
-            e1 = bi1 + c1;
+        int c0 = 0, c1 = 0;  // the branch lists ascend in selection slot: slice [kb, ke)
+        for (int k = kb; k < ke; ++k) {
+            if (plan->h_tab[sel->h_angle[k]].branch) ++c1; else ++c0;
         }
+        const int e0 = bi0 + c0, e1 = bi1 + c1;
         a.bbeg[0] = bi0; a.bend[0] = e0;
         a.bbeg[1] = bi1; a.bend[1] = e1;
         a.k_begin = kb;
         a.n_k = ke - kb;
         a.H = plan->H; a.W = plan->W; a.Z = plan->Z; a.B = plan->B;
         a.n_bands = n_bands;
-        // angle groups: enough CTAs for >= ~4 waves of 2 CTAs/SM on big launches
-        const int max_branch = std::max(e0 - bi0, e1 - bi1);
-        const long long base_ctas = (long long)n_tiles * n_bands * plan->Z * 2;
-        long long want = (long long)plan->sm_count * 2 * 4;
-        int groups = (int)std::min<long long>(std::max(1LL, want / std::max(1LL, base_ctas)),
-                                              std::max(1, (max_branch + 3) / 4));
-        a.n_groups = std::max(1, groups);
-        dim3 grid(n_tiles, n_bands * plan->Z, 2 * a.n_groups);
+        a.n_tiles = n_tiles;
+        // one CTA per item; angle groups until ~`waves` waves of resident CTAs
+        const int active_branches = (c0 > 0) + (c1 > 0);
+        const long long base_items = (long long)n_tiles * n_bands * plan->Z * std::max(1, active_branches);
+        const int max_branch = std::max(c0, c1);
+        const long long slots = (long long)plan->sm_count * MINB;
+        long long groups = (slots * waves + base_items - 1) / base_items;
+        groups = std::max(1LL, std::min<long long>(groups, std::max(1, max_branch / 2)));
+        a.n_groups = (int)groups;
+        a.n_items = (int)std::min<long long>((long long)n_tiles * n_bands * plan->Z * 2 * groups,
+                                             (long long)INT32_MAX);
         {
             ProfScope ps(ws, PT_PROF_FWD_BAND, st);
-            fwd_band_kernel<TY, TX, NT><<<grid, NT, T::SMEM, st>>>(a);
+            fwd_band_kernel<TY, TX, NT, MINB><<<a.n_items, NT, T::SMEM, st>>>(a);
             PT_CHECK_LAUNCH();
         }
 
@@ -326,6 +551,7 @@ static int run_forward_cfg(pt_plan* plan, Workspace* ws, const pt_selection* sel
         r.nb_row = nb_row;
         r.nb_col = nb_col;
         r.data = data;
+        r.data2 = data2;
         r.y = y;
         r.block_sums = sumsq ? ws->red + red_off : nullptr;
         const size_t tot = (size_t)(ke - kb) * plan->Z * plan->B;
@@ -346,16 +572,19 @@ static int run_forward_cfg(pt_plan* plan, Workspace* ws, const pt_selection* sel
 }
 
 int launch_forward(pt_plan* plan, Workspace* ws, const pt_selection* sel, const float* x,
-                   const float* x2, const float* data, float* y, double* sumsq, cudaStream_t st)
+                   const float* x2, const float* data, float* y, double* sumsq, cudaStream_t st,
+                   const float* data2)
 {
     if (sel->n == 0) {
         if (sumsq) PT_CHECK_CUDA(cudaMemsetAsync(sumsq, 0, sizeof(double), st));
         return PT_OK;
     }
-    switch (plan->fwd_ty) {
-        case 64: return run_forward_cfg<64, 256, 256>(plan, ws, sel, x, x2, data, y, sumsq, st);
-        case 32: return run_forward_cfg<32, 128, 256>(plan, ws, sel, x, x2, data, y, sumsq, st);
-        default: return run_forward_cfg<16, 64, 128>(plan, ws, sel, x, x2, data, y, sumsq, st);
+    switch (plan->fwd_cfg) {
+#define PT_FWD_CASE(id, TY, TX, NT, MB) \
+    case id: return run_forward_cfg<TY, TX, NT, MB>(plan, ws, sel, x, x2, data, y, sumsq, st, data2);
+        PT_FWD_CONFIGS(PT_FWD_CASE)
+#undef PT_FWD_CASE
+        default: set_error("bad forward config"); return PT_EINVAL;
     }
 }
 
@@ -417,13 +646,13 @@ __device__ __forceinline__ void step_epilogue(const pt_step_epilogue& ep, size_t
 }
 
 template <int TR, int TC, int NT, int NA, bool TWO_TAP>
-__global__ void __launch_bounds__(NT) adj_gather_kernel(AdjArgs P)
+__global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
 {
     constexpr int PIX = TR * TC / NT;  // pixels per thread
     constexpr int ROWSTEP = NT / TC;
     extern __shared__ float slots[];
-    __shared__ float s_br[NA], s_bc[NA], s_e0[NA], s_sg[NA];
-    __shared__ int s_off[NA];
+    __shared__ float s_br[NA], s_bc[NA], s_e0[NA], s_sg[NA], s_step[NA];
+    __shared__ int s_off[NA], s_bbase[NA];
 
     const int tid = threadIdx.x;
     const int cl = tid % TC;
@@ -459,51 +688,96 @@ __global__ void __launch_bounds__(NT) adj_gather_kernel(AdjArgs P)
             s_e0[tid] = (float)e0;
             s_sg[tid] = (float)fabs(t.sigma);
             s_off[tid] = -jlo;  // slot index of local bin 0
-            // global bin of slot index 0 stored in the slot header region below
-            reinterpret_cast<int*>(slots)[tid] = (int)bref + jlo;
+            s_bbase[tid] = (int)bref + jlo;  // global bin of slot index 0
+            s_step[tid] = t.step_len;
         }
         __syncthreads();
-        // stage the touched bins (scaled by step_len), zero outside [0, B)
-        float* sl = slots + NA;
-        for (int idx = tid; idx < nc * P.slot; idx += NT) {
-            const int a = idx / P.slot, j = idx - a * P.slot;
-            const int k = kb + a;
-            const int b = reinterpret_cast<const int*>(slots)[a] + j;
-            float v = 0.f;
-            if (b >= 0 && b < P.B) {
-                const AngleTab t = P.tab[P.sel_angle[k]];
-                v = P.y[((size_t)k * P.Z + z) * P.B + b] * t.step_len;
+        // stage the touched bins (scaled by step_len), zero outside [0, B):
+        // one warp per angle, lanes along the bins (coalesced)
+        float* sl = slots;
+        {
+            constexpr int NW = NT / 32;
+            const int warp = tid >> 5, lane = tid & 31;
+            for (int a = warp; a < nc; a += NW) {
+                const int k = kb + a;
+                const int bb = s_bbase[a];
+                const float stp = s_step[a];
+                const float* yrow = P.y + ((size_t)k * P.Z + z) * P.B;
+                float* dst = sl + a * P.slot;
+                for (int j = lane; j < P.slot; j += 32) {
+                    const int b = bb + j;
+                    dst[j] = (b >= 0 && b < P.B) ? __ldg(yrow + b) * stp : 0.f;
+                }
             }
-            sl[idx] = v;
         }
         __syncthreads();
-        float acc_i[PIX];
+        if (TWO_TAP) {
+            // packed pairs of pixels (rows rg + 4(2jj), rg + 4(2jj+1))
+            f2 acc2[PIX / 2];
 #pragma unroll
-        for (int j = 0; j < PIX; ++j) acc_i[j] = 0.f;
-        for (int a = 0; a < nc; ++a) {
-            const float br = s_br[a], sg = s_sg[a];
-            const float cterm = fmaf((float)cl, s_bc[a], s_e0[a]);
-            const int ybase = a * P.slot + s_off[a] - kMagicBits;
+            for (int jj = 0; jj < PIX / 2; ++jj) acc2[jj] = pk(0.f, 0.f);
+            const f2 mg2 = pk(kMagic, kMagic), one2 = pk(1.f, 1.f);
+            const uint32_t sl_u32 = smem_u32(sl) - (uint32_t)kMagicBits * 4u;
+            f2 rr[PIX / 2];
 #pragma unroll
-            for (int j = 0; j < PIX; ++j) {
-                const float bl = fmaf((float)(rg + j * ROWSTEP), br, cterm);
-                const float tt = __fadd_rd(bl, kMagic);
-                const float phi = bl - (tt - kMagic);
-                const float* yp = sl + (ybase + __float_as_int(tt));
-                if (TWO_TAP) {
-                    const float w0 = fmaxf(0.f, fmaf(-sg, phi, 1.f));
-                    const float w1 = fmaxf(0.f, fmaf(sg, phi, 1.f - sg));
-                    acc_i[j] = fmaf(w0, yp[0], fmaf(w1, yp[1], acc_i[j]));
-                } else {
+            for (int jj = 0; jj < PIX / 2; ++jj)
+                rr[jj] = pk((float)(rg + (2 * jj) * ROWSTEP), (float)(rg + (2 * jj + 1) * ROWSTEP));
+            const float clf = (float)cl;
+#pragma unroll 1
+            for (int a = 0; a < nc; ++a) {
+                const float br = s_br[a], sg = s_sg[a];
+                const float cterm = fmaf(clf, s_bc[a], s_e0[a]);
+                const uint32_t yb = opaque(sl_u32 + (uint32_t)(a * P.slot + s_off[a]) * 4u);
+                const f2 ct2 = pk(cterm, cterm), br2 = pk(br, br);
+                const f2 nsg2 = pk(-sg, -sg), sg2 = pk(sg, sg), oms2 = pk(1.f - sg, 1.f - sg);
+#pragma unroll
+                for (int jj = 0; jj < PIX / 2; ++jj) {
+                    const f2 bl = fma2(rr[jj], br2, ct2);
+                    const f2 t = add2_rm(bl, mg2);
+                    const f2 phi = sub2(bl, sub2(t, mg2));
+                    f2 w0 = fma2(nsg2, phi, one2);
+                    f2 w1 = fma2(sg2, phi, oms2);
+                    float w0a, w0b, w1a, w1b, ta, tb, y0a, y1a, y0b, y1b;
+                    upk(w0, w0a, w0b);
+                    upk(w1, w1a, w1b);
+                    w0 = pk(fmaxf(w0a, 0.f), fmaxf(w0b, 0.f));
+                    w1 = pk(fmaxf(w1a, 0.f), fmaxf(w1b, 0.f));
+                    upk(t, ta, tb);
+                    lds_pair(mad4(__float_as_uint(ta), yb), y0a, y1a);
+                    lds_pair(mad4(__float_as_uint(tb), yb), y0b, y1b);
+                    acc2[jj] = fma2(w0, pk(y0a, y0b), fma2(w1, pk(y1a, y1b), acc2[jj]));
+                }
+            }
+#pragma unroll
+            for (int jj = 0; jj < PIX / 2; ++jj) {
+                float a0, a1;
+                upk(acc2[jj], a0, a1);
+                acc_o[2 * jj] += a0;
+                acc_o[2 * jj + 1] += a1;
+            }
+        } else {
+            float acc_i[PIX];
+#pragma unroll
+            for (int j = 0; j < PIX; ++j) acc_i[j] = 0.f;
+            for (int a = 0; a < nc; ++a) {
+                const float br = s_br[a], sg = s_sg[a];
+                const float cterm = fmaf((float)cl, s_bc[a], s_e0[a]);
+                const int ybase = a * P.slot + s_off[a] - kMagicBits;
+#pragma unroll
+                for (int j = 0; j < PIX; ++j) {
+                    const float bl = fmaf((float)(rg + j * ROWSTEP), br, cterm);
+                    const float tt = __fadd_rd(bl, kMagic);
+                    const float phi = bl - (tt - kMagic);
+                    const float* yp = sl + (ybase + __float_as_int(tt));
                     for (int q = -P.cand_half + 1; q <= P.cand_half; ++q) {
                         const float w = fmaxf(0.f, 1.f - sg * fabsf((float)q - phi));
                         acc_i[j] = fmaf(w, yp[q], acc_i[j]);
                     }
                 }
             }
-        }
 #pragma unroll
-        for (int j = 0; j < PIX; ++j) acc_o[j] += acc_i[j];
+            for (int j = 0; j < PIX; ++j) acc_o[j] += acc_i[j];
+        }
         __syncthreads();
     }
 
@@ -536,7 +810,7 @@ static constexpr int kTR = 32, kTC = 64, kNT = 256, kNA = 32;
 template <bool TWO>
 static int run_gather(pt_plan* plan, const AdjArgs& a, cudaStream_t st)
 {
-    const size_t smem = (size_t)(kNA + kNA * a.slot) * sizeof(float);
+    const size_t smem = (size_t)(kNA * a.slot) * sizeof(float);
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
         PT_CHECK_CUDA(cudaFuncSetAttribute(adj_gather_kernel<kTR, kTC, kNT, kNA, TWO>,

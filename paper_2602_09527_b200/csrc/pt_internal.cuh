@@ -23,6 +23,7 @@ namespace pt {
 // with cB = (B-1)/2, cH = (H-1)/2, cW = (W-1)/2; step_len = h/max(|cos|,|sin|).
 struct AngleTab {
     double sigma, m, a0;
+    double isig, im;  // 1/sigma, 1/m (0 when m == 0)
     float step_len;
     int branch;
 };
@@ -84,6 +85,8 @@ struct Workspace {
     size_t partial_floats = 0;
     double* red = nullptr;
     size_t red_doubles = 0;
+    float* image = nullptr;  // image-sized temp (difference images)
+    size_t image_floats = 0;
     Profiler* prof = nullptr;
 };
 struct ProfScope {
@@ -107,7 +110,7 @@ struct pt_plan {
     pt::AngleTab* d_tab = nullptr;
     int32_t cand_half = 1;     // gather candidates per side: ceil(h/ds) (1 = two-tap)
     int32_t gather_slot = 0;   // floats of staged sinogram per angle in the gather
-    int32_t fwd_ty = 64, fwd_tx = 256;
+    int32_t fwd_cfg = 0, fwd_ty = 64, fwd_tx = 256;
     int32_t n_bands = 0;
     int32_t max_angles_per_launch = 0;
     pt::Workspace ws;
@@ -119,8 +122,11 @@ struct pt_plan {
 
 namespace pt {
 // kernels (projector.cu)
+void forward_config(int cfg, int32_t* ty, int32_t* tx);
+// y = A_S (x - x2) - data_S - data2_S; data / data2 are full sinograms indexed by angle
 int launch_forward(pt_plan* plan, Workspace* ws, const pt_selection* sel, const float* x,
-                   const float* x2, const float* data, float* y, double* sumsq, cudaStream_t st);
+                   const float* x2, const float* data, float* y, double* sumsq, cudaStream_t st,
+                   const float* data2 = nullptr);
 int launch_adjoint(pt_plan* plan, const pt_selection* sel, const float* y, float* x_out,
                    float alpha, int accumulate, const pt_step_epilogue* ep, cudaStream_t st,
                    Workspace* ws = nullptr, int cat = PT_PROF_GATHER);

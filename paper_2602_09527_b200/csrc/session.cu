@@ -128,7 +128,8 @@ struct pt_session {
     float *saga_table = nullptr, *saga_sum = nullptr;
     float *dp = nullptr, *dq = nullptr, *dw = nullptr;
     float* fgp_work = nullptr;
-    float* r = nullptr;  // residual rows (largest selection)
+    float* r = nullptr;      // residual rows (largest selection)
+    float* rsnap = nullptr;  // SVRG: A x_snap - b over the owned angles (snapshot residual)
     float* g = nullptr;  // partial gradient (multi-GPU)
     int64_t* bad = nullptr;
     pt::Workspace ws;
@@ -195,20 +196,30 @@ int allreduce(pt_session* s, float* buf, cudaStream_t st)
     return PT_OK;
 }
 
-// G = A^T (A x - b) over the owned angles, summed over ranks (estimators.py:40-48)
-int full_gradient(pt_session* s, const float* x, float* out, cudaStream_t st)
+// G = A^T (A x - b) over the owned angles, summed over ranks (estimators.py:40-48).
+// The residual A x - b is kept in `res` (SVRG: the snapshot residual, so each
+// step's A_i(x - x_snap) = (A_i x - b_i) - (A_i x_snap - b_i) needs one
+// projection of x only; the subtraction is done in float64 in the reduction).
+int full_gradient(pt_session* s, const float* x, float* out, float* res, cudaStream_t st)
 {
     pt::ProfScope ps(&s->ws, PT_PROF_SNAPSHOT, st);
     pt_plan* P = s->plan;
-    int rc = pt::launch_forward(P, &s->ws, s->own_all, x, nullptr, s->data, s->r, nullptr, st);
+    int rc = pt::launch_forward(P, &s->ws, s->own_all, x, nullptr, s->data, res, nullptr, st);
     if (rc) return rc;
     if (s->own_all->n == 0) {
         PT_CHECK_CUDA(cudaMemsetAsync(out, 0, s->n * 4, st));
     } else {
-        rc = pt::launch_adjoint(P, s->own_all, s->r, out, 1.f, 0, nullptr, st);
+        rc = pt::launch_adjoint(P, s->own_all, res, out, 1.f, 0, nullptr, st);
         if (rc) return rc;
     }
     return allreduce(s, out, st);
+}
+
+// The snapshot residual indexed by geometry angle (rows [lo, hi) are owned).
+const float* rsnap_by_angle(const pt_session* s)
+{
+    const int lo = (int)((long long)s->plan->A * s->rank / s->world);
+    return s->rsnap - (ptrdiff_t)lo * s->plan->Z * s->plan->B;
 }
 
 }  // namespace
@@ -243,7 +254,10 @@ int pt_session_create(pt_plan* plan, const pt_solver_desc* desc, const float* da
     int rc = PT_OK;
     auto A = [&](float** p, size_t cnt) { if (rc == PT_OK) rc = alloc_f(p, cnt); };
     A(&s->x[0], n); A(&s->x[1], n); A(&s->h, n); A(&s->v, n); A(&s->xhat, n);
-    if (desc->estimator == PT_EST_SVRG || desc->estimator == PT_EST_LSVRG) { A(&s->snap, n); A(&s->fg, n); }
+    if (desc->estimator == PT_EST_SVRG || desc->estimator == PT_EST_LSVRG) {
+        A(&s->snap, n); A(&s->fg, n);
+        A(&s->rsnap, (size_t)plan->A * plan->Z * plan->B);
+    }
     if (desc->estimator == PT_EST_SAGA) { A(&s->saga_table, n * desc->n_subsets); A(&s->saga_sum, n); }
     if (desc->prox_kind == 1) {
         A(&s->dp, n); A(&s->dq, n);
@@ -278,7 +292,7 @@ int pt_session_destroy(pt_session* s)
     if (!s) return PT_OK;
     cudaDeviceSynchronize();
     float* bufs[] = {s->x[0], s->x[1], s->h, s->v, s->xhat, s->snap, s->fg, s->saga_table,
-                     s->saga_sum, s->dp, s->dq, s->dw, s->fgp_work, s->r, s->g};
+                     s->saga_sum, s->dp, s->dq, s->dw, s->fgp_work, s->r, s->g, s->rsnap};
     for (float* b : bufs)
         if (b) cudaFree(b);
     if (s->bad) cudaFree(s->bad);
@@ -295,7 +309,7 @@ int pt_session_init(pt_session* s, void* stream)
     cudaStream_t st = (cudaStream_t)stream;
     // init_svrg_state (estimators.py:117-123): snapshot = x0, G = full gradient
     PT_CHECK_CUDA(cudaMemcpyAsync(s->snap, s->x[s->cur], s->n * 4, cudaMemcpyDeviceToDevice, st));
-    return full_gradient(s, s->snap, s->fg, st);
+    return full_gradient(s, s->snap, s->fg, s->rsnap, st);
 }
 
 int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
@@ -316,7 +330,7 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
                 pt::ProfScope ps(&s->ws, PT_PROF_OTHER, st);
                 PT_CHECK_CUDA(cudaMemcpyAsync(s->snap, s->x[s->cur], s->n * 4, cudaMemcpyDeviceToDevice, st));
             }
-            rc = full_gradient(s, s->snap, s->fg, st);
+            rc = full_gradient(s, s->snap, s->fg, s->rsnap, st);
             if (rc) return rc;
         }
         const pt_selection* sel = s->own_all;
@@ -334,8 +348,11 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
         const int theta = (p >= 1.0) ? 1 : (host_theta ? host_theta[j] : 0);
 
         // forward: residual rows of the (own part of the) selection
-        if (vr) rc = pt::launch_forward(P, &s->ws, sel, xc, s->snap, nullptr, s->r, nullptr, st);
-        else rc = pt::launch_forward(P, &s->ws, sel, xc, nullptr, s->data, s->r, nullptr, st);
+        if (vr)  // A_i (x - x_snap) = (A_i x - b_i) - (A_i x_snap - b_i)
+            rc = pt::launch_forward(P, &s->ws, sel, xc, nullptr, s->data, s->r, nullptr, st,
+                                    rsnap_by_angle(s));
+        else
+            rc = pt::launch_forward(P, &s->ws, sel, xc, nullptr, s->data, s->r, nullptr, st);
         if (rc) return rc;
 
         pt_step_epilogue ep;
