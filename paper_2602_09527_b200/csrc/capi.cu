@@ -69,6 +69,11 @@ static AngleTab make_tab(double theta, int H, int W, int B, double ds, double h)
     }
     t.isig = 1.0 / t.sigma;
     t.im = fabs(t.m) < 1e-300 ? 0.0 : 1.0 / t.m;
+    // d(b, r, c) = sigma b + ar r + ac c + a0 (pos_b - lane); b_f solves d = 0
+    const double ar = t.branch ? -1.0 : t.m, ac = t.branch ? t.m : -1.0;
+    t.gbr = -ar / t.sigma;
+    t.gbc = -ac / t.sigma;
+    t.gg = -t.a0 / t.sigma;
     return t;
 }
 

@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "pt_internal.cuh"
+#include "pt_simd.cuh"
 
 namespace pt {
 
@@ -112,9 +113,77 @@ __device__ __forceinline__ void fgp2d_iteration(
     }
 }
 
+// Interior iteration with packed f32x2 arithmetic.  A thread's strip rows are
+// held as pairs (j, j + H2), H2 = STRIP/2, so the up-neighbour of pair j is
+// pair j-1 and the down-neighbour of pair j is pair j+1 (one repack at the
+// strip ends): the stencil needs no lane shuffling.
+template <int RW, int RH, int STRIP>
+__device__ __forceinline__ void fgp2d_iteration_packed(
+    f2 (&V)[STRIP / 2], f2 (&Pp)[STRIP / 2], f2 (&Q)[STRIP / 2], f2 (&R)[STRIP / 2],
+    f2 (&S)[STRIP / 2], f2 (&U)[STRIP / 2], float (*S_s)[RW + 1], float (*S_u)[RW + 1],
+    float (*S_r)[RW], float (*S_ut)[RW], int tx, int ty, float lam, float eta, float beta,
+    int nonneg)
+{
+    constexpr int NS = RH / STRIP;
+    constexpr int H2 = STRIP / 2;
+    const int row0 = ty * STRIP;
+    const f2 nlam2 = pk(-lam, -lam), eta2 = pk(eta, eta), beta2 = pk(beta, beta);
+#pragma unroll
+    for (int j = 0; j < H2; ++j) {
+        float a, b;
+        upk(S[j], a, b);
+        S_s[row0 + j][tx] = a;
+        S_s[row0 + j + H2][tx] = b;
+    }
+    S_r[ty][tx] = hi_of(R[H2 - 1]);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < H2; ++j) {
+        const f2 r_up = j ? R[j - 1] : pk(ty ? S_r[ty - 1][tx] : 0.f, lo_of(R[H2 - 1]));
+        const f2 s_left = pk(tx ? S_s[row0 + j][tx - 1] : 0.f, tx ? S_s[row0 + j + H2][tx - 1] : 0.f);
+        // _diff_adjoint (regularizers.py:70-76): ((-r + r_up) - s) + s_left
+        const f2 o = add2(sub2(sub2(r_up, R[j]), S[j]), s_left);
+        f2 u = fma2(nlam2, o, V[j]);
+        float ua, ub;
+        upk(u, ua, ub);
+        if (nonneg) {
+            ua = (ua < 0.f) ? 0.f : ua;
+            ub = (ub < 0.f) ? 0.f : ub;
+            u = pk(ua, ub);
+        }
+        U[j] = u;
+        S_u[row0 + j][tx] = ua;
+        S_u[row0 + j + H2][tx] = ub;
+    }
+    S_ut[ty][tx] = lo_of(U[0]);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < H2; ++j) {
+        // rows (j+1, j+1+H2); for the last pair these are (H2 -> pair 0 hi, next strip's first row)
+        const f2 u_down = (j < H2 - 1) ? U[j + 1]
+                                       : pk(hi_of(U[0]), ty < NS - 1 ? S_ut[ty + 1][tx] : 0.f);
+        const f2 u_right = pk(tx < RW - 1 ? S_u[row0 + j][tx + 1] : 0.f,
+                              tx < RW - 1 ? S_u[row0 + j + H2][tx + 1] : 0.f);
+        const f2 gv = sub2(u_down, U[j]);
+        const f2 gh = sub2(u_right, U[j]);
+        const f2 ph = fma2(eta2, gv, R[j]);
+        const f2 qh = fma2(eta2, gh, S[j]);
+        const f2 n2 = fma2(ph, ph, mul2(qh, qh));
+        float na, nb;
+        upk(n2, na, nb);
+        const f2 inv = pk((na > 1.f) ? rsqrtf(na) : 1.f, (nb > 1.f) ? rsqrtf(nb) : 1.f);
+        const f2 pn = mul2(ph, inv), qn = mul2(qh, inv);
+        R[j] = fma2(beta2, sub2(pn, Pp[j]), pn);
+        S[j] = fma2(beta2, sub2(qn, Q[j]), qn);
+        Pp[j] = pn;
+        Q[j] = qn;
+    }
+}
+
 template <int RW, int RH, int STRIP>
 __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
 {
+    constexpr int H2 = STRIP / 2;
     __shared__ float S_s[RH][RW + 1];
     __shared__ float S_u[RH][RW + 1];
     __shared__ float S_r[RH / STRIP][RW];
@@ -133,32 +202,70 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
     // the whole region, and one point beyond it, strictly inside the image
     const bool edge = !(i0 >= 0 && j0 >= 0 && i0 + RH < P.H && j0 + RW < P.W);
 
-    float v[STRIP], p[STRIP], q[STRIP], r[STRIP], s[STRIP], u[STRIP];
+    // packed state: pair j = strip rows (j, j + H2)
+    f2 V[H2], Pp[H2], Q[H2], R[H2], S[H2], U[H2];
     unsigned in_mask = 0;
 #pragma unroll
-    for (int k = 0; k < STRIP; ++k) {
-        const int gi = i0 + row0 + k;
-        const bool in = col_in && gi >= 0 && gi < P.H;
-        if (in) in_mask |= 1u << k;
-        const size_t o = in ? (size_t)gi * P.W + gj : 0;
-        v[k] = in ? P.v[o] : 0.f;
-        p[k] = in ? P.p_in[o] : 0.f;
-        q[k] = in ? P.q_in[o] : 0.f;
-        r[k] = in ? (P.r_in ? P.r_in[o] : p[k]) : 0.f;
-        s[k] = in ? (P.s_in ? P.s_in[o] : q[k]) : 0.f;
-        u[k] = 0.f;
+    for (int j = 0; j < H2; ++j) {
+        float vv[2], pv[2], qv[2], rv[2], sv[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int k = j + h * H2;
+            const int gi = i0 + row0 + k;
+            const bool in = col_in && gi >= 0 && gi < P.H;
+            if (in) in_mask |= 1u << k;
+            const size_t o = in ? (size_t)gi * P.W + gj : 0;
+            vv[h] = in ? P.v[o] : 0.f;
+            pv[h] = in ? P.p_in[o] : 0.f;
+            qv[h] = in ? P.q_in[o] : 0.f;
+            rv[h] = in ? (P.r_in ? P.r_in[o] : pv[h]) : 0.f;
+            sv[h] = in ? (P.s_in ? P.s_in[o] : qv[h]) : 0.f;
+        }
+        V[j] = pk(vv[0], vv[1]);
+        Pp[j] = pk(pv[0], pv[1]);
+        Q[j] = pk(qv[0], qv[1]);
+        R[j] = pk(rv[0], rv[1]);
+        S[j] = pk(sv[0], sv[1]);
+        U[j] = pk(0.f, 0.f);
     }
     for (int it = 0; it < P.n_iter; ++it) {
-        if (edge)
+        if (!edge) {
+            fgp2d_iteration_packed<RW, RH, STRIP>(V, Pp, Q, R, S, U, S_s, S_u, S_r, S_ut, tx, ty,
+                                                  P.lam, P.eta, P.beta[it], P.nonneg);
+        } else {
+            float v[STRIP], p[STRIP], q[STRIP], r[STRIP], s[STRIP], u[STRIP];
+#pragma unroll
+            for (int j = 0; j < H2; ++j) {
+                upk(V[j], v[j], v[j + H2]);
+                upk(Pp[j], p[j], p[j + H2]);
+                upk(Q[j], q[j], q[j + H2]);
+                upk(R[j], r[j], r[j + H2]);
+                upk(S[j], s[j], s[j + H2]);
+                upk(U[j], u[j], u[j + H2]);
+            }
             fgp2d_iteration<RW, RH, STRIP, true>(v, p, q, r, s, u, S_s, S_u, S_r, S_ut, tx, ty, i0,
                                                  P.H, not_last_col, in_mask, P.lam, P.eta,
                                                  P.beta[it], P.nonneg);
-        else
-            fgp2d_iteration<RW, RH, STRIP, false>(v, p, q, r, s, u, S_s, S_u, S_r, S_ut, tx, ty, i0,
-                                                  P.H, not_last_col, in_mask, P.lam, P.eta,
-                                                  P.beta[it], P.nonneg);
+#pragma unroll
+            for (int j = 0; j < H2; ++j) {
+                Pp[j] = pk(p[j], p[j + H2]);
+                Q[j] = pk(q[j], q[j + H2]);
+                R[j] = pk(r[j], r[j + H2]);
+                S[j] = pk(s[j], s[j + H2]);
+                U[j] = pk(u[j], u[j + H2]);
+            }
+        }
     }
 
+    float v[STRIP], p[STRIP], q[STRIP], r[STRIP], s[STRIP];
+#pragma unroll
+    for (int j = 0; j < H2; ++j) {
+        upk(V[j], v[j], v[j + H2]);
+        upk(Pp[j], p[j], p[j + H2]);
+        upk(Q[j], q[j], q[j + H2]);
+        upk(R[j], r[j], r[j + H2]);
+        upk(S[j], s[j], s[j + H2]);
+    }
     const bool col_inner = tx >= P.halo && tx < RW - P.halo;
     const float lam = P.lam;
     if (P.final_) {

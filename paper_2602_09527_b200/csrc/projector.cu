@@ -12,6 +12,7 @@
 #include <cstdlib>
 
 #include "pt_internal.cuh"
+#include "pt_simd.cuh"
 
 namespace pt {
 
@@ -20,45 +21,6 @@ namespace pt {
 static constexpr float kMagic = 12582912.0f;
 static constexpr int kMagicBits = 0x4B400000;
 
-// Packed float32x2 arithmetic (sm_100a FFMA2 / FADD2): two Joseph samples or
-// two pixels per instruction, halving the FP issue slots of the hot loops.
-struct f2 {
-    unsigned long long v;
-};
-__device__ __forceinline__ f2 pk(float a, float b)
-{
-    f2 r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ void upk(f2 r, float& a, float& b)
-{
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r.v));
-}
-__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c)
-{
-    f2 r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
-    return r;
-}
-__device__ __forceinline__ f2 add2(f2 a, f2 b)
-{
-    f2 r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-    return r;
-}
-__device__ __forceinline__ f2 add2_rm(f2 a, f2 b)
-{
-    f2 r;
-    asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-    return r;
-}
-__device__ __forceinline__ f2 sub2(f2 a, f2 b)
-{
-    f2 r;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-    return r;
-}
 __device__ __forceinline__ uint32_t smem_u32(const void* p)
 {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -160,6 +122,11 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const float* src, bool v
 {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src),
                  "r"(valid ? 4 : 0));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const float* src, int valid_bytes)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                 "r"(valid_bytes));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 __device__ __forceinline__ void cp_async_wait_one() { asm volatile("cp.async.wait_group 1;"); }
@@ -609,6 +576,8 @@ struct AdjArgs {
     int32_t H, W, Z, B;
     int32_t slot;
     int32_t cand_half;
+    int32_t nbuf;     // staging buffers (2: chunk pipeline)
+    int32_t n_epi;    // epilogue operand planes prefetched into shared memory
     float alpha;
     int32_t accumulate;
     float* out;
@@ -616,24 +585,24 @@ struct AdjArgs {
     pt_step_epilogue ep;
 };
 
-__device__ __forceinline__ void step_epilogue(const pt_step_epilogue& ep, size_t p, float g)
+// The estimator + ProxSkip step of one pixel (estimators.py:55,92-94,146;
+// solvers.py:236-246) given its gradient g and the prefetched operands.
+__device__ __forceinline__ void step_epilogue_vals(const pt_step_epilogue& ep, size_t p, float g,
+                                                   float xv, float hv, float a0v, float a1v)
 {
     float est;
     switch (ep.estimator) {
         case PT_EST_FULL: est = g; break;
         case PT_EST_SGD: est = ep.n_scale * g; break;
         case PT_EST_SAGA: {
-            const float old = ep.aux0[p];
-            const float s = ep.aux1[p];
-            est = ep.n_scale * g + (s - ep.n_scale * old);
-            ep.aux1[p] = (s - old) + g;
+            est = ep.n_scale * g + (a1v - ep.n_scale * a0v);
+            ep.aux1[p] = (a1v - a0v) + g;
             ep.aux0[p] = g;
             break;
         }
-        default: est = ep.n_scale * g + ep.aux0[p]; break;  // svrg / lsvrg
+        default: est = ep.n_scale * g + a0v; break;  // svrg / lsvrg
     }
-    const float hv = ep.h[p];
-    const float base = ep.x[p] - ep.gamma * est;
+    const float base = xv - ep.gamma * est;
     const float xh = base + ep.gamma * hv;
     if (ep.theta) {
         ep.v_out[p] = base + ep.hcoef * hv;
@@ -645,98 +614,149 @@ __device__ __forceinline__ void step_epilogue(const pt_step_epilogue& ep, size_t
     }
 }
 
+__device__ __forceinline__ void step_epilogue(const pt_step_epilogue& ep, size_t p, float g)
+{
+    const bool saga = ep.estimator == PT_EST_SAGA;
+    const bool vr = ep.estimator == PT_EST_SVRG || ep.estimator == PT_EST_LSVRG;
+    step_epilogue_vals(ep, p, g, ep.x[p], ep.h[p], (saga || vr) ? ep.aux0[p] : 0.f,
+                       saga ? ep.aux1[p] : 0.f);
+}
+
 template <int TR, int TC, int NT, int NA, bool TWO_TAP>
 __global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
 {
     constexpr int PIX = TR * TC / NT;  // pixels per thread
     constexpr int ROWSTEP = NT / TC;
-    extern __shared__ float slots[];
-    __shared__ float s_br[NA], s_bc[NA], s_e0[NA], s_sg[NA], s_step[NA];
-    __shared__ int s_off[NA], s_bbase[NA];
+    constexpr int NW = NT / 32;
+    extern __shared__ float smem[];
+    __shared__ float s_br[2][NA], s_bc[2][NA], s_e0[2][NA], s_S1[2][NA], s_A0[2][NA];
+    __shared__ int s_off[2][NA], s_bbase[2][NA];
+    __shared__ uint32_t s_yaddr[2][NA];
 
     const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
     const int cl = tid % TC;
     const int rg = tid / TC;
     const int r0 = blockIdx.y * TR;
     const int c0 = blockIdx.x * TC;
     const int z = blockIdx.z;
     const size_t plane = (size_t)P.H * P.W;
+    const uint32_t stage_u32 = smem_u32(smem);
+    const uint32_t epi_u32 = stage_u32 + (uint32_t)(P.nbuf * NA * P.slot) * 4u;
+
+    // --- epilogue operands: prefetched with cp.async, consumed at the end ---
+    if (P.n_epi) {
+        const bool vec = (P.W % 4) == 0;  // 16-byte rows (c0 is a multiple of TC)
+        for (int e = 0; e < P.n_epi; ++e) {
+            const float* srcp = e == 0 ? P.ep.x : e == 1 ? P.ep.h : e == 2 ? P.ep.aux0 : P.ep.aux1;
+            const float* base = srcp + (size_t)z * plane;
+            const uint32_t dst = epi_u32 + (uint32_t)(e * TR * TC) * 4u;
+            if (vec) {
+                constexpr int Q = TC / 4;  // 16-byte quads per tile row
+                for (int idx = tid; idx < TR * Q; idx += NT) {
+                    const int rl = idx / Q, q = idx - rl * Q;
+                    const int r = r0 + rl, c = c0 + 4 * q;
+                    const int nvalid = (r < P.H) ? max(0, min(4, P.W - c)) : 0;
+                    cp_async16(dst + (uint32_t)(rl * TC + 4 * q) * 4u,
+                               base + (nvalid ? (size_t)r * P.W + c : 0), 4 * nvalid);
+                }
+            } else {
+                for (int idx = tid; idx < TR * TC; idx += NT) {
+                    const int rl = idx / TC, cc = idx - rl * TC;
+                    const int r = r0 + rl, c = c0 + cc;
+                    const bool ok = r < P.H && c < P.W;
+                    cp_async4(dst + (uint32_t)idx * 4u, base + (ok ? (size_t)r * P.W + c : 0), ok);
+                }
+            }
+        }
+        cp_async_commit();
+    }
+
+    // per-chunk preparation: angle parameters in the tile frame (float64 ->
+    // float32) and the touched sinogram bins (cp.async, zero outside [0, B))
+    auto prepare = [&](int kb, int buf) {
+        const int nc = min(NA, P.n_sel - kb);
+        if (tid < nc) {
+            const AngleTab& t = P.tab[P.sel_angle[kb + tid]];
+            const double gbr = t.gbr, gbc = t.gbc;
+            // crossing bin b_f(r, c) = gbr r + gbc c + gg (pos(b_f) == lane)
+            const double bf00 = gbr * r0 + gbc * c0 + t.gg;
+            const double bref = floor(bf00);
+            const double e0 = bf00 - bref;
+            const double lo = e0 + fmin(0.0, gbr) * (TR - 1) + fmin(0.0, gbc) * (TC - 1);
+            const int jlo = (int)floor(lo) - P.cand_half - 1;
+            const float stp = t.step_len;
+            s_br[buf][tid] = (float)gbr;
+            s_bc[buf][tid] = (float)gbc;
+            s_e0[buf][tid] = (float)e0;
+            s_A0[buf][tid] = stp;
+            s_S1[buf][tid] = (float)(stp * fabs(t.sigma));
+            // shared byte address of local bin 0 minus the floor-trick offset:
+            // a runtime value, so the compiler keeps it folded in one IMAD
+            s_yaddr[buf][tid] = stage_u32 + (uint32_t)((buf * NA + tid) * P.slot - jlo) * 4u -
+                                (uint32_t)kMagicBits * 4u;
+            s_bbase[buf][tid] = (int)bref + jlo;
+            s_off[buf][tid] = -jlo;
+        }
+        __syncthreads();
+        // staging: one warp per angle, lanes along the bins
+        for (int a = warp; a < nc; a += NW) {
+            const int k = kb + a;
+            const int bb = s_bbase[buf][a];
+            const float* yrow = P.y + ((size_t)k * P.Z + z) * P.B;
+            const uint32_t dst = stage_u32 + (uint32_t)((buf * NA + a) * P.slot) * 4u;
+            for (int j = lane; j < P.slot; j += 32) {
+                const int b = bb + j;
+                const bool ok = b >= 0 && b < P.B;
+                cp_async4(dst + (uint32_t)j * 4u, yrow + (ok ? b : 0), ok);
+            }
+        }
+        cp_async_commit();
+    };
 
     float acc_o[PIX];
 #pragma unroll
     for (int j = 0; j < PIX; ++j) acc_o[j] = 0.f;
+    f2 rr[PIX / 2];
+#pragma unroll
+    for (int jj = 0; jj < PIX / 2; ++jj)
+        rr[jj] = pk((float)(rg + (2 * jj) * ROWSTEP), (float)(rg + (2 * jj + 1) * ROWSTEP));
+    const float clf = (float)cl;
+    const f2 mg2 = pk(kMagic, kMagic);
 
-    for (int kb = 0; kb < P.n_sel; kb += NA) {
+    const int n_chunks = (P.n_sel + NA - 1) / NA;
+    if (n_chunks > 0) prepare(0, 0);
+    for (int ci = 0; ci < n_chunks; ++ci) {
+        const int buf = (P.nbuf == 2) ? (ci & 1) : 0;
+        const int kb = ci * NA;
         const int nc = min(NA, P.n_sel - kb);
-        if (tid < nc) {
-            const int k = kb + tid;
-            const AngleTab t = P.tab[P.sel_angle[k]];
-            // d(b, r, c) = sigma*b + ar*r + ac*c + a0
-            const double ar = t.branch ? -1.0 : t.m;
-            const double ac = t.branch ? t.m : -1.0;
-            const double bf00 = -(ar * r0 + ac * c0 + t.a0) / t.sigma;
-            const double bref = floor(bf00);
-            const double br = -ar / t.sigma, bc = -ac / t.sigma;
-            const double e0 = bf00 - bref;
-            // local crossing range over the tile corners
-            const double v1 = e0 + br * (TR - 1), v2 = e0 + bc * (TC - 1);
-            const double v3 = e0 + br * (TR - 1) + bc * (TC - 1);
-            const double lo = fmin(fmin(e0, v1), fmin(v2, v3));
-            const int jlo = (int)floor(lo) - P.cand_half - 1;
-            s_br[tid] = (float)br;
-            s_bc[tid] = (float)bc;
-            s_e0[tid] = (float)e0;
-            s_sg[tid] = (float)fabs(t.sigma);
-            s_off[tid] = -jlo;  // slot index of local bin 0
-            s_bbase[tid] = (int)bref + jlo;  // global bin of slot index 0
-            s_step[tid] = t.step_len;
-        }
-        __syncthreads();
-        // stage the touched bins (scaled by step_len), zero outside [0, B):
-        // one warp per angle, lanes along the bins (coalesced)
-        float* sl = slots;
-        {
-            constexpr int NW = NT / 32;
-            const int warp = tid >> 5, lane = tid & 31;
-            for (int a = warp; a < nc; a += NW) {
-                const int k = kb + a;
-                const int bb = s_bbase[a];
-                const float stp = s_step[a];
-                const float* yrow = P.y + ((size_t)k * P.Z + z) * P.B;
-                float* dst = sl + a * P.slot;
-                for (int j = lane; j < P.slot; j += 32) {
-                    const int b = bb + j;
-                    dst[j] = (b >= 0 && b < P.B) ? __ldg(yrow + b) * stp : 0.f;
-                }
-            }
+        if (P.nbuf == 2 && ci + 1 < n_chunks) {
+            prepare(kb + NA, buf ^ 1);
+            cp_async_wait_one();
+        } else {
+            cp_async_wait_all();
         }
         __syncthreads();
         if (TWO_TAP) {
-            // packed pairs of pixels (rows rg + 4(2jj), rg + 4(2jj+1))
             f2 acc2[PIX / 2];
 #pragma unroll
             for (int jj = 0; jj < PIX / 2; ++jj) acc2[jj] = pk(0.f, 0.f);
-            const f2 mg2 = pk(kMagic, kMagic), one2 = pk(1.f, 1.f);
-            const uint32_t sl_u32 = smem_u32(sl) - (uint32_t)kMagicBits * 4u;
-            f2 rr[PIX / 2];
-#pragma unroll
-            for (int jj = 0; jj < PIX / 2; ++jj)
-                rr[jj] = pk((float)(rg + (2 * jj) * ROWSTEP), (float)(rg + (2 * jj + 1) * ROWSTEP));
-            const float clf = (float)cl;
 #pragma unroll 1
             for (int a = 0; a < nc; ++a) {
-                const float br = s_br[a], sg = s_sg[a];
-                const float cterm = fmaf(clf, s_bc[a], s_e0[a]);
-                const uint32_t yb = opaque(sl_u32 + (uint32_t)(a * P.slot + s_off[a]) * 4u);
+                const float br = s_br[buf][a], S1 = s_S1[buf][a], A0 = s_A0[buf][a];
+                const float cterm = fmaf(clf, s_bc[buf][a], s_e0[buf][a]);
+                const uint32_t yb = s_yaddr[buf][a];
                 const f2 ct2 = pk(cterm, cterm), br2 = pk(br, br);
-                const f2 nsg2 = pk(-sg, -sg), sg2 = pk(sg, sg), oms2 = pk(1.f - sg, 1.f - sg);
+                const f2 nS1 = pk(-S1, -S1), S12 = pk(S1, S1), A02 = pk(A0, A0),
+                         A0mS1 = pk(A0 - S1, A0 - S1);
 #pragma unroll
                 for (int jj = 0; jj < PIX / 2; ++jj) {
                     const f2 bl = fma2(rr[jj], br2, ct2);
                     const f2 t = add2_rm(bl, mg2);
                     const f2 phi = sub2(bl, sub2(t, mg2));
-                    f2 w0 = fma2(nsg2, phi, one2);
-                    f2 w1 = fma2(sg2, phi, oms2);
+                    // step_len * hat(pos_b - lane) for b = floor(b_f), floor(b_f) + 1
+                    f2 w0 = fma2(nS1, phi, A02);
+                    f2 w1 = fma2(S12, phi, A0mS1);
                     float w0a, w0b, w1a, w1b, ta, tb, y0a, y1a, y0b, y1b;
                     upk(w0, w0a, w0b);
                     upk(w1, w1a, w1b);
@@ -756,13 +776,14 @@ __global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
                 acc_o[2 * jj + 1] += a1;
             }
         } else {
+            const float* sl = smem + buf * NA * P.slot;
             float acc_i[PIX];
 #pragma unroll
             for (int j = 0; j < PIX; ++j) acc_i[j] = 0.f;
             for (int a = 0; a < nc; ++a) {
-                const float br = s_br[a], sg = s_sg[a];
-                const float cterm = fmaf((float)cl, s_bc[a], s_e0[a]);
-                const int ybase = a * P.slot + s_off[a] - kMagicBits;
+                const float br = s_br[buf][a], S1 = s_S1[buf][a], A0 = s_A0[buf][a];
+                const float cterm = fmaf(clf, s_bc[buf][a], s_e0[buf][a]);
+                const int ybase = a * P.slot + s_off[buf][a] - kMagicBits;
 #pragma unroll
                 for (int j = 0; j < PIX; ++j) {
                     const float bl = fmaf((float)(rg + j * ROWSTEP), br, cterm);
@@ -770,7 +791,7 @@ __global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
                     const float phi = bl - (tt - kMagic);
                     const float* yp = sl + (ybase + __float_as_int(tt));
                     for (int q = -P.cand_half + 1; q <= P.cand_half; ++q) {
-                        const float w = fmaxf(0.f, 1.f - sg * fabsf((float)q - phi));
+                        const float w = fmaxf(0.f, A0 - S1 * fabsf((float)q - phi));
                         acc_i[j] = fmaf(w, yp[q], acc_i[j]);
                     }
                 }
@@ -780,12 +801,15 @@ __global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
         }
         __syncthreads();
     }
+    if (n_chunks == 0 && P.n_epi) cp_async_wait_all();
 
     const int c = c0 + cl;
     if (c >= P.W) return;
+    const float* epi = smem + P.nbuf * NA * P.slot;
 #pragma unroll
     for (int j = 0; j < PIX; ++j) {
-        const int r = r0 + rg + j * ROWSTEP;
+        const int rl = rg + j * ROWSTEP;
+        const int r = r0 + rl;
         if (r >= P.H) continue;
         const size_t p = (size_t)z * plane + (size_t)r * P.W + c;
         if (P.mode == 0) {
@@ -793,7 +817,10 @@ __global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
             if (P.accumulate) v += P.out[p];
             P.out[p] = v;
         } else {
-            step_epilogue(P.ep, p, acc_o[j]);
+            const int e = rl * TC + cl;
+            step_epilogue_vals(P.ep, p, acc_o[j], epi[e], epi[TR * TC + e],
+                               P.n_epi > 2 ? epi[2 * TR * TC + e] : 0.f,
+                               P.n_epi > 3 ? epi[3 * TR * TC + e] : 0.f);
         }
     }
 }
@@ -810,7 +837,7 @@ static constexpr int kTR = 32, kTC = 64, kNT = 256, kNA = 32;
 template <bool TWO>
 static int run_gather(pt_plan* plan, const AdjArgs& a, cudaStream_t st)
 {
-    const size_t smem = (size_t)(kNA * a.slot) * sizeof(float);
+    const size_t smem = (size_t)(a.nbuf * kNA * a.slot + a.n_epi * kTR * kTC) * sizeof(float);
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
         PT_CHECK_CUDA(cudaFuncSetAttribute(adj_gather_kernel<kTR, kTC, kNT, kNA, TWO>,
@@ -837,11 +864,19 @@ int launch_adjoint(pt_plan* plan, const pt_selection* sel, const float* y, float
     a.H = plan->H; a.W = plan->W; a.Z = plan->Z; a.B = plan->B;
     a.slot = plan->gather_slot;
     a.cand_half = plan->cand_half;
+    a.nbuf = sel->n > kNA ? 2 : 1;
     a.alpha = alpha;
     a.accumulate = accumulate;
     a.out = x_out;
     a.mode = ep ? 1 : 0;
-    if (ep) a.ep = *ep; else memset(&a.ep, 0, sizeof(a.ep));
+    if (ep) {
+        a.ep = *ep;
+        a.n_epi = ep->estimator == PT_EST_SAGA ? 4
+                : (ep->estimator == PT_EST_SVRG || ep->estimator == PT_EST_LSVRG) ? 3 : 2;
+    } else {
+        memset(&a.ep, 0, sizeof(a.ep));
+        a.n_epi = 0;
+    }
     if (plan->cand_half == 1) return run_gather<true>(plan, a, st);
     return run_gather<false>(plan, a, st);
 }

@@ -24,6 +24,8 @@ namespace pt {
 struct AngleTab {
     double sigma, m, a0;
     double isig, im;  // 1/sigma, 1/m (0 when m == 0)
+    // gather: crossing bin b_f(r, c) = gbr*r + gbc*c + gg, where pos(b_f) == lane
+    double gbr, gbc, gg;
     float step_len;
     int branch;
 };
