@@ -219,6 +219,10 @@ int pt_session_profile(pt_session* s, double* host_ms, int64_t* host_calls);
 int pt_nccl_unique_id(const char* nccl_path, uint8_t* host_out128);
 int pt_session_attach_nccl(pt_session* s, const char* nccl_path, const uint8_t* host_id128,
                            int32_t rank, int32_t world);
+/* Test hook: run the angle-sector decomposition of `world` ranks on this one
+ * device (each sector's partial A_i^T r computed separately and summed, which
+ * is exactly what ncclAllReduce sums across real ranks).  Call before run. */
+int pt_session_emulate_sectors(pt_session* s, int32_t world);
 
 #ifdef __cplusplus
 }

@@ -138,6 +138,10 @@ struct pt_session {
     double dual_weight = 0.0;
     std::vector<pt_selection*> subsets;  // (own rows of) subset i
     pt_selection* own_all = nullptr;     // all (own) angles
+    // test hook: G virtual angle sectors on one device (sums what the ranks' allreduce sums)
+    int emu = 1;
+    std::vector<std::vector<pt_selection*>> emu_subsets;  // [sector][subset]
+    std::vector<pt_selection*> emu_all;                    // [sector]
     // NCCL
     NcclApi nccl;
     nccl_comm comm = nullptr;
@@ -206,6 +210,21 @@ int full_gradient(pt_session* s, const float* x, float* out, float* res, cudaStr
     pt_plan* P = s->plan;
     int rc = pt::launch_forward(P, &s->ws, s->own_all, x, nullptr, s->data, res, nullptr, st);
     if (rc) return rc;
+    if (s->emu > 1) {
+        // virtual sectors: each sector's A_S^T over the shared residual, summed
+        for (int g = 0; g < s->emu; ++g) {
+            const pt_selection* sg = s->emu_all[g];
+            if (sg->n == 0) {
+                if (g == 0) PT_CHECK_CUDA(cudaMemsetAsync(out, 0, s->n * 4, st));
+                continue;
+            }
+            // the residual rows of sector g start at its first angle
+            const size_t off = (size_t)sg->h_angle[0] * P->Z * P->B;
+            rc = pt::launch_adjoint(P, sg, res + off, out, 1.f, g > 0, nullptr, st);
+            if (rc) return rc;
+        }
+        return PT_OK;
+    }
     if (s->own_all->n == 0) {
         PT_CHECK_CUDA(cudaMemsetAsync(out, 0, s->n * 4, st));
     } else {
@@ -348,7 +367,9 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
         const int theta = (p >= 1.0) ? 1 : (host_theta ? host_theta[j] : 0);
 
         // forward: residual rows of the (own part of the) selection
-        if (vr)  // A_i (x - x_snap) = (A_i x - b_i) - (A_i x_snap - b_i)
+        if (s->emu > 1)
+            ;  // per virtual sector below
+        else if (vr)  // A_i (x - x_snap) = (A_i x - b_i) - (A_i x_snap - b_i)
             rc = pt::launch_forward(P, &s->ws, sel, xc, nullptr, s->data, s->r, nullptr, st,
                                     rsnap_by_angle(s));
         else
@@ -375,7 +396,24 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
         ep.v_out = s->v;
         ep.xhat_out = s->xhat;
         ep.bad_iter = s->bad;
-        if (s->world == 1) {
+        if (s->emu > 1) {
+            // virtual ranks: partial A_i^T r per sector, summed in g, then the epilogue
+            for (int g = 0; g < s->emu && !rc; ++g) {
+                const pt_selection* sg = (d.estimator == PT_EST_FULL) ? s->emu_all[g]
+                                                                      : s->emu_subsets[g][i];
+                if (sg->n == 0) {
+                    if (g == 0) PT_CHECK_CUDA(cudaMemsetAsync(s->g, 0, s->n * 4, st));
+                    continue;
+                }
+                if (vr)
+                    rc = pt::launch_forward(P, &s->ws, sg, xc, nullptr, s->data, s->r, nullptr, st,
+                                            rsnap_by_angle(s));
+                else
+                    rc = pt::launch_forward(P, &s->ws, sg, xc, nullptr, s->data, s->r, nullptr, st);
+                if (!rc) rc = pt::launch_adjoint(P, sg, s->r, s->g, 1.f, g > 0, nullptr, st, &s->ws);
+            }
+            if (!rc) rc = pt::launch_epilogue(P, s->g, &ep, st);
+        } else if (s->world == 1) {
             rc = pt::launch_adjoint(P, sel, s->r, nullptr, 1.f, 0, &ep, st, &s->ws);
         } else {
             if (sel->n == 0) {
@@ -466,6 +504,36 @@ int pt_nccl_unique_id(const char* nccl_path, uint8_t* host_out128)
     int e = api.get_uid(&id);
     if (e != 0) { pt::set_error("ncclGetUniqueId failed (%d)", e); return PT_ENCCL; }
     memcpy(host_out128, id.internal, 128);
+    return PT_OK;
+}
+
+int pt_session_emulate_sectors(pt_session* s, int32_t world)
+{
+    if (!s || world < 1) { pt::set_error("bad argument"); return PT_EINVAL; }
+    if (s->world != 1) { pt::set_error("session already attached to NCCL"); return PT_EINVAL; }
+    pt_plan* P = s->plan;
+    const int A = P->A;
+    s->emu_subsets.assign(world, {});
+    s->emu_all.assign(world, nullptr);
+    for (int g = 0; g < world; ++g) {
+        const int lo = (int)((long long)A * g / world), hi = (int)((long long)A * (g + 1) / world);
+        std::vector<int32_t> own;
+        for (int a = lo; a < hi; ++a) own.push_back(a);
+        int rc = pt_selection_create(P, own.data(), (int32_t)own.size(), &s->emu_all[g]);
+        if (rc) return rc;
+        if (s->d.estimator != PT_EST_FULL) {
+            for (int k = 0; k < s->d.n_subsets; ++k) {
+                std::vector<int32_t> idx;
+                for (int a = k; a < A; a += s->d.n_subsets)
+                    if (a >= lo && a < hi) idx.push_back(a);
+                pt_selection* sel = nullptr;
+                rc = pt_selection_create(P, idx.data(), (int32_t)idx.size(), &sel);
+                if (rc) return rc;
+                s->emu_subsets[g].push_back(sel);
+            }
+        }
+    }
+    s->emu = world;
     return PT_OK;
 }
 

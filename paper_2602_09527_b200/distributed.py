@@ -45,14 +45,31 @@ def attach(session, rank: int | None = None, world: int | None = None,
     if world == 1:
         return
     path = nccl_library_path().encode()
-    uid = (ctypes.c_uint8 * 128)()
-    if rank == 0:
+
+    def make_uid() -> bytes:
+        uid = (ctypes.c_uint8 * 128)()
         N.check(N.lib().pt_nccl_unique_id(path, uid), "ncclGetUniqueId")
-    payload = [bytes(uid)]
-    dist.broadcast_object_list(payload, src=0, group=group)
-    uid = (ctypes.c_uint8 * 128)(*payload[0])
+        return bytes(uid)
+
+    payload = share_unique_id(make_uid, rank, group)
+    uid = (ctypes.c_uint8 * 128)(*payload)
     N.check(N.lib().pt_session_attach_nccl(session.handle, path, uid, rank, world),
             "attach_nccl")
+
+
+def share_unique_id(make_uid, rank: int, group=None) -> bytes:
+    """Rank 0 creates the 128-byte NCCL unique id, every rank receives it."""
+    payload = [make_uid() if rank == 0 else None]
+    dist.broadcast_object_list(payload, src=0, group=group)
+    uid = payload[0]
+    if not isinstance(uid, (bytes, bytearray)) or len(uid) != 128:
+        raise RuntimeError("bad NCCL unique id")
+    return bytes(uid)
+
+
+def emulate_sectors(session, world: int) -> None:
+    """Single-device emulation of `world` angle-sector ranks (test hook)."""
+    N.check(N.lib().pt_session_emulate_sectors(session.handle, int(world)), "emulate")
 
 
 def replicas_identical(x: torch.Tensor, group=None) -> bool:
