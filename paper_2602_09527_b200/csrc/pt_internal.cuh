@@ -5,7 +5,9 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -120,6 +122,9 @@ struct pt_plan {
     std::mutex mu;
     std::vector<pt_selection*> selections;
     pt_selection* all = nullptr;
+    // (n_subsets, lo, hi) -> (sector selection, subset selections of the sector)
+    std::map<std::tuple<int, int, int>,
+             std::pair<pt_selection*, std::vector<pt_selection*>>> sector_cache;
 };
 
 namespace pt {

@@ -131,6 +131,7 @@ struct pt_session {
     float* r = nullptr;      // residual rows (largest selection)
     float* rsnap = nullptr;  // SVRG: A x_snap - b over the owned angles (snapshot residual)
     float* g = nullptr;  // partial gradient (multi-GPU)
+    float* slab = nullptr;  // backing allocation of the buffers above
     int64_t* bad = nullptr;
     pt::Workspace ws;
     pt::Profiler prof;
@@ -156,37 +157,58 @@ int alloc_f(float** p, size_t n)
     return PT_OK;
 }
 
-// Selections of this rank: subset k = {k, k+N, ...} (geometry.py:75-82)
-// restricted to the owned angle sector.
+// Selections of angles [lo, hi): subset k = {k, k+N, ...} (geometry.py:75-82)
+// restricted to the sector; cached in the plan (a session or a rank reuses them).
+int sector_selections(pt_plan* P, int n_subsets, int lo, int hi, pt_selection** all_out,
+                      std::vector<pt_selection*>* subs_out)
+{
+    {
+        std::lock_guard<std::mutex> g(P->mu);
+        auto it = P->sector_cache.find({n_subsets, lo, hi});
+        if (it != P->sector_cache.end()) {
+            *all_out = it->second.first;
+            *subs_out = it->second.second;
+            return PT_OK;
+        }
+    }
+    const int A = P->A;
+    pt_selection* all = nullptr;
+    std::vector<pt_selection*> subs;
+    int rc;
+    if (lo == 0 && hi == A) {
+        all = P->all;
+    } else {
+        std::vector<int32_t> own;
+        for (int a = lo; a < hi; ++a) own.push_back(a);
+        rc = pt_selection_create(P, own.data(), (int32_t)own.size(), &all);
+        if (rc) return rc;
+    }
+    for (int k = 0; k < n_subsets; ++k) {
+        std::vector<int32_t> idx;
+        for (int a = k; a < A; a += n_subsets)
+            if (a >= lo && a < hi) idx.push_back(a);
+        pt_selection* sel = nullptr;
+        rc = pt_selection_create(P, idx.data(), (int32_t)idx.size(), &sel);
+        if (rc) return rc;
+        subs.push_back(sel);
+    }
+    {
+        std::lock_guard<std::mutex> g(P->mu);
+        P->sector_cache[{n_subsets, lo, hi}] = {all, subs};
+    }
+    *all_out = all;
+    *subs_out = subs;
+    return PT_OK;
+}
+
 int build_selections(pt_session* s)
 {
     pt_plan* P = s->plan;
     const int A = P->A;
     const int lo = (int)((long long)A * s->rank / s->world);
     const int hi = (int)((long long)A * (s->rank + 1) / s->world);
-    std::vector<int32_t> own;
-    for (int a = lo; a < hi; ++a) own.push_back(a);
-    int rc;
-    if (s->world == 1) {
-        s->own_all = P->all;
-    } else {
-        rc = pt_selection_create(P, own.data(), (int32_t)own.size(), &s->own_all);
-        if (rc) return rc;
-    }
-    s->subsets.clear();
-    if (s->d.estimator != PT_EST_FULL) {
-        const int N = s->d.n_subsets;
-        for (int k = 0; k < N; ++k) {
-            std::vector<int32_t> idx;
-            for (int a = k; a < A; a += N)
-                if (a >= lo && a < hi) idx.push_back(a);
-            pt_selection* sel = nullptr;
-            rc = pt_selection_create(P, idx.data(), (int32_t)idx.size(), &sel);
-            if (rc) return rc;
-            s->subsets.push_back(sel);
-        }
-    }
-    return PT_OK;
+    const int n = (s->d.estimator != PT_EST_FULL) ? s->d.n_subsets : 0;
+    return sector_selections(P, n, lo, hi, &s->own_all, &s->subsets);
 }
 
 int allreduce(pt_session* s, float* buf, cudaStream_t st)
@@ -271,7 +293,9 @@ int pt_session_create(pt_plan* plan, const pt_solver_desc* desc, const float* da
     s->n = (size_t)plan->Z * plan->H * plan->W;
     const size_t n = s->n;
     int rc = PT_OK;
-    auto A = [&](float** p, size_t cnt) { if (rc == PT_OK) rc = alloc_f(p, cnt); };
+    // one slab for all state buffers (256-byte aligned carve-outs)
+    std::vector<std::pair<float**, size_t>> req;
+    auto A = [&](float** p, size_t cnt) { req.push_back({p, (std::max<size_t>(1, cnt) + 63) & ~size_t(63)}); };
     A(&s->x[0], n); A(&s->x[1], n); A(&s->h, n); A(&s->v, n); A(&s->xhat, n);
     if (desc->estimator == PT_EST_SVRG || desc->estimator == PT_EST_LSVRG) {
         A(&s->snap, n); A(&s->fg, n);
@@ -285,6 +309,20 @@ int pt_session_create(pt_plan* plan, const pt_solver_desc* desc, const float* da
     }
     A(&s->r, (size_t)plan->A * plan->Z * plan->B);
     A(&s->g, n);
+    {
+        size_t total = 0;
+        for (auto& q : req) total += q.second;
+        if (cudaMalloc(&s->slab, total * sizeof(float)) != cudaSuccess) {
+            pt::set_error("session allocation of %zu bytes failed", total * sizeof(float));
+            rc = PT_ECUDA;
+        } else {
+            size_t off = 0;
+            for (auto& q : req) {
+                *q.first = s->slab + off;
+                off += q.second;
+            }
+        }
+    }
     if (rc == PT_OK && cudaMalloc(&s->bad, sizeof(int64_t)) != cudaSuccess) rc = PT_ECUDA;
     if (rc == PT_OK) rc = pt::workspace_alloc(plan, &s->ws);
     s->ws.prof = &s->prof;
@@ -310,10 +348,7 @@ int pt_session_destroy(pt_session* s)
 {
     if (!s) return PT_OK;
     cudaDeviceSynchronize();
-    float* bufs[] = {s->x[0], s->x[1], s->h, s->v, s->xhat, s->snap, s->fg, s->saga_table,
-                     s->saga_sum, s->dp, s->dq, s->dw, s->fgp_work, s->r, s->g, s->rsnap};
-    for (float* b : bufs)
-        if (b) cudaFree(b);
+    if (s->slab) cudaFree(s->slab);
     if (s->bad) cudaFree(s->bad);
     pt::workspace_free(&s->ws);
     if (s->comm && s->nccl.destroy) s->nccl.destroy(s->comm);
@@ -515,23 +550,11 @@ int pt_session_emulate_sectors(pt_session* s, int32_t world)
     const int A = P->A;
     s->emu_subsets.assign(world, {});
     s->emu_all.assign(world, nullptr);
+    const int n = (s->d.estimator != PT_EST_FULL) ? s->d.n_subsets : 0;
     for (int g = 0; g < world; ++g) {
         const int lo = (int)((long long)A * g / world), hi = (int)((long long)A * (g + 1) / world);
-        std::vector<int32_t> own;
-        for (int a = lo; a < hi; ++a) own.push_back(a);
-        int rc = pt_selection_create(P, own.data(), (int32_t)own.size(), &s->emu_all[g]);
+        int rc = sector_selections(P, n, lo, hi, &s->emu_all[g], &s->emu_subsets[g]);
         if (rc) return rc;
-        if (s->d.estimator != PT_EST_FULL) {
-            for (int k = 0; k < s->d.n_subsets; ++k) {
-                std::vector<int32_t> idx;
-                for (int a = k; a < A; a += s->d.n_subsets)
-                    if (a >= lo && a < hi) idx.push_back(a);
-                pt_selection* sel = nullptr;
-                rc = pt_selection_create(P, idx.data(), (int32_t)idx.size(), &sel);
-                if (rc) return rc;
-                s->emu_subsets[g].push_back(sel);
-            }
-        }
     }
     s->emu = world;
     return PT_OK;
