@@ -191,7 +191,9 @@ def main():
         # final image as float32 plus the row columns
         c1 = config_run("c1", record_objective=False)
         c1["c1_image"] = c1["c1_image"].astype(np.float32)
-        c1["c1_b"] = c1["c1_b"].astype(np.float64)
+        # b is not stored (size cap): tests regenerate it with the pinned oracle
+        # forward (<= 1e-14 of the reference's) and the same noise draw
+        del c1["c1_b"]
         np.savez_compressed(os.path.join(HERE, "reference_c1.npz"), **c1)
         print("c1 reference work_seconds", float(c1["c1_work_seconds"]))
 

@@ -198,3 +198,27 @@ def test_angle_sector_decomposition_matches_single_rank(est, world):
         st.session.run(subs, th, rf, 0)
         outs.append(cpu(st.x))
     assert rel_l2(outs[1], outs[0]) <= 1e-5
+
+
+def test_config1_whole_run_matches_reference(oracle):
+    """BASELINE config 1 whole: 512^2, 720x768, SAGA N=20 (20x512^2 table),
+    p=0.05, FGP 100, 100 epochs = 2000 iterations, against the reference's
+    own run (tests/golden/reference_c1.npz; b regenerated with the pinned
+    oracle)."""
+    import os
+    from conftest import GOLDEN
+    from test_oracle import config1_problem
+    c1 = np.load(os.path.join(GOLDEN, "reference_c1.npz"))
+    cfg, g, b = config1_problem(oracle)
+    proj = Projector(g, cfg.size, cfg.size)
+    tv = TvProxConfig(alpha=float(c1["c1_alpha"]), inner_iterations=cfg.fgp_inner)
+    problem = TomoProblem(proj, b, tv=tv)
+    scfg = SolverConfig(gamma=float(c1["c1_gamma"]), skip_probability=cfg.p,
+                        n_subsets=cfg.n_subsets, estimator=cfg.estimator,
+                        max_data_passes=cfg.max_data_passes, seed=cfg.solver_seed)
+    rec = run(scfg, problem)
+    assert rel_l2(cpu(rec.image), c1["c1_image"]) <= TOL
+    assert np.array_equal(rec.column("data_passes"), c1["c1_passes"])
+    assert np.array_equal(rec.column("prox_calls"), c1["c1_prox"])
+    assert rec.iterations == list(c1["c1_iters"])
+    assert proj.norm_sq(50, 0) == pytest.approx(float(c1["c1_L"]), rel=1e-5)
