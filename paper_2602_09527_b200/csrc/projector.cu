@@ -110,9 +110,9 @@ struct FwdArgs {
 
 template <int TY, int TX>
 struct FwdTile {
-    static constexpr int HL = TY / 2 + 3;
+    static constexpr int HL = ((TY / 2 + 3) + 3) & ~3;     // halo, a multiple of 4 lanes
     static constexpr int NL = TX + 2 * HL;                 // lanes staged per band
-    static constexpr int PITCH_R = NL | 1;                  // row branch: [TY][PITCH_R]
+    static constexpr int PITCH_R = NL + 4;                  // row branch: [TY][PITCH_R], 16-B rows
     static constexpr int PITCH_C = TY + 1;                  // column branch: [NL][PITCH_C]
     static constexpr int BUF = (TY * PITCH_R > NL * PITCH_C) ? TY * PITCH_R : NL * PITCH_C;
     static constexpr int SMEM = BUF * 4;
@@ -172,7 +172,18 @@ __device__ __forceinline__ void stage_tile(const FwdArgs& P, const FwdItem& it, 
     const int s0 = it.band * TY;
     const int lane_org = it.tile * TX - T::HL;
     const float* img = P.x + (size_t)it.z * P.H * P.W;
-    if (it.branch == 0) {
+    if (it.branch == 0 && (P.W & 3) == 0) {
+        // [st][ll] = img[s0 + st][lane_org + ll]: 16-byte copies (lane_org and
+        // W are multiples of 4), zero-filled outside the image
+        constexpr int NQ = T::NL / 4;
+        for (int idx = threadIdx.x; idx < TY * NQ; idx += NT) {
+            const int st = idx / NQ, qq = idx - st * NQ;
+            const int r = s0 + st, c = lane_org + 4 * qq;
+            const int nvalid = (r < P.H && c >= 0) ? max(0, min(4, P.W - c)) : 0;
+            cp_async16(buf + (uint32_t)(st * T::PITCH_R + 4 * qq) * 4u,
+                       img + (nvalid ? (size_t)r * P.W + c : 0), 4 * nvalid);
+        }
+    } else if (it.branch == 0) {
         // [st][ll] = img[s0 + st][lane_org + ll]: a warp per tile row
         for (int st = warp; st < TY; st += NW) {
             const int r = s0 + st;
@@ -266,7 +277,7 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
     __shared__ int s_pref[CH + 1];
     __shared__ int s_blo[CH];
     __shared__ int s_k[CH];
-    __shared__ double s_a0[CH], s_sig[CH], s_m[CH], s_im[CH];
+    __shared__ float s_plb[CH], s_sig[CH], s_m[CH], s_im[CH];
 
     const int tid = threadIdx.x;
     const FwdItem it = decode_item(P, blockIdx.x);
@@ -315,10 +326,12 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
                 cnt = (int)max(0LL, bhi - blo);
                 s_blo[tid] = (int)blo;
                 s_k[tid] = k;
-                s_a0[tid] = t.a0;
-                s_sig[tid] = t.sigma;
-                s_m[tid] = t.m;
-                s_im[tid] = t.im;
+                // tile-local lane position of ray blo at step 0 (float64 -> float32;
+                // per ray only (b - blo) * sigma, |.| <~ TX, is added in float32)
+                s_plb[tid] = (float)(t.a0 + (double)blo * t.sigma + (double)s0 * t.m - (double)lane_org);
+                s_sig[tid] = (float)t.sigma;
+                s_m[tid] = (float)t.m;
+                s_im[tid] = (float)t.im;
             }
             int v = cnt;  // inclusive warp scan of the ray counts
 #pragma unroll
@@ -338,23 +351,23 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
         int j = 0;
         for (int w = tid; w < total; w += NT) {
             while (w >= s_pref[j + 1]) ++j;
-            const int b = s_blo[j] + (w - s_pref[j]);
-            const double m = s_m[j];
-            // global lane position at st = 0
-            const double P0 = s_a0[j] + (double)b * s_sig[j] + (double)s0 * m;
-            // steps where pos in [-1.5, n_lanes + 0.5]: outside, both taps are zero
+            const int db = w - s_pref[j];
+            const int b = s_blo[j] + db;
+            const float mf = s_m[j];
+            const float pl = fmaf((float)db, s_sig[j], s_plb[j]);  // tile-local lane at st = 0
+            // steps where pos in [-1.5, n_lanes + 0.5] (global lanes): outside,
+            // both taps are zero (float32 is ample for a 0.5-lane margin)
+            const float P0 = pl + (float)lane_org;
             int st_a = 0, st_b = ty_valid;
-            if (s_im[j] == 0.0) {
-                if (P0 < -1.5 || P0 > n_lanes + 0.5) st_b = 0;
+            const float im = s_im[j];
+            if (im == 0.f) {
+                if (P0 < -1.5f || P0 > n_lanes + 0.5f) st_b = 0;
             } else {
-                const double im = s_im[j];
-                const double e1 = (-1.5 - P0) * im, e2 = ((double)n_lanes + 0.5 - P0) * im;
-                const double lo = fmin(e1, e2), hi = fmax(e1, e2);
-                st_a = max(st_a, (int)ceil(fmin(fmax(lo, -1.0), (double)TY + 1.0)));
-                st_b = min(st_b, (int)floor(fmin(fmax(hi, -2.0), (double)TY + 1.0)) + 1);
+                const float e1 = (-1.5f - P0) * im, e2 = ((float)n_lanes + 0.5f - P0) * im;
+                const float lo = fminf(e1, e2), hi = fmaxf(e1, e2);
+                st_a = max(st_a, (int)ceilf(fminf(fmaxf(lo, -1.f), (float)TY + 1.f)));
+                st_b = min(st_b, (int)floorf(fminf(fmaxf(hi, -2.f), (float)TY + 1.f)) + 1);
             }
-            const float pl = (float)(P0 - (double)lane_org);  // tile-local lane position
-            const float mf = (float)m;
             const float acc = branch == 0
                 ? ray_band_sum<4, T::PITCH_R * 4>(tile_u32, st_a, st_b, pl, mf)
                 : ray_band_sum<T::PITCH_C * 4, 4>(tile_u32, st_a, st_b, pl, mf);
