@@ -275,9 +275,8 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
     extern __shared__ float sm[];
     constexpr int CH = 32;
     __shared__ int s_pref[CH + 1];
-    __shared__ int s_blo[CH];
-    __shared__ int s_k[CH];
-    __shared__ float s_plb[CH], s_sig[CH], s_m[CH], s_im[CH];
+    __shared__ int2 s_bk[CH];       // {first owned ray, selection slot}
+    __shared__ float4 s_ray[CH];    // {tile-local lane of ray blo at st 0, sigma, m, 1/m}
 
     const int tid = threadIdx.x;
     const FwdItem it = decode_item(P, blockIdx.x);
@@ -324,14 +323,12 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
                 blo = max(blo, 0LL);
                 bhi = min(bhi, (long long)P.B);
                 cnt = (int)max(0LL, bhi - blo);
-                s_blo[tid] = (int)blo;
-                s_k[tid] = k;
+                s_bk[tid] = make_int2((int)blo, k);
                 // tile-local lane position of ray blo at step 0 (float64 -> float32;
                 // per ray only (b - blo) * sigma, |.| <~ TX, is added in float32)
-                s_plb[tid] = (float)(t.a0 + (double)blo * t.sigma + (double)s0 * t.m - (double)lane_org);
-                s_sig[tid] = (float)t.sigma;
-                s_m[tid] = (float)t.m;
-                s_im[tid] = (float)t.im;
+                s_ray[tid] = make_float4(
+                    (float)(t.a0 + (double)blo * t.sigma + (double)s0 * t.m - (double)lane_org),
+                    (float)t.sigma, (float)t.m, (float)t.im);
             }
             int v = cnt;  // inclusive warp scan of the ray counts
 #pragma unroll
@@ -352,14 +349,16 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
         for (int w = tid; w < total; w += NT) {
             while (w >= s_pref[j + 1]) ++j;
             const int db = w - s_pref[j];
-            const int b = s_blo[j] + db;
-            const float mf = s_m[j];
-            const float pl = fmaf((float)db, s_sig[j], s_plb[j]);  // tile-local lane at st = 0
+            const int2 bk = s_bk[j];
+            const float4 ry = s_ray[j];
+            const int b = bk.x + db;
+            const float mf = ry.z;
+            const float pl = fmaf((float)db, ry.y, ry.x);  // tile-local lane at st = 0
             // steps where pos in [-1.5, n_lanes + 0.5] (global lanes): outside,
             // both taps are zero (float32 is ample for a 0.5-lane margin)
             const float P0 = pl + (float)lane_org;
             int st_a = 0, st_b = ty_valid;
-            const float im = s_im[j];
+            const float im = ry.w;
             if (im == 0.f) {
                 if (P0 < -1.5f || P0 > n_lanes + 0.5f) st_b = 0;
             } else {
@@ -371,7 +370,7 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
             const float acc = branch == 0
                 ? ray_band_sum<4, T::PITCH_R * 4>(tile_u32, st_a, st_b, pl, mf)
                 : ray_band_sum<T::PITCH_C * 4, 4>(tile_u32, st_a, st_b, pl, mf);
-            const size_t kk = (size_t)(s_k[j] - P.k_begin);
+            const size_t kk = (size_t)(bk.y - P.k_begin);
             P.partial[(((size_t)it.band * P.n_k + kk) * P.Z + it.z) * P.B + b] = acc;
         }
         __syncthreads();
@@ -642,9 +641,10 @@ __global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
     constexpr int ROWSTEP = NT / TC;
     constexpr int NW = NT / 32;
     extern __shared__ float smem[];
-    __shared__ float s_br[2][NA], s_bc[2][NA], s_e0[2][NA], s_S1[2][NA], s_A0[2][NA];
-    __shared__ int s_off[2][NA], s_bbase[2][NA];
-    __shared__ uint32_t s_yaddr[2][NA];
+    // per-angle tile-frame parameters: {gbr, gbc, e0, S1} and {A0, y address}
+    __shared__ float4 s_p4[2][NA];
+    __shared__ float2 s_p2[2][NA];
+    __shared__ int s_off[2][NA];
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -689,8 +689,12 @@ __global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
     // float32) and the touched sinogram bins (cp.async, zero outside [0, B))
     auto prepare = [&](int kb, int buf) {
         const int nc = min(NA, P.n_sel - kb);
-        if (tid < nc) {
-            const AngleTab& t = P.tab[P.sel_angle[kb + tid]];
+        // one warp per angle: every lane evaluates the angle's tile-frame
+        // parameters (float64 -> float32, identical across lanes), lane 0
+        // publishes them, the lanes stage the touched bins -- no CTA barrier
+        for (int a = warp; a < nc; a += NW) {
+            const int k = kb + a;
+            const AngleTab& t = P.tab[P.sel_angle[k]];
             const double gbr = t.gbr, gbc = t.gbc;
             // crossing bin b_f(r, c) = gbr r + gbc c + gg (pos(b_f) == lane)
             const double bf00 = gbr * r0 + gbc * c0 + t.gg;
@@ -698,30 +702,23 @@ __global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
             const double e0 = bf00 - bref;
             const double lo = e0 + fmin(0.0, gbr) * (TR - 1) + fmin(0.0, gbc) * (TC - 1);
             const int jlo = (int)floor(lo) - P.cand_half - 1;
-            const float stp = t.step_len;
-            s_br[buf][tid] = (float)gbr;
-            s_bc[buf][tid] = (float)gbc;
-            s_e0[buf][tid] = (float)e0;
-            s_A0[buf][tid] = stp;
-            s_S1[buf][tid] = (float)(stp * fabs(t.sigma));
-            // shared byte address of local bin 0 minus the floor-trick offset:
-            // a runtime value, so the compiler keeps it folded in one IMAD
-            s_yaddr[buf][tid] = stage_u32 + (uint32_t)((buf * NA + tid) * P.slot - jlo) * 4u -
-                                (uint32_t)kMagicBits * 4u;
-            s_bbase[buf][tid] = (int)bref + jlo;
-            s_off[buf][tid] = -jlo;
-        }
-        __syncthreads();
-        // staging: one warp per angle, lanes along the bins
-        for (int a = warp; a < nc; a += NW) {
-            const int k = kb + a;
-            const int bb = s_bbase[buf][a];
+            if (lane == 0) {
+                const float stp = t.step_len;
+                s_p4[buf][a] = make_float4((float)gbr, (float)gbc, (float)e0,
+                                           (float)(stp * fabs(t.sigma)));
+                // shared byte address of local bin 0 minus the floor-trick offset
+                const uint32_t ya = stage_u32 + (uint32_t)((buf * NA + a) * P.slot - jlo) * 4u -
+                                    (uint32_t)kMagicBits * 4u;
+                s_p2[buf][a] = make_float2(stp, __uint_as_float(ya));
+                s_off[buf][a] = -jlo;
+            }
+            const int bb = (int)bref + jlo;
             const float* yrow = P.y + ((size_t)k * P.Z + z) * P.B;
             const uint32_t dst = stage_u32 + (uint32_t)((buf * NA + a) * P.slot) * 4u;
             for (int j = lane; j < P.slot; j += 32) {
-                const int b = bb + j;
-                const bool ok = b >= 0 && b < P.B;
-                cp_async4(dst + (uint32_t)j * 4u, yrow + (ok ? b : 0), ok);
+                const int bj = bb + j;
+                const bool ok = bj >= 0 && bj < P.B;
+                cp_async4(dst + (uint32_t)j * 4u, yrow + (ok ? bj : 0), ok);
             }
         }
         cp_async_commit();
@@ -756,9 +753,11 @@ __global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
             for (int jj = 0; jj < PIX / 2; ++jj) acc2[jj] = pk(0.f, 0.f);
 #pragma unroll 1
             for (int a = 0; a < nc; ++a) {
-                const float br = s_br[buf][a], S1 = s_S1[buf][a], A0 = s_A0[buf][a];
-                const float cterm = fmaf(clf, s_bc[buf][a], s_e0[buf][a]);
-                const uint32_t yb = s_yaddr[buf][a];
+                const float4 q4 = s_p4[buf][a];
+                const float2 q2 = s_p2[buf][a];
+                const float br = q4.x, S1 = q4.w, A0 = q2.x;
+                const float cterm = fmaf(clf, q4.y, q4.z);
+                const uint32_t yb = __float_as_uint(q2.y);
                 const f2 ct2 = pk(cterm, cterm), br2 = pk(br, br);
                 const f2 nS1 = pk(-S1, -S1), S12 = pk(S1, S1), A02 = pk(A0, A0),
                          A0mS1 = pk(A0 - S1, A0 - S1);
@@ -794,8 +793,10 @@ __global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
 #pragma unroll
             for (int j = 0; j < PIX; ++j) acc_i[j] = 0.f;
             for (int a = 0; a < nc; ++a) {
-                const float br = s_br[buf][a], S1 = s_S1[buf][a], A0 = s_A0[buf][a];
-                const float cterm = fmaf(clf, s_bc[buf][a], s_e0[buf][a]);
+                const float4 q4 = s_p4[buf][a];
+                const float2 q2 = s_p2[buf][a];
+                const float br = q4.x, S1 = q4.w, A0 = q2.x;
+                const float cterm = fmaf(clf, q4.y, q4.z);
                 const int ybase = a * P.slot + s_off[buf][a] - kMagicBits;
 #pragma unroll
                 for (int j = 0; j < PIX; ++j) {
