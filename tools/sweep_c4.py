@@ -1,0 +1,138 @@
+"""BASELINE config 4 on the GPU: the p x estimator sweep on the config-1 problem
+(512^2, 720 angles x 768 bins, 20 subsets), 100 epochs per cell, reporting
+time-to-objective within 1e-3 relative of a 2000-iteration FISTA reference
+(derived post hoc from the objective rows, as the
+reference has no objective-based stop); plus the projector-only forward +
+adjoint throughput at 4096^2 / 3600 angles / 5800 bins.
+
+    python tools/sweep_c4.py [--fista 2000] [--epochs 100] [--out profiles/sweep_c4.json]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2602_09527_b200 import (ParallelGeometry, Projector, SolverConfig, TomoProblem,  # noqa
+                                   TvProxConfig, default_gamma, fista_gamma, problems, run,
+                                   run_fista)
+
+
+def build_problem():
+    cfg = problems.CONFIGS["c4"]
+    g = ParallelGeometry.uniform(cfg.n_angles, cfg.n_bins)
+    proj = Projector(g, cfg.size, cfg.size)
+    x_true = problems.phantom_for(cfg)
+    clean = proj.forward(x_true).double().cpu().numpy()
+    b = problems.add_noise(clean, cfg.noise, cfg.noise_seed)
+    alpha = problems.alpha_from_backprojection(float(proj.adjoint(b).abs().max()), cfg.n_pixels)
+    lip = proj.norm_sq(cfg.power_iterations, cfg.power_seed)
+    tv = TvProxConfig(alpha=alpha, inner_iterations=cfg.fgp_inner)
+    return cfg, proj, TomoProblem(proj, b, tv=tv), lip, alpha
+
+
+THRESHOLDS = (1e-1, 3e-2, 1e-2, 1e-3)
+
+
+def time_to_target(rec, target):
+    obj = rec.column("objective")
+    wall = rec.column("wall_seconds")
+    passes = rec.column("data_passes")
+    hit = np.nonzero(obj <= target)[0]
+    if len(hit) == 0:
+        return None, None
+    return float(wall[hit[0]]), float(passes[hit[0]])
+
+
+def times_to(rec, f_star):
+    out = {}
+    for t in THRESHOLDS:
+        s, p = time_to_target(rec, f_star * (1.0 + t))
+        out[f"{t:g}"] = {"seconds": s, "passes": p}
+    return out
+
+
+def projector_throughput(size=4096, n_angles=3600, n_bins=5800, reps=3):
+    g = ParallelGeometry.uniform(n_angles, n_bins)
+    proj = Projector(g, size, size)
+    plan = proj.plan
+    x = torch.tensor(problems.ellipse_phantom(size, 30, 9), device="cuda", dtype=torch.float32)
+    y = torch.empty((n_angles, n_bins), device="cuda")
+    out = torch.empty_like(x)
+    plan.forward_into(x, y)
+    plan.adjoint_into(y, out)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record()
+    for _ in range(reps):
+        plan.forward_into(x, y)
+    ev[1].record()
+    for _ in range(reps):
+        plan.adjoint_into(y, out)
+    ev[2].record()
+    torch.cuda.synchronize()
+    t_fwd = ev[0].elapsed_time(ev[1]) / reps / 1e3
+    t_adj = ev[1].elapsed_time(ev[2]) / reps / 1e3
+    nnz = plan.nnz(tuple(range(0, n_angles, 40)))  # 90-angle sample, scaled
+    nnz_full = nnz * 40
+    return {"size": size, "n_angles": n_angles, "n_bins": n_bins,
+            "forward_s": t_fwd, "adjoint_s": t_adj,
+            "nnz_estimate": nnz_full,
+            "forward_operand_GBps": 4 * nnz_full / t_fwd / 1e9,
+            "adjoint_operand_GBps": 4 * nnz_full / t_adj / 1e9,
+            "samples_per_s_fwd": nnz_full / 2 / t_fwd}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--fista", type=int, default=2000)
+    ap.add_argument("--epochs", type=int, default=100)
+    ap.add_argument("--out", default="profiles/sweep_c4.json")
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    cfg, proj, problem, lip, alpha = build_problem()
+    t0 = time.perf_counter()
+    ref = run_fista(SolverConfig(gamma=fista_gamma(lip), max_data_passes=args.fista, seed=0),
+                    problem, record_objective=True)
+    fista_s = time.perf_counter() - t0
+    from paper_2602_09527_b200 import composite_objective
+    f_star = composite_objective(ref.image, problem)
+    target = f_star * (1.0 + 1e-3)
+    cells = []
+    for est in ("full", "sgd", "saga", "svrg"):
+        for p in (1.0, 0.5, 0.1, 0.05, 0.01):
+            passes = args.epochs * (3.0 if est == "svrg" else 1.0)
+            scfg = SolverConfig(gamma=default_gamma(est, lip), skip_probability=p,
+                                n_subsets=cfg.n_subsets if est != "full" else 1, estimator=est,
+                                max_data_passes=passes, seed=0)
+            rec = run(scfg, problem, record_objective=True)
+            tt, tp = time_to_target(rec, target)
+            cells.append({"estimator": est, "p": p, "epochs": args.epochs,
+                          "final_objective": float(rec.column("objective")[-1]),
+                          "final_rel_gap": float(rec.column("objective")[-1] / f_star - 1.0),
+                          "prox_calls": int(rec.column("prox_calls")[-1]),
+                          "work_seconds": float(rec.column("wall_seconds")[-1]),
+                          "time_to_1e-3_s": tt, "passes_to_1e-3": tp,
+                          "time_to_rel_gap": times_to(rec, f_star)})
+            print(json.dumps(cells[-1]), flush=True)
+    result = {"workload": "BASELINE config 4: 512^2, 720x768, 20 subsets, FGP-TV 100",
+              "fista_iterations": args.fista, "fista_seconds": fista_s, "f_star": f_star,
+              "fista_time_to_rel_gap": times_to(ref, f_star),
+              "alpha": alpha, "L": lip, "cells": cells,
+              "projector_4096": projector_throughput()}
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    with open(args.out, "w") as fh:
+        json.dump(result, fh, indent=1)
+    print(json.dumps(result["projector_4096"]))
+
+
+if __name__ == "__main__":
+    main()
