@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
             const size_t kk = (size_t)(bk.y - P.k_begin);
             P.partial[(((size_t)it.band * P.n_k + kk) * P.Z + it.z) * P.B + b] = acc;
         }
-        __syncthreads();
+        if (cbeg + CH < a_end) __syncthreads();  // chunk tables are rewritten next
     }
 }
 
@@ -813,9 +813,12 @@ __global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
 #pragma unroll
             for (int j = 0; j < PIX; ++j) acc_o[j] += acc_i[j];
         }
+        if (ci + 1 < n_chunks) __syncthreads();  // buffers are restaged next
+    }
+    if (n_chunks == 0 && P.n_epi) {
+        cp_async_wait_all();
         __syncthreads();
     }
-    if (n_chunks == 0 && P.n_epi) cp_async_wait_all();
 
     const int c = c0 + cl;
     if (c >= P.W) return;
