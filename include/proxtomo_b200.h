@@ -215,7 +215,8 @@ int pt_session_profile(pt_session* s, double* host_ms, int64_t* host_calls);
  * unique_id: 128 bytes from pt_nccl_unique_id on rank 0, broadcast by the
  * caller.  After attach, the session's per-step subset gradients cover only
  * angles [rank*A/world, (rank+1)*A/world) and are summed by ncclAllReduce on
- * the session stream before the epilogue. */
+ * the session stream before the epilogue (world == 1 runs that path on a
+ * one-rank communicator). */
 int pt_nccl_unique_id(const char* nccl_path, uint8_t* host_out128);
 int pt_session_attach_nccl(pt_session* s, const char* nccl_path, const uint8_t* host_id128,
                            int32_t rank, int32_t world);

@@ -213,7 +213,7 @@ int build_selections(pt_session* s)
 
 int allreduce(pt_session* s, float* buf, cudaStream_t st)
 {
-    if (s->world == 1) return PT_OK;
+    if (!s->comm) return PT_OK;
     int e = s->nccl.allreduce(buf, buf, s->n, kNcclFloat32, kNcclSum, s->comm, st);
     if (e != 0) {
         pt::set_error("ncclAllReduce: %s", s->nccl.errstr ? s->nccl.errstr(e) : "error");
@@ -448,7 +448,7 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
                 if (!rc) rc = pt::launch_adjoint(P, sg, s->r, s->g, 1.f, g > 0, nullptr, st, &s->ws);
             }
             if (!rc) rc = pt::launch_epilogue(P, s->g, &ep, st);
-        } else if (s->world == 1) {
+        } else if (!s->comm) {
             rc = pt::launch_adjoint(P, sel, s->r, nullptr, 1.f, 0, &ep, st, &s->ws);
         } else {
             if (sel->n == 0) {
@@ -545,7 +545,7 @@ int pt_nccl_unique_id(const char* nccl_path, uint8_t* host_out128)
 int pt_session_emulate_sectors(pt_session* s, int32_t world)
 {
     if (!s || world < 1) { pt::set_error("bad argument"); return PT_EINVAL; }
-    if (s->world != 1) { pt::set_error("session already attached to NCCL"); return PT_EINVAL; }
+    if (s->comm) { pt::set_error("session already attached to NCCL"); return PT_EINVAL; }
     pt_plan* P = s->plan;
     const int A = P->A;
     s->emu_subsets.assign(world, {});
@@ -564,7 +564,9 @@ int pt_session_attach_nccl(pt_session* s, const char* nccl_path, const uint8_t* 
                            int32_t rank, int32_t world)
 {
     if (!s || !host_id128 || world < 1 || rank < 0 || rank >= world) { pt::set_error("bad argument"); return PT_EINVAL; }
-    if (world == 1) return PT_OK;
+    if (s->comm) { pt::set_error("session already attached"); return PT_EINVAL; }
+    // world == 1 is accepted: a one-rank communicator exercises the whole
+    // sharded data path (partial gradient -> ncclAllReduce -> epilogue)
     int rc = nccl_load(nccl_path, &s->nccl);
     if (rc) return rc;
     nccl_uid id;

@@ -42,8 +42,6 @@ def attach(session, rank: int | None = None, world: int | None = None,
     torch.distributed process group (the ranks of one node, one GPU each)."""
     rank = dist.get_rank(group) if rank is None else rank
     world = dist.get_world_size(group) if world is None else world
-    if world == 1:
-        return
     path = nccl_library_path().encode()
 
     def make_uid() -> bytes:

@@ -267,9 +267,13 @@ class RunRecord:
                                       for v in row) + "\n")
 
 
-def _init_state(config: SolverConfig, problem: TomoProblem, x0, stream=None) -> IterateState:
+def _init_state(config: SolverConfig, problem: TomoProblem, x0, stream=None,
+                data_parallel: bool = False) -> IterateState:
     """solvers.py:159-186: x0 (or zeros), h = 0, three PCG64 streams, the
-    staggered partition, SAGA zeros, SVRG initial snapshot (+1 pass)."""
+    staggered partition, SAGA zeros, SVRG initial snapshot (+1 pass).
+
+    data_parallel: shard the angles over the torch.distributed ranks (one GPU
+    each; the library's own NCCL communicator, see distributed.py)."""
     shape = problem.projector.shape
     if x0 is not None and tuple(x0.shape) != tuple(shape):
         raise ValueError(f"x0 shape {tuple(x0.shape)} does not match grid {shape}")
@@ -280,6 +284,9 @@ def _init_state(config: SolverConfig, problem: TomoProblem, x0, stream=None) -> 
                                               config.n_subsets)
     stream = stream if stream is not None else torch.cuda.current_stream()
     session = _Session(config, problem, x0, stream)
+    if data_parallel:
+        from . import distributed as _dist
+        _dist.attach(session)
     state = IterateState(session=session, partition=partition,
                          rng_subset=np.random.default_rng(streams[0]),
                          rng_theta=np.random.default_rng(streams[1]),
@@ -424,15 +431,18 @@ def _metrics_row(passes, wall, x, reference, ground_truth, prox_calls, problem,
 
 
 def run(config: SolverConfig, problem: TomoProblem, x0=None, reference=None,
-        ground_truth=None, record_objective: bool = False, stream=None) -> RunRecord:
+        ground_truth=None, record_objective: bool = False, stream=None,
+        data_parallel: bool = False) -> RunRecord:
     """Run the skip-capable loop until tolerance or budget exhaustion (:327-336).
 
     Rows are logged at every data-pass boundary exactly as :280-324; the
     iterations between two rows are one native segment.  The host syncs only
-    at rows that need a metric (or for a time budget) and at the end."""
+    at rows that need a metric (or for a time budget) and at the end.
+    data_parallel=True shards the projection angles over the torch.distributed
+    ranks (every rank calls run with the same arguments)."""
     stream = stream if stream is not None else torch.cuda.current_stream()
     with torch.cuda.stream(stream):
-        state = _init_state(config, problem, x0, stream)
+        state = _init_state(config, problem, x0, stream, data_parallel=data_parallel)
         return _run_loop(state, config, problem, reference, ground_truth, record_objective,
                          stream)
 

@@ -222,3 +222,28 @@ def test_config1_whole_run_matches_reference(oracle):
     assert np.array_equal(rec.column("prox_calls"), c1["c1_prox"])
     assert rec.iterations == list(c1["c1_iters"])
     assert proj.norm_sq(50, 0) == pytest.approx(float(c1["c1_L"]), rel=1e-5)
+
+
+def test_nccl_data_path_on_one_rank_is_bitwise_identical(small_runs):
+    """The multi-GPU data path through a real (one-rank) NCCL communicator:
+    dlopen of torch's libnccl, unique-id exchange over torch.distributed,
+    partial gradient -> ncclAllReduce -> separate epilogue kernel.  With one
+    rank it must reproduce the fused single-GPU path bit for bit."""
+    import socket
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        problem, lip = small_problem(small_runs)
+        cfg = SolverConfig(gamma=1.0 / lip, skip_probability=0.4, n_subsets=5,
+                           estimator="svrg", max_data_passes=30, seed=23)
+        a = run(cfg, problem)
+        b = run(cfg, TomoProblem(problem.projector, small_runs["small_data"], tv=problem.tv),
+                data_parallel=True)
+        assert torch.equal(a.image, b.image)
+        assert a.iterations == b.iterations
+    finally:
+        dist.destroy_process_group()
