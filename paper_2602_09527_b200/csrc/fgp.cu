@@ -23,6 +23,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "pt_internal.cuh"
@@ -116,54 +117,65 @@ __device__ __forceinline__ void fgp2d_iteration(
 // Interior iteration with packed f32x2 arithmetic.  A thread's strip rows are
 // held as pairs (j, j + H2), H2 = STRIP/2, so the up-neighbour of pair j is
 // pair j-1 and the down-neighbour of pair j is pair j+1 (one repack at the
-// strip ends): the stencil needs no lane shuffling.
+// strip ends): the stencil needs no lane shuffling.  The left/right exchange
+// planes store the pairs as float2 (one 64-bit LDS/STS per pair, operands land
+// in aligned register pairs).
+__device__ __forceinline__ float rsqrt_ftz(float x)
+{
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ f2 ld2(const float2* p)
+{
+    f2 r;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(r.v) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+    return r;
+}
+__device__ __forceinline__ void st2(float2* p, f2 v)
+{
+    asm volatile("st.shared.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "l"(v.v));
+}
+
 template <int RW, int RH, int STRIP>
 __device__ __forceinline__ void fgp2d_iteration_packed(
     f2 (&V)[STRIP / 2], f2 (&Pp)[STRIP / 2], f2 (&Q)[STRIP / 2], f2 (&R)[STRIP / 2],
-    f2 (&S)[STRIP / 2], f2 (&U)[STRIP / 2], float (*S_s)[RW + 1], float (*S_u)[RW + 1],
+    f2 (&S)[STRIP / 2], f2 (&U)[STRIP / 2], float2 (*S_s2)[RW + 1], float2 (*S_u2)[RW + 1],
     float (*S_r)[RW], float (*S_ut)[RW], int tx, int ty, float lam, float eta, float beta,
     int nonneg)
 {
     constexpr int NS = RH / STRIP;
     constexpr int H2 = STRIP / 2;
-    const int row0 = ty * STRIP;
+    const int prow0 = ty * H2;
     const f2 nlam2 = pk(-lam, -lam), eta2 = pk(eta, eta), beta2 = pk(beta, beta);
+    const f2 zero2 = pk(0.f, 0.f);
 #pragma unroll
-    for (int j = 0; j < H2; ++j) {
-        float a, b;
-        upk(S[j], a, b);
-        S_s[row0 + j][tx] = a;
-        S_s[row0 + j + H2][tx] = b;
-    }
+    for (int j = 0; j < H2; ++j) st2(&S_s2[prow0 + j][tx], S[j]);
     S_r[ty][tx] = hi_of(R[H2 - 1]);
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < H2; ++j) {
         const f2 r_up = j ? R[j - 1] : pk(ty ? S_r[ty - 1][tx] : 0.f, lo_of(R[H2 - 1]));
-        const f2 s_left = pk(tx ? S_s[row0 + j][tx - 1] : 0.f, tx ? S_s[row0 + j + H2][tx - 1] : 0.f);
+        const f2 s_left = tx ? ld2(&S_s2[prow0 + j][tx - 1]) : zero2;
         // _diff_adjoint (regularizers.py:70-76): ((-r + r_up) - s) + s_left
         const f2 o = add2(sub2(sub2(r_up, R[j]), S[j]), s_left);
         f2 u = fma2(nlam2, o, V[j]);
-        float ua, ub;
-        upk(u, ua, ub);
         if (nonneg) {
-            ua = (ua < 0.f) ? 0.f : ua;
-            ub = (ub < 0.f) ? 0.f : ub;
-            u = pk(ua, ub);
+            float ua, ub;
+            upk(u, ua, ub);
+            u = pk((ua < 0.f) ? 0.f : ua, (ub < 0.f) ? 0.f : ub);  // NaN propagates
         }
         U[j] = u;
-        S_u[row0 + j][tx] = ua;
-        S_u[row0 + j + H2][tx] = ub;
+        st2(&S_u2[prow0 + j][tx], u);
     }
     S_ut[ty][tx] = lo_of(U[0]);
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < H2; ++j) {
-        // rows (j+1, j+1+H2); for the last pair these are (H2 -> pair 0 hi, next strip's first row)
+        // rows (j+1, j+1+H2); for the last pair: (pair 0 hi, next strip's first row)
         const f2 u_down = (j < H2 - 1) ? U[j + 1]
                                        : pk(hi_of(U[0]), ty < NS - 1 ? S_ut[ty + 1][tx] : 0.f);
-        const f2 u_right = pk(tx < RW - 1 ? S_u[row0 + j][tx + 1] : 0.f,
-                              tx < RW - 1 ? S_u[row0 + j + H2][tx + 1] : 0.f);
+        const f2 u_right = (tx < RW - 1) ? ld2(&S_u2[prow0 + j][tx + 1]) : zero2;
         const f2 gv = sub2(u_down, U[j]);
         const f2 gh = sub2(u_right, U[j]);
         const f2 ph = fma2(eta2, gv, R[j]);
@@ -171,7 +183,8 @@ __device__ __forceinline__ void fgp2d_iteration_packed(
         const f2 n2 = fma2(ph, ph, mul2(qh, qh));
         float na, nb;
         upk(n2, na, nb);
-        const f2 inv = pk((na > 1.f) ? rsqrtf(na) : 1.f, (nb > 1.f) ? rsqrtf(nb) : 1.f);
+        // max(1, |.|): the projection only rescales when |.| > 1 (no denormals there)
+        const f2 inv = pk((na > 1.f) ? rsqrt_ftz(na) : 1.f, (nb > 1.f) ? rsqrt_ftz(nb) : 1.f);
         const f2 pn = mul2(ph, inv), qn = mul2(qh, inv);
         R[j] = fma2(beta2, sub2(pn, Pp[j]), pn);
         S[j] = fma2(beta2, sub2(qn, Q[j]), qn);
@@ -184,8 +197,13 @@ template <int RW, int RH, int STRIP>
 __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
 {
     constexpr int H2 = STRIP / 2;
-    __shared__ float S_s[RH][RW + 1];
-    __shared__ float S_u[RH][RW + 1];
+    // the scalar (edge / epilogue) and the pair (interior) exchange planes
+    // share one buffer: a CTA uses one layout at a time
+    __shared__ __align__(16) float S_buf[2 * RH * (RW + 1)];
+    float (*S_s)[RW + 1] = reinterpret_cast<float (*)[RW + 1]>(S_buf);
+    float (*S_u)[RW + 1] = reinterpret_cast<float (*)[RW + 1]>(S_buf + RH * (RW + 1));
+    float2 (*S_s2)[RW + 1] = reinterpret_cast<float2 (*)[RW + 1]>(S_buf);
+    float2 (*S_u2)[RW + 1] = reinterpret_cast<float2 (*)[RW + 1]>(S_buf + RH * (RW + 1));
     __shared__ float S_r[RH / STRIP][RW];
     __shared__ float S_ut[RH / STRIP][RW];
 
@@ -230,7 +248,7 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
     }
     for (int it = 0; it < P.n_iter; ++it) {
         if (!edge) {
-            fgp2d_iteration_packed<RW, RH, STRIP>(V, Pp, Q, R, S, U, S_s, S_u, S_r, S_ut, tx, ty,
+            fgp2d_iteration_packed<RW, RH, STRIP>(V, Pp, Q, R, S, U, S_s2, S_u2, S_r, S_ut, tx, ty,
                                                   P.lam, P.eta, P.beta[it], P.nonneg);
         } else {
             float v[STRIP], p[STRIP], q[STRIP], r[STRIP], s[STRIP], u[STRIP];
@@ -525,8 +543,14 @@ int launch_tv_prox(pt_plan* plan, const float* v, double lam, int inner, int non
         return launch_fgp3d(plan, v, lam, inner, nonneg, p, q, w, x_out, xhat, h, p_over_gamma,
                             iteration, bad_iter, work, st);
     if (std::min(plan->H, plan->W) >= 256)
+    {
+        static const int tmax = [] {
+            const char* e = getenv("PT_FGP_T");
+            return e ? std::max(1, std::min(8, atoi(e))) : 6;
+        }();
         return run_fgp2d<64, 64, 8>(plan, v, lam, inner, nonneg, p, q, x_out, xhat, h,
-                                    p_over_gamma, iteration, bad_iter, work, st, 6);
+                                    p_over_gamma, iteration, bad_iter, work, st, tmax);
+    }
     return run_fgp2d<32, 32, 8>(plan, v, lam, inner, nonneg, p, q, x_out, xhat, h,
                                 p_over_gamma, iteration, bad_iter, work, st, 3);
 }
