@@ -78,6 +78,10 @@ __device__ __forceinline__ uint32_t opaque(uint32_t v)
     X(5, 16, 256, 256, 4)        \
     X(6, 32, 256, 128, 8)        \
     X(7, 32, 128, 128, 8)        \
+    X(8, 128, 128, 512, 1)       \
+    X(9, 128, 256, 512, 1)       \
+    X(10, 64, 512, 512, 1)       \
+    X(11, 64, 256, 1024, 1)      \
     X(100, 32, 128, 256, 4)      \
     X(101, 16, 64, 128, 8)
 
@@ -411,8 +415,19 @@ __global__ void __launch_bounds__(256) fwd_reduce_kernel(RedArgs P)
         const AngleTab at = P.tab[ang];
         const int nb = at.branch ? P.nb_col : P.nb_row;
         const size_t stride = (size_t)P.n_k * P.Z * P.B;
-        double s = 0.0;
-        for (int band = 0; band < nb; ++band) s += (double)P.partial[band * stride + idx];
+        // four independent float64 partial sums (latency), combined pairwise
+        const float* pp = P.partial + idx;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int band = 0;
+        for (; band + 4 <= nb; band += 4) {
+            const float a = __ldcs(pp + (size_t)band * stride);
+            const float b2 = __ldcs(pp + (size_t)(band + 1) * stride);
+            const float c = __ldcs(pp + (size_t)(band + 2) * stride);
+            const float d = __ldcs(pp + (size_t)(band + 3) * stride);
+            s0 += a; s1 += b2; s2 += c; s3 += d;
+        }
+        for (; band < nb; ++band) s0 += __ldcs(pp + (size_t)band * stride);
+        const double s = (s0 + s1) + (s2 + s3);
         double yd = s * (double)at.step_len;
         if (P.data) yd -= (double)P.data[((size_t)ang * P.Z + z) * P.B + b];
         if (P.data2) yd -= (double)P.data2[((size_t)ang * P.Z + z) * P.B + b];
