@@ -720,7 +720,7 @@ __global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
             if (lane == 0) {
                 const float stp = t.step_len;
                 s_p4[buf][a] = make_float4((float)gbr, (float)gbc, (float)e0,
-                                           (float)(stp * fabs(t.sigma)));
+                                           (float)fabs(t.sigma));
                 // shared byte address of local bin 0 minus the floor-trick offset
                 const uint32_t ya = stage_u32 + (uint32_t)((buf * NA + a) * P.slot - jlo) * 4u -
                                     (uint32_t)kMagicBits * 4u;
@@ -761,6 +761,15 @@ __global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
         } else {
             cp_async_wait_all();
         }
+        // scale the staged bins by step_len: every lane rescales exactly the
+        // elements its own cp.async wrote (complete after its wait), so the
+        // CTA barrier below publishes the scaled values
+        __syncwarp();
+        for (int a = warp; a < nc; a += NW) {
+            const float stp = s_p2[buf][a].x;
+            float* row = smem + (size_t)(buf * NA + a) * P.slot;
+            for (int j = lane; j < P.slot; j += 32) row[j] *= stp;
+        }
         __syncthreads();
         if (TWO_TAP) {
             f2 acc2[PIX / 2];
@@ -770,25 +779,24 @@ __global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
             for (int a = 0; a < nc; ++a) {
                 const float4 q4 = s_p4[buf][a];
                 const float2 q2 = s_p2[buf][a];
-                const float br = q4.x, S1 = q4.w, A0 = q2.x;
+                const float br = q4.x, S1 = q4.w;
                 const float cterm = fmaf(clf, q4.y, q4.z);
                 const uint32_t yb = __float_as_uint(q2.y);
                 const f2 ct2 = pk(cterm, cterm), br2 = pk(br, br);
-                const f2 nS1 = pk(-S1, -S1), S12 = pk(S1, S1), A02 = pk(A0, A0),
-                         A0mS1 = pk(A0 - S1, A0 - S1);
+                const float nS1 = -S1, oS1 = 1.f - S1;
 #pragma unroll
                 for (int jj = 0; jj < PIX / 2; ++jj) {
                     const f2 bl = fma2(rr[jj], br2, ct2);
                     const f2 t = add2_rm(bl, mg2);
                     const f2 phi = sub2(bl, sub2(t, mg2));
-                    // step_len * hat(pos_b - lane) for b = floor(b_f), floor(b_f) + 1
-                    f2 w0 = fma2(nS1, phi, A02);
-                    f2 w1 = fma2(S12, phi, A0mS1);
-                    float w0a, w0b, w1a, w1b, ta, tb, y0a, y1a, y0b, y1b;
-                    upk(w0, w0a, w0b);
-                    upk(w1, w1a, w1b);
-                    w0 = pk(fmaxf(w0a, 0.f), fmaxf(w0b, 0.f));
-                    w1 = pk(fmaxf(w1a, 0.f), fmaxf(w1b, 0.f));
+                    // hat(pos_b - lane) for b = floor(b_f), floor(b_f) + 1 (the
+                    // bins carry step_len); saturating FMAs clamp at 0 (<= 1 anyway)
+                    float pa, pb, ta, tb, y0a, y1a, y0b, y1b;
+                    upk(phi, pa, pb);
+                    const f2 w0 = pk(__saturatef(fmaf(nS1, pa, 1.f)),
+                                     __saturatef(fmaf(nS1, pb, 1.f)));
+                    const f2 w1 = pk(__saturatef(fmaf(S1, pa, oS1)),
+                                     __saturatef(fmaf(S1, pb, oS1)));
                     upk(t, ta, tb);
                     lds_pair(mad4(__float_as_uint(ta), yb), y0a, y1a);
                     lds_pair(mad4(__float_as_uint(tb), yb), y0b, y1b);
@@ -810,7 +818,7 @@ __global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
             for (int a = 0; a < nc; ++a) {
                 const float4 q4 = s_p4[buf][a];
                 const float2 q2 = s_p2[buf][a];
-                const float br = q4.x, S1 = q4.w, A0 = q2.x;
+                const float br = q4.x, S1 = q4.w;
                 const float cterm = fmaf(clf, q4.y, q4.z);
                 const int ybase = a * P.slot + s_off[buf][a] - kMagicBits;
 #pragma unroll
@@ -820,7 +828,7 @@ __global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
                     const float phi = bl - (tt - kMagic);
                     const float* yp = sl + (ybase + __float_as_int(tt));
                     for (int q = -P.cand_half + 1; q <= P.cand_half; ++q) {
-                        const float w = fmaxf(0.f, A0 - S1 * fabsf((float)q - phi));
+                        const float w = fmaxf(0.f, 1.f - S1 * fabsf((float)q - phi));
                         acc_i[j] = fmaf(w, yp[q], acc_i[j]);
                     }
                 }
