@@ -161,6 +161,23 @@ int pt_diff_norms(const float* x, const float* ref, int64_t n, double* out, void
 int pt_operator_norm_sq(pt_plan* plan, float* v0, int32_t iterations, double* host_out,
                         void* stream);
 
+/* Diagonally preconditioned PDHG reference solver, elementwise steps
+ * (solvers.py:395-455; the projector calls are pt_forward with the data
+ * subtraction and pt_adjoint).  Images are (n_slices, height, width) stacks
+ * of independent 2D planes (the reference is 2D: n_slices = 1).
+ *   dual_sino: y = (y + sigma_a * resid) / (1 + sigma_a)                (:434)
+ *   dual_tv:   (zv, zh) = clip to |.| <= alpha of (zv, zh) + sigma_d D xbar (:436-442)
+ *   primal:    x' = x - tau (ascent + D^T(zv, zh)) [max(., 0) if nonneg];
+ *              xbar = 2 x' - x; x = x'; zv == NULL skips the TV term;
+ *              non-finite x' lowers *bad_iter to `iteration`        (:443-451) */
+int pt_pdhg_dual_sino(float* y, const float* resid, const float* sigma_a, int64_t n,
+                      void* stream);
+int pt_pdhg_dual_tv(const float* xbar, float* zv, float* zh, int32_t n_slices, int32_t height,
+                    int32_t width, double sigma_d, double alpha, void* stream);
+int pt_pdhg_primal(float* x, float* xbar, const float* ascent, const float* zv, const float* zh,
+                   const float* tau, int32_t n_slices, int32_t height, int32_t width,
+                   int32_t nonneg, int64_t iteration, int64_t* bad_iter, void* stream);
+
 /* ------------------------------------------------------------------ */
 /* Native executor for the ProxSkip loop (solvers.py:159-324).          */
 /* ------------------------------------------------------------------ */

@@ -160,3 +160,66 @@ def run_proxskip(projector: OracleProjector, data, *, gamma, p, estimator, n_sub
     res.image = x
     res.k = k
     return res
+
+
+def _forward_diff(x):
+    """regularizers.py:62-68: forward differences, 0 on the last row / column."""
+    gv = np.zeros_like(x)
+    gh = np.zeros_like(x)
+    gv[:-1, :] = x[1:, :] - x[:-1, :]
+    gh[:, :-1] = x[:, 1:] - x[:, :-1]
+    return gv, gh
+
+
+def _diff_adjoint(a, b):
+    """regularizers.py:71-76: D^T(a, b) using only the [:-1] parts."""
+    out = np.zeros_like(a)
+    out[:-1, :] -= a[:-1, :]
+    out[1:, :] += a[:-1, :]
+    out[:, :-1] -= b[:, :-1]
+    out[:, 1:] += b[:, :-1]
+    return out
+
+
+def run_pdhg(projector, data, n_iterations, alpha=0.0, nonneg=False, snapshot_at=None):
+    """Diagonally preconditioned PDHG (solvers.py:395-455), float64."""
+    data = np.asarray(data, dtype=np.float64)
+    shape = projector.shape
+    row_sums = projector.forward(np.ones(shape))
+    with np.errstate(divide="ignore"):
+        sigma_a = np.where(row_sums > 0.0, 1.0 / row_sums, 0.0)
+    col_sums = projector.adjoint(np.ones_like(data))
+    if alpha > 0.0:
+        dc = np.zeros(shape)
+        dc[:-1, :] += 1.0
+        dc[1:, :] += 1.0
+        dc[:, :-1] += 1.0
+        dc[:, 1:] += 1.0
+        col_sums = col_sums + dc
+    tau = 1.0 / np.maximum(col_sums, 1e-12)
+    sigma_d = 0.5
+    x = np.zeros(shape)
+    x_bar = x.copy()
+    y = np.zeros_like(data)
+    zv = np.zeros(shape)
+    zh = np.zeros(shape)
+    snapshot = None
+    for it in range(1, n_iterations + 1):
+        y = (y + sigma_a * (projector.forward(x_bar) - data)) / (1.0 + sigma_a)
+        ascent = projector.adjoint(y)
+        if alpha > 0.0:
+            gv, gh = _forward_diff(x_bar)
+            zv = zv + sigma_d * gv
+            zh = zh + sigma_d * gh
+            scale = np.maximum(1.0, np.sqrt(zv * zv + zh * zh) / alpha)
+            zv /= scale
+            zh /= scale
+            ascent = ascent + _diff_adjoint(zv, zh)
+        x_old = x
+        x = x - tau * ascent
+        if nonneg:
+            np.maximum(x, 0.0, out=x)
+        x_bar = 2.0 * x - x_old
+        if snapshot_at is not None and it == snapshot_at:
+            snapshot = x.copy()
+    return (x, snapshot) if snapshot_at is not None else x

@@ -81,6 +81,10 @@ _SIGS = {
     "pt_session_set_profiling": (ctypes.c_int, [c_vp, c_i32]),
     "pt_session_profile": (ctypes.c_int, [c_vp, ctypes.POINTER(c_f64), ctypes.POINTER(c_i64)]),
     "pt_session_emulate_sectors": (ctypes.c_int, [c_vp, c_i32]),
+    "pt_pdhg_dual_sino": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "pt_pdhg_dual_tv": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_f64, c_f64, c_vp]),
+    "pt_pdhg_primal": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32,
+                                      c_i32, c_i64, c_vp, c_vp]),
     "pt_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint8)]),
     "pt_session_attach_nccl": (ctypes.c_int, [c_vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint8),
                                               c_i32, c_i32]),

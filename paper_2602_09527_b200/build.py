@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libproxtomo_b200.so")
-SOURCES = ["capi.cu", "projector.cu", "fgp.cu", "reduce.cu", "session.cu"]
+SOURCES = ["capi.cu", "projector.cu", "fgp.cu", "reduce.cu", "session.cu", "pdhg.cu"]
 HEADERS = ["pt_internal.cuh", "pt_simd.cuh", os.path.join("..", "..", "include", "proxtomo_b200.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

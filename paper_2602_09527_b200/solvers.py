@@ -628,6 +628,74 @@ def run_fista(config: SolverConfig, problem: TomoProblem, x0=None, reference=Non
     return _full_loop(config, problem, x0, reference, ground_truth, record_objective, step)
 
 
+def run_pdhg_reference(problem: TomoProblem, n_iterations: int, snapshot_at: int | None = None):
+    """High-accuracy reference by diagonally preconditioned primal-dual
+    iterations on the saddle form (solvers.py:395-455), on the device.
+
+    Per iteration: the forward with the data subtraction fused (A xbar - b),
+    the dual sinogram step, the gather adjoint, the TV dual step and the
+    primal step (pdhg.cu).  Returns the final iterate, or (final, snapshot)
+    when ``snapshot_at`` is given; device float32 tensors.  A non-finite
+    iterate raises DivergenceError(first bad iteration, max tau)."""
+    if n_iterations < 1:
+        raise ValueError("n_iterations must be >= 1")
+    if problem.denoiser is not None:
+        raise ValueError("reference solver needs an explicit objective, not a denoiser")
+    projector = problem.projector
+    if getattr(projector, "n_slices", 1) != 1:
+        raise ValueError("the PDHG reference is 2D (solvers.py:395-455)")
+    data = problem.device_data()
+    alpha = problem.tv.alpha if problem.tv is not None else 0.0
+    nonneg = problem.tv.nonneg if problem.tv is not None else False
+    H, W = projector.shape
+    plan = projector.plan
+    lib = N.lib()
+    stream = N.stream_handle()
+    ones = torch.ones((H, W), device="cuda")
+    row_sums = torch.empty_like(data)
+    plan.forward_into(ones, row_sums)
+    sigma_a = torch.where(row_sums > 0, 1.0 / row_sums, torch.zeros_like(row_sums)).contiguous()
+    col_sums = torch.empty((H, W), device="cuda")
+    plan.adjoint_into(torch.ones_like(data), col_sums)
+    if alpha > 0.0:
+        diff_cols = torch.zeros((H, W), device="cuda")
+        diff_cols[:-1, :] += 1.0
+        diff_cols[1:, :] += 1.0
+        diff_cols[:, :-1] += 1.0
+        diff_cols[:, 1:] += 1.0
+        col_sums = col_sums + diff_cols
+    tau = (1.0 / torch.clamp(col_sums, min=1e-12)).contiguous()
+    sigma_d = 0.5
+    x = torch.zeros((H, W), device="cuda")
+    x_bar = torch.zeros_like(x)
+    y = torch.zeros_like(data)
+    resid = torch.empty_like(data)
+    ascent = torch.empty_like(x)
+    zv = torch.zeros_like(x) if alpha > 0.0 else None
+    zh = torch.zeros_like(x) if alpha > 0.0 else None
+    bad = torch.full((1,), 2 ** 62, device="cuda", dtype=torch.int64)
+    snapshot = None
+    for it in range(1, n_iterations + 1):
+        plan.forward_into(x_bar, resid, data=data)
+        N.check(lib.pt_pdhg_dual_sino(N.ptr(y), N.ptr(resid), N.ptr(sigma_a), y.numel(),
+                                      stream), "pdhg")
+        plan.adjoint_into(y, ascent)
+        if alpha > 0.0:
+            N.check(lib.pt_pdhg_dual_tv(N.ptr(x_bar), N.ptr(zv), N.ptr(zh), 1, H, W, sigma_d,
+                                        float(alpha), stream), "pdhg")
+        N.check(lib.pt_pdhg_primal(N.ptr(x), N.ptr(x_bar), N.ptr(ascent), N.ptr(zv), N.ptr(zh),
+                                   N.ptr(tau), 1, H, W, int(bool(nonneg)), it, N.ptr(bad),
+                                   stream), "pdhg")
+        if snapshot_at is not None and it == snapshot_at:
+            snapshot = x.clone()
+    first_bad = int(bad.item())
+    if first_bad < 2 ** 62:
+        raise DivergenceError(first_bad, float(tau.max()))
+    if snapshot_at is not None:
+        return x, snapshot
+    return x
+
+
 def optimal_p(mu: float, lipschitz: float) -> float:
     """sqrt(mu / L) clamped into (0, 1] (:458-465)."""
     if mu <= 0.0 or lipschitz <= 0.0:

@@ -142,6 +142,24 @@ def small_run_fixtures():
     return out
 
 
+def pdhg_fixtures():
+    """The reference's PDHG solver (solvers.py:395-455) on the small problem,
+    with and without TV; a snapshot part-way."""
+    from proxtomo.solvers import run_pdhg_reference
+    g = P.ParallelGeometry.uniform(10, 23)
+    proj = P.Projector(g, 16, 16)
+    rng = np.random.default_rng(0)
+    truth = np.zeros((16, 16))
+    truth[4:12, 5:11] = 1.0
+    data = proj.forward(truth) + 0.1 * rng.standard_normal((10, 23))
+    out = {"pdhg_data": data}
+    x, snap = run_pdhg_reference(TomoProblem(proj, data, tv=TvProxConfig(alpha=0.5)), 300,
+                                 snapshot_at=40)
+    out["pdhg_tv_x"], out["pdhg_tv_snap40"] = x, snap
+    out["pdhg_plain_x"] = run_pdhg_reference(TomoProblem(proj, data), 120)
+    return out
+
+
 def config_run(name: str, record_objective=True):
     cfg = problems.CONFIGS[name]
     g = P.ParallelGeometry.uniform(cfg.n_angles, cfg.n_bins)
@@ -182,6 +200,9 @@ def main():
     fx.update(schedule_fixtures())
     np.savez_compressed(os.path.join(HERE, "reference_units.npz"), **fx)
     np.savez_compressed(os.path.join(HERE, "reference_small_runs.npz"), **small_run_fixtures())
+    np.savez_compressed(os.path.join(HERE, "reference_pdhg.npz"), **pdhg_fixtures())
+    if "--pdhg-only" in sys.argv:
+        return
     c0 = config_run("c0")
     np.savez_compressed(os.path.join(HERE, "reference_c0.npz"), **c0)
     print("c0 reference work_seconds", float(c0["c0_work_seconds"]), "prox",

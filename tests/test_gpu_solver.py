@@ -247,3 +247,20 @@ def test_nccl_data_path_on_one_rank_is_bitwise_identical(small_runs):
         assert a.iterations == b.iterations
     finally:
         dist.destroy_process_group()
+
+
+def test_pdhg_reference_matches_reference():
+    """Device PDHG (pdhg.cu + projector) vs the reference's own PDHG runs."""
+    import os
+    from conftest import GOLDEN
+    from paper_2602_09527_b200 import run_pdhg_reference
+    f = np.load(os.path.join(GOLDEN, "reference_pdhg.npz"))
+    proj = Projector(ParallelGeometry.uniform(10, 23), 16, 16)
+    x, snap = run_pdhg_reference(TomoProblem(proj, f["pdhg_data"], tv=TvProxConfig(alpha=0.5)),
+                                 300, snapshot_at=40)
+    assert rel_l2(cpu(x), f["pdhg_tv_x"]) <= TOL
+    assert rel_l2(cpu(snap), f["pdhg_tv_snap40"]) <= TOL
+    x = run_pdhg_reference(TomoProblem(proj, f["pdhg_data"]), 120)
+    assert rel_l2(cpu(x), f["pdhg_plain_x"]) <= TOL
+    with pytest.raises(ValueError):
+        run_pdhg_reference(TomoProblem(proj, f["pdhg_data"]), 0)
