@@ -242,6 +242,20 @@ int pt_session_attach_nccl(pt_session* s, const char* nccl_path, const uint8_t* 
  * is exactly what ncclAllReduce sums across real ranks).  Call before run. */
 int pt_session_emulate_sectors(pt_session* s, int32_t world);
 
+/* z-slab decomposition of a slice-stacked 3D volume: the
+ * session's plan holds this rank's planes [z_offset, z_offset + Z) of a
+ * z_total-plane volume and `data` its sinogram rows (A, Z, B).  The projector,
+ * gradients and snapshot are slab-local (rays never cross slices); the 3D TV
+ * prox exchanges one boundary plane of the duals per inner iteration (and of
+ * its input once per call) with ranks -+ 1 by ncclSend/ncclRecv on the
+ * session stream.  Ranks must hold consecutive slabs in rank order. */
+int pt_session_attach_nccl_zslab(pt_session* s, const char* nccl_path, const uint8_t* host_id128,
+                                 int32_t rank, int32_t world, int32_t z_offset, int32_t z_total);
+/* Test hook: run the 3D TV prox as `slabs` virtual z-slabs of this volume on
+ * one device (each slab sees its neighbours only through its ghost planes,
+ * filled by device copies).  Call before run. */
+int pt_session_emulate_zslabs(pt_session* s, int32_t slabs);
+
 #ifdef __cplusplus
 }
 #endif

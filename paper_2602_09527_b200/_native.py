@@ -88,6 +88,10 @@ _SIGS = {
     "pt_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint8)]),
     "pt_session_attach_nccl": (ctypes.c_int, [c_vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint8),
                                               c_i32, c_i32]),
+    "pt_session_attach_nccl_zslab": (ctypes.c_int, [c_vp, ctypes.c_char_p,
+                                                    ctypes.POINTER(ctypes.c_uint8), c_i32, c_i32,
+                                                    c_i32, c_i32]),
+    "pt_session_emulate_zslabs": (ctypes.c_int, [c_vp, c_i32]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -18,12 +18,14 @@
 // neighbour needs cross threads: s and u through shared-memory planes
 // (left / right neighbours), r and u of the strip ends through two small
 // row buffers (up / down neighbours).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "pt_internal.cuh"
@@ -333,8 +335,8 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
 int64_t fgp_workspace_floats(const pt_plan* plan)
 {
     // two ping-pong sets of (p, q, r, s) [2D] or (p, q, w, r, s, t) [3D]
-    const int64_t n = (int64_t)plan->Z * plan->H * plan->W;
-    return plan->Z > 1 ? 12 * n : 8 * n;
+    if (plan->Z > 1) return fgp3d_slab_floats(plan->Z, plan->H, plan->W);
+    return 8 * (int64_t)plan->H * plan->W;
 }
 
 template <int RW, int RH, int STRIP>
@@ -405,130 +407,516 @@ static int run_fgp2d(pt_plan* plan, const float* v, double lam, int inner, int n
 // ---------------------------------------------------------------------------
 // 3D isotropic FGP on a (Z, H, W) volume (slice-stacked geometry, config 3).
 // No reference code exists: the 2D algorithm with a
-// third forward difference along z and dual step 1/(12 lam).  Two passes per
-// inner iteration: u from the dual neighbours, then the pointwise dual update.
+// third forward difference along z and dual step 1/(12 lam).
+//
+// One fused launch per inner iteration.  State: the duals P_k and the
+// momentum duals R_k = P_k + beta_{k-1} (P_k - P_{k-1}), each a set laid out
+// [Zl + 2][3][H][W] (the three components of a plane contiguous, one ghost
+// plane below and above).  An iteration reads R_k (with halo), P_k and v and
+// writes P_{k+1}, R_{k+1}: 52 B per voxel, with u = max(v - lam D^T R_k, 0)
+// recomputed on chip.  A CTA owns a TY x TX column of the volume over a run of
+// planes and marches it along z: the R / v / P boxes of plane z + NS - 1 are
+// in flight (TMA into an NS-stage shared-memory ring, mbarrier completion;
+// cp.async when W % 4 != 0) while u of plane z + 1 and the dual step of plane
+// z are computed from shared memory.
+//
+// z-slabs: a rank (or a virtual slab on one device) owns
+// planes [z0, z0 + Zl) of Zg; the ghost planes of the R sets and one ghost
+// plane of v above hold the neighbours' boundary planes, refreshed by a halo
+// exchange after every iteration (fgp3d_run).  Ghost planes on the global
+// boundary are zero.
 // ---------------------------------------------------------------------------
 struct Fgp3Args {
-    int Z, H, W;
-    const float* v;
-    const float *r, *s, *t;  // momentum duals (read in the u pass)
-    float *pp, *qq, *ww;     // duals
-    float *rr, *ss, *tt;     // momentum duals (written in the dual pass)
-    float* u;
-    float lam, eta, beta;
+    int Zl, H, W, z0, Zg, zchunk;
+    const float* v;     // [Zl][H][W]
+    const float* vtop;  // v of global plane z0 + Zl (ghost)
+    const float* P;     // P_k      [Zl + 2][3][H][W]
+    const float* R;     // R_k
+    float* Pn;          // P_{k+1}
+    float* Rn;          // R_{k+1}
+    float lam, eta, beta;  // beta = beta_k (momentum of the output)
     int nonneg;
 };
 
-__device__ __forceinline__ float dt3(const float* a, const float* b, const float* c, int Z, int H,
-                                     int W, int k, int i, int j, size_t o)
+// TMA descriptors of one launch: R_k and P_k as 4D tensors (W, H, 3, Zl + 2),
+// v as (W, H, Zl), its ghost plane as (W, H); zero fill outside.
+struct Fgp3Maps {
+    CUtensorMap R, P, V, Vt;
+};
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
 {
-    const size_t plane = (size_t)H * W;
-    float x = (i < H - 1) ? -a[o] : 0.f;
-    if (i > 0) x += a[o - W];
-    if (j < W - 1) x -= b[o];
-    if (j > 0) x += b[o - 1];
-    if (k < Z - 1) x -= c[o];
-    if (k > 0) x += c[o - plane];
-    return x;
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W_%=;\n}" ::"r"(bar), "r"(parity));
+}
+__device__ __forceinline__ void cpa4(uint32_t dst, const float* src, bool valid)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src),
+                 "r"(valid ? 4 : 0));
 }
 
-__global__ void fgp3d_u_kernel(Fgp3Args P)
+// Stage layout of one plane: R box [3][TY+2][TX+8] (rows i0-1 .., columns
+// j0-4 ..), v box [TY+2][TX+8] (same window), P box [3][TY][TX].
+template <int TX, int TY, int NS>
+struct Fgp3Tile {
+    static constexpr int NT = TX * TY / 2;      // 2 output rows per thread
+    static constexpr int RW = TX + 8, RR = TY + 2, ARR = RR * RW;
+    static constexpr int VOFF = (3 * ARR + 31) & ~31;
+    static constexpr int POFF = (VOFF + ARR + 31) & ~31;
+    static constexpr int PARR = TX * TY;
+    static constexpr int STAGE = (POFF + 3 * PARR + 31) & ~31;
+    static constexpr int NWW = (TY + 1) * (TX + 1);   // u window
+    static constexpr int SMEM_FLOATS = NS * STAGE + 2 * NWW;
+    static constexpr int TMA_BYTES_RV = 4 * ARR * 4, TMA_BYTES_P = 3 * PARR * 4;
+};
+
+template <int TX, int TY, int NS, bool TMA>
+__global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
+                                                                 const __grid_constant__ Fgp3Maps m)
 {
-    const size_t n = (size_t)P.Z * P.H * P.W;
+    using T = Fgp3Tile<TX, TY, NS>;
+    constexpr int NT = T::NT, RW = T::RW, RR = T::RR, ARR = T::ARR, NWW = T::NWW;
+    constexpr int KU = (NWW + NT - 1) / NT;
+    extern __shared__ __align__(128) float fsm[];
+    __shared__ __align__(8) uint64_t mbar[NS];
+    float* sU = fsm + NS * T::STAGE;  // [2][TY+1][TX+1]
+    const uint32_t fsm_u32 = (uint32_t)__cvta_generic_to_shared(fsm);
+
+    const int tid = threadIdx.x;
+    const int i0 = blockIdx.y * TY, j0 = blockIdx.x * TX;
+    const int zb = blockIdx.z * a.zchunk;
+    const int ze = min(a.Zl, zb + a.zchunk);
+    const int H = a.H, W = a.W;
+    const size_t HW = (size_t)H * W;
+
+    if (TMA) {
+        if (tid == 0) {
+            for (int k = 0; k < NS; ++k)
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                    (uint32_t)__cvta_generic_to_shared(&mbar[k])));
+            asm volatile("fence.mbarrier_init.release.cluster;");
+        }
+        __syncthreads();
+    }
+    // plane p (local; -1 / Zl are ghosts) into stage s
+    auto stage = [&](int p, int s) {
+        const uint32_t sb = fsm_u32 + (uint32_t)(s * T::STAGE) * 4u;
+        const bool withv = p >= 0;  // v of plane -1 is never used
+        if (TMA) {
+            if (tid != 0) return;
+            const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&mbar[s]);
+            const uint32_t bytes = (uint32_t)((withv ? T::TMA_BYTES_RV : 3 * ARR * 4) + T::TMA_BYTES_P);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                         "r"(bytes));
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb),
+                "l"(&m.R), "r"(j0 - 4), "r"(i0 - 1), "r"(0), "r"(p + 1), "r"(bar) : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb + (uint32_t)T::POFF * 4u),
+                "l"(&m.P), "r"(j0), "r"(i0), "r"(0), "r"(p + 1), "r"(bar) : "memory");
+            if (withv && p < a.Zl)
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(sb + (uint32_t)T::VOFF * 4u),
+                    "l"(&m.V), "r"(j0 - 4), "r"(i0 - 1), "r"(p), "r"(bar) : "memory");
+            else if (withv)
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%2, %3}], [%4];" ::"r"(sb + (uint32_t)T::VOFF * 4u),
+                    "l"(&m.Vt), "r"(j0 - 4), "r"(i0 - 1), "r"(bar) : "memory");
+        } else {
+            // element copies of the used windows (columns j0-1 .. j0+TX, zero fill)
+            const size_t b0 = ((size_t)(p + 1) * 3) * HW;
+            const float* vb = (p < a.Zl) ? a.v + (size_t)max(p, 0) * HW : a.vtop;
+            constexpr int CW = TX + 2, NR = 4 * RR * CW;  // R (3) + v windows
+            for (int idx = tid; idx < NR; idx += NT) {
+                const int arr = idx / (RR * CW), rem = idx - arr * (RR * CW);
+                const int r = rem / CW, c = rem - r * CW;
+                const int gi = i0 - 1 + r, gj = j0 - 1 + c;
+                const bool ok = gi >= 0 && gi < H && gj >= 0 && gj < W && (arr < 3 || withv);
+                const float* src = arr < 3 ? a.R + b0 + arr * HW : vb;
+                cpa4(sb + (uint32_t)((arr < 3 ? arr * ARR : T::VOFF) + r * RW + 3 + c) * 4u,
+                     src + (ok ? gi * W + gj : 0), ok);
+            }
+            for (int idx = tid; idx < 3 * T::PARR; idx += NT) {
+                const int comp = idx / T::PARR, rem = idx - comp * T::PARR;
+                const int r = rem / TX, c = rem - r * TX;
+                const int gi = i0 + r, gj = j0 + c;
+                const bool ok = gi < H && gj < W;
+                cpa4(sb + (uint32_t)(T::POFF + idx) * 4u,
+                     a.P + b0 + comp * HW + (ok ? gi * W + gj : 0), ok);
+            }
+            asm volatile("cp.async.commit_group;");
+        }
+    };
+    auto issue = [&](int p) {  // plane p into stage (p - zb + 1) mod NS, if used by this run
+        if (p <= a.Zl && p <= ze) stage(p, (p - zb + 1) % NS);
+        else if (!TMA) asm volatile("cp.async.commit_group;");
+    };
+    auto landed = [&](int p) {
+        if (TMA) {
+            const int u = p - zb + 1;
+            mbar_wait((uint32_t)__cvta_generic_to_shared(&mbar[u % NS]), (uint32_t)((u / NS) & 1));
+        }
+    };
+    // this thread's u positions in the (TY+1) x (TX+1) window: staged offset
+    // and guard bits (0: i < H-1, 1: i > 0, 2: j < W-1, 3: j > 0, 4: inside)
+    int uOff[KU], uG[KU];
+#pragma unroll
+    for (int k = 0; k < KU; ++k) {
+        const int idx = tid + k * NT, r = idx / (TX + 1), c = idx - r * (TX + 1);
+        const int gi = i0 + r, gj = j0 + c;
+        uOff[k] = (r + 1) * RW + 4 + c;
+        uG[k] = (idx < NWW) ? ((gi < H - 1) | ((gi > 0) << 1) | ((gj < W - 1) << 2) |
+                               ((gj > 0) << 3) | ((gi < H && gj < W) << 4))
+                            : -1;
+    }
+    // u of plane z (its stage s) into sU[z & 1]; R_w of z - 1 from stage s1
+    auto compute_U = [&](int z, int s, int s1) {
+        const int zg = a.z0 + z;
+        const bool zlo = zg > 0, zhi = zg < a.Zg - 1;
+        const float* st = fsm + s * T::STAGE;
+        const float* st1 = fsm + s1 * T::STAGE;
+        float* U = sU + (z & 1) * NWW;
+#pragma unroll
+        for (int k = 0; k < KU; ++k) {
+            const int gd = uG[k];
+            if (gd < 0) continue;
+            const int o = uOff[k];
+            float u = 0.f;
+            if (gd & 16) {
+                // D^T(R) in the order of the reference's _diff_adjoint (+ z)
+                float x = (gd & 1) ? -st[o] : 0.f;
+                if (gd & 2) x += st[o - RW];
+                if (gd & 4) x -= st[ARR + o];
+                if (gd & 8) x += st[ARR + o - 1];
+                if (zhi) x -= st[2 * ARR + o];
+                if (zlo) x += st1[2 * ARR + o];
+                u = st[T::VOFF + o] - a.lam * x;
+                if (a.nonneg) u = (u < 0.f) ? 0.f : u;
+            }
+            U[tid + k * NT] = u;
+        }
+    };
+
+    // prologue: planes zb - 1 .. zb + NS - 2 issued; u of zb
+    for (int p = zb - 1; p <= zb + NS - 2; ++p) issue(p);
+    if (!TMA) asm volatile("cp.async.wait_group %0;" ::"n"(NS - 2));
+    landed(zb - 1);
+    landed(zb);
+    __syncthreads();
+    compute_U(zb, 1 % NS, 0);
+    const int tx = tid % TX, ty = tid / TX;
+    constexpr int RSTEP = TY / 2;
+    const int gj = j0 + tx;
+    for (int z = zb; z < ze; ++z) {
+        const int s0 = (z - zb + 1) % NS, s1 = (z - zb + 2) % NS;  // stages of z, z + 1
+        const int zg = a.z0 + z;
+        const bool top = zg < a.Zg - 1;
+        __syncthreads();      // the stage of plane z - 1 is consumed
+        issue(z + NS - 1);    // into it
+        if (!TMA) asm volatile("cp.async.wait_group %0;" ::"n"(NS - 2));
+        landed(z + 1);
+        __syncthreads();
+        if (top) compute_U(z + 1, s1, s0);
+        __syncthreads();
+        const float* st = fsm + s0 * T::STAGE;
+        const float* U0 = sU + (z & 1) * NWW;
+        const float* U1 = sU + ((z + 1) & 1) * NWW;
+        float* __restrict__ pn = a.Pn + ((size_t)(z + 1) * 3) * HW;
+        float* __restrict__ rn = a.Rn + ((size_t)(z + 1) * 3) * HW;
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const int r = ty + rr * RSTEP, gi = i0 + r;
+            if (gi >= H || gj >= W) continue;
+            const int wi = r * (TX + 1) + tx;
+            const int o = (r + 1) * RW + 4 + tx;
+            const float uo = U0[wi];
+            const float gv = (gi < H - 1) ? U0[wi + TX + 1] - uo : 0.f;
+            const float gh = (gj < W - 1) ? U0[wi + 1] - uo : 0.f;
+            const float gz = top ? U1[wi] - uo : 0.f;
+            const float ph = st[o] + a.eta * gv;
+            const float qh = st[ARR + o] + a.eta * gh;
+            const float wh = st[2 * ARR + o] + a.eta * gz;
+            const float n2 = ph * ph + qh * qh + wh * wh;
+            const float inv = (n2 > 1.f) ? rsqrt_ftz(n2) : 1.f;
+            const float p0 = ph * inv, p1 = qh * inv, p2 = wh * inv;
+            const int po = T::POFF + r * TX + tx;
+            const float* pc = st + po;
+            const int g = gi * W + gj;
+            pn[g] = p0;
+            pn[HW + g] = p1;
+            pn[2 * HW + g] = p2;
+            rn[g] = p0 + a.beta * (p0 - pc[0]);
+            rn[HW + g] = p1 + a.beta * (p1 - pc[T::PARR]);
+            rn[2 * HW + g] = p2 + a.beta * (p2 - pc[2 * T::PARR]);
+        }
+    }
+    if (!TMA) asm volatile("cp.async.wait_group 0;");
+}
+
+// caller duals (three [Zl][H][W] arrays) -> interiors of the P and R sets
+__global__ void fgp3d_pack_kernel(const float* p, const float* q, const float* w, float* pset,
+                                  float* rset, int Zl, int H, int W)
+{
+    const size_t HW = (size_t)H * W, n = (size_t)Zl * HW;
     for (size_t o = (size_t)blockIdx.x * blockDim.x + threadIdx.x; o < n;
          o += (size_t)gridDim.x * blockDim.x) {
-        const int j = (int)(o % P.W);
-        const size_t t1 = o / P.W;
-        const int i = (int)(t1 % P.H);
-        const int k = (int)(t1 / P.H);
-        float uu = P.v[o] - P.lam * dt3(P.r, P.s, P.t, P.Z, P.H, P.W, k, i, j, o);
-        if (P.nonneg) uu = (uu < 0.f) ? 0.f : uu;
-        P.u[o] = uu;
+        const size_t z = o / HW, ij = o - z * HW;
+        const size_t d = ((z + 1) * 3) * HW + ij;
+        const float a = p[o], b = q[o], c = w[o];
+        pset[d] = a; pset[d + HW] = b; pset[d + 2 * HW] = c;
+        rset[d] = a; rset[d + HW] = b; rset[d + 2 * HW] = c;
     }
 }
 
-__global__ void fgp3d_dual_kernel(Fgp3Args P)
+// x = max(v - lam D^T(P), 0), h += (p/gamma)(x - x_hat), duals back to the caller
+__global__ void fgp3d_final_kernel(Fgp3Args a, float* p_out, float* q_out, float* w_out,
+                                   float* x_out, const float* xhat, float* h, float pog,
+                                   long long iteration, long long* bad_iter)
 {
-    const size_t n = (size_t)P.Z * P.H * P.W;
-    const size_t plane = (size_t)P.H * P.W;
+    const int H = a.H, W = a.W;
+    const size_t HW = (size_t)H * W, n = (size_t)a.Zl * HW;
     for (size_t o = (size_t)blockIdx.x * blockDim.x + threadIdx.x; o < n;
          o += (size_t)gridDim.x * blockDim.x) {
-        const int j = (int)(o % P.W);
-        const size_t t1 = o / P.W;
-        const int i = (int)(t1 % P.H);
-        const int k = (int)(t1 / P.H);
-        const float uo = P.u[o];
-        const float gv = (i < P.H - 1) ? P.u[o + P.W] - uo : 0.f;
-        const float gh = (j < P.W - 1) ? P.u[o + 1] - uo : 0.f;
-        const float gz = (k < P.Z - 1) ? P.u[o + plane] - uo : 0.f;
-        const float ph = P.rr[o] + P.eta * gv;
-        const float qh = P.ss[o] + P.eta * gh;
-        const float wh = P.tt[o] + P.eta * gz;
-        const float n2 = ph * ph + qh * qh + wh * wh;
-        const float inv = (n2 > 1.f) ? rsqrtf(n2) : 1.f;
-        const float pn = ph * inv, qn = qh * inv, wn = wh * inv;
-        P.rr[o] = pn + P.beta * (pn - P.pp[o]);
-        P.ss[o] = qn + P.beta * (qn - P.qq[o]);
-        P.tt[o] = wn + P.beta * (wn - P.ww[o]);
-        P.pp[o] = pn;
-        P.qq[o] = qn;
-        P.ww[o] = wn;
+        const int z = (int)(o / HW);
+        const size_t ij = o - (size_t)z * HW;
+        const int i = (int)(ij / W), j = (int)(ij - (size_t)i * W);
+        const int zg = a.z0 + z;
+        const float* P = a.P + ((size_t)(z + 1) * 3) * HW + ij;
+        const float pc = P[0], qc = P[HW], wc = P[2 * HW];
+        float x = (i < H - 1) ? -pc : 0.f;
+        if (i > 0) x += P[-(ptrdiff_t)W];
+        if (j < W - 1) x -= qc;
+        if (j > 0) x += P[HW - 1];
+        if (zg < a.Zg - 1) x -= wc;
+        if (zg > 0) x += P[2 * HW - 3 * (ptrdiff_t)HW];
+        float xv = a.v[o] - a.lam * x;
+        if (a.nonneg) xv = (xv < 0.f) ? 0.f : xv;
+        x_out[o] = xv;
+        if (h) h[o] = h[o] + pog * (xv - xhat[o]);
+        p_out[o] = pc;
+        q_out[o] = qc;
+        w_out[o] = wc;
+        if (!isfinite(xv) && bad_iter) atomicMin(bad_iter, iteration);
     }
 }
 
-__global__ void fgp3d_final_kernel(Fgp3Args P, float* x_out, const float* xhat, float* h,
-                                   float pog, long long iteration, long long* bad_iter)
+int64_t fgp3d_slab_floats(int Zl, int H, int W)
 {
-    const size_t n = (size_t)P.Z * P.H * P.W;
-    for (size_t o = (size_t)blockIdx.x * blockDim.x + threadIdx.x; o < n;
-         o += (size_t)gridDim.x * blockDim.x) {
-        const int j = (int)(o % P.W);
-        const size_t t1 = o / P.W;
-        const int i = (int)(t1 % P.H);
-        const int k = (int)(t1 / P.H);
-        float x = P.v[o] - P.lam * dt3(P.pp, P.qq, P.ww, P.Z, P.H, P.W, k, i, j, o);
-        if (P.nonneg) x = (x < 0.f) ? 0.f : x;
-        x_out[o] = x;
-        if (h) h[o] = h[o] + pog * (x - xhat[o]);
-        if (!isfinite(x) && bad_iter) atomicMin(bad_iter, iteration);
-    }
+    // four sets (P, R ping-pong) + the ghost plane of v
+    return 12 * (int64_t)(Zl + 2) * H * W + (int64_t)H * W;
 }
 
-int launch_fgp3d(pt_plan* plan, const float* v, double lam, int inner, int nonneg, float* p,
-                 float* q, float* w, float* x_out, const float* xhat, float* h, float pog,
-                 int64_t iteration, int64_t* bad_iter, float* work, cudaStream_t st)
+// set k of a slab workspace: 0 / 1 = P, R of the even iterations, 2 / 3 = odd
+static inline float* fgp3d_set(float* work, int which, int Zl, int H, int W)
 {
-    const size_t n = (size_t)plan->Z * plan->H * plan->W;
-    Fgp3Args a;
-    a.Z = plan->Z; a.H = plan->H; a.W = plan->W;
-    a.v = v;
-    a.pp = p; a.qq = q; a.ww = w;
-    a.rr = work; a.ss = work + n; a.tt = work + 2 * n;
-    a.u = work + 3 * n;
-    a.r = a.rr; a.s = a.ss; a.t = a.tt;
-    a.lam = (float)lam;
-    a.eta = (float)(1.0 / (12.0 * lam));
-    a.nonneg = nonneg;
-    PT_CHECK_CUDA(cudaMemcpyAsync(a.rr, p, n * 4, cudaMemcpyDeviceToDevice, st));
-    PT_CHECK_CUDA(cudaMemcpyAsync(a.ss, q, n * 4, cudaMemcpyDeviceToDevice, st));
-    PT_CHECK_CUDA(cudaMemcpyAsync(a.tt, w, n * 4, cudaMemcpyDeviceToDevice, st));
-    const int blocks = (int)std::min<size_t>((n + 255) / 256, (size_t)plan->sm_count * 16);
-    double t = 1.0;
-    for (int kk = 0; kk < inner; ++kk) {
-        const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
-        a.beta = (float)((t - 1.0) / tn);
-        t = tn;
-        fgp3d_u_kernel<<<blocks, 256, 0, st>>>(a);
-        PT_CHECK_LAUNCH();
-        fgp3d_dual_kernel<<<blocks, 256, 0, st>>>(a);
-        PT_CHECK_LAUNCH();
+    return work + (size_t)which * 3 * (size_t)(Zl + 2) * H * W;
+}
+static inline float* fgp3d_vtop(float* work, int Zl, int H, int W)
+{
+    return work + 12 * (size_t)(Zl + 2) * H * W;
+}
+
+// Ghost planes of set `which` (and of v when `with_v`) for every local slab:
+// neighbours inside the process by copies, across ranks by the halo callback
+// (NCCL send/recv with rank -+ 1).
+static int fgp3d_exchange(const Fgp3Slab* sl, int G, int H, int W, int which, bool with_v,
+                          const ZHalo* halo, cudaStream_t st)
+{
+    const size_t HW = (size_t)H * W, plane3 = 3 * HW;
+    for (int g = 0; g < G; ++g) {
+        float* set = fgp3d_set(sl[g].work, which, sl[g].Zl, H, W);
+        if (g > 0) {
+            const float* lo = fgp3d_set(sl[g - 1].work, which, sl[g - 1].Zl, H, W);
+            PT_CHECK_CUDA(cudaMemcpyAsync(set, lo + (size_t)sl[g - 1].Zl * plane3, plane3 * 4,
+                                          cudaMemcpyDeviceToDevice, st));
+        }
+        if (g + 1 < G) {
+            const float* hi = fgp3d_set(sl[g + 1].work, which, sl[g + 1].Zl, H, W);
+            PT_CHECK_CUDA(cudaMemcpyAsync(set + (size_t)(sl[g].Zl + 1) * plane3, hi + plane3,
+                                          plane3 * 4, cudaMemcpyDeviceToDevice, st));
+            if (with_v)
+                PT_CHECK_CUDA(cudaMemcpyAsync(fgp3d_vtop(sl[g].work, sl[g].Zl, H, W), sl[g + 1].v,
+                                              HW * 4, cudaMemcpyDeviceToDevice, st));
+        }
     }
-    fgp3d_final_kernel<<<blocks, 256, 0, st>>>(a, x_out, xhat, h, pog, (long long)iteration,
-                                               (long long*)bad_iter);
+    if (halo && halo->world > 1) {
+        // remote neighbours of the first / last local slab
+        const Fgp3Slab& f = sl[0];
+        const Fgp3Slab& l = sl[G - 1];
+        float* fs = fgp3d_set(f.work, which, f.Zl, H, W);
+        float* ls = fgp3d_set(l.work, which, l.Zl, H, W);
+        int rc = halo->exchange(halo->ctx, fs + plane3, fs, ls + (size_t)l.Zl * plane3,
+                                ls + (size_t)(l.Zl + 1) * plane3, plane3, st);
+        if (rc) return rc;
+        if (with_v) {
+            rc = halo->exchange(halo->ctx, f.v, nullptr, nullptr, fgp3d_vtop(l.work, l.Zl, H, W),
+                                HW, st);
+            if (rc) return rc;
+        }
+    }
+    return PT_OK;
+}
+
+typedef CUresult (*fn_encode_tiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static fn_encode_tiled encode_tiled()
+{
+    static fn_encode_tiled fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+                cudaSuccess || q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return (fn_encode_tiled)p;
+    }();
+    return fn;
+}
+
+// float32 tensor of `rank` dims (innermost first, dense), box `box`
+static int make_map(CUtensorMap* m, const float* base, int rank, const cuuint64_t* dims,
+                    const cuuint32_t* box)
+{
+    fn_encode_tiled enc = encode_tiled();
+    if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return PT_ECUDA; }
+    cuuint64_t strides[4];
+    cuuint64_t acc = 4;
+    for (int d = 0; d + 1 < rank; ++d) {
+        acc *= dims[d];
+        strides[d] = acc;
+    }
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, (void*)base, dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed (%d)", (int)r); return PT_ECUDA; }
+    return PT_OK;
+}
+
+template <int TX, int TY, int NS, bool TMA>
+static int fgp3d_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
+{
+    using T = Fgp3Tile<TX, TY, NS>;
+    const size_t smem = (size_t)T::SMEM_FLOATS * 4;
+    static bool attr = false;
+    if (!attr) {
+        PT_CHECK_CUDA(cudaFuncSetAttribute(fgp3d_iter_kernel<TX, TY, NS, TMA>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    Fgp3Maps m;
+    memset(&m, 0, sizeof(m));
+    if (TMA) {
+        const cuuint64_t W = a.W, H = a.H;
+        const cuuint64_t d4[4] = {W, H, 3, (cuuint64_t)a.Zl + 2};
+        const cuuint32_t bR[4] = {(cuuint32_t)T::RW, (cuuint32_t)T::RR, 3, 1};
+        const cuuint32_t bP[4] = {(cuuint32_t)TX, (cuuint32_t)TY, 3, 1};
+        const cuuint64_t d3[3] = {W, H, (cuuint64_t)a.Zl};
+        const cuuint32_t b3[3] = {(cuuint32_t)T::RW, (cuuint32_t)T::RR, 1};
+        int rc = make_map(&m.R, a.R, 4, d4, bR);
+        if (!rc) rc = make_map(&m.P, a.P, 4, d4, bP);
+        if (!rc) rc = make_map(&m.V, a.v, 3, d3, b3);
+        if (!rc) rc = make_map(&m.Vt, a.vtop, 2, d3, b3);
+        if (rc) return rc;
+    }
+    static const int zc_env = [] {
+        const char* e = getenv("PT_FGP3_ZCHUNK");
+        return e ? std::max(1, atoi(e)) : 0;
+    }();
+    const int gx = (a.W + TX - 1) / TX, gy = (a.H + TY - 1) / TY;
+    // runs of 16 planes (two extra staged planes per run); measured at 256^3:
+    // 8 -> 155 us, 16 -> 153 us, 32 -> 165 us, 64 -> 189 us per iteration
+    a.zchunk = zc_env ? zc_env : 16;
+    dim3 grid(gx, gy, (a.Zl + a.zchunk - 1) / a.zchunk);
+    fgp3d_iter_kernel<TX, TY, NS, TMA><<<grid, T::NT, smem, st>>>(a, m);
     PT_CHECK_LAUNCH();
     return PT_OK;
 }
 
+int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int inner,
+              int nonneg, float pog, int64_t iteration, int64_t* bad_iter, const ZHalo* halo,
+              int sm_count, cudaStream_t st)
+{
+    // TMA needs 16-byte row pitch; 64 x 8 tiles, 3-stage ring
+    const bool tma = (W % 4) == 0 && encode_tiled() != nullptr;
+    std::vector<double> betas(inner);
+    double t = 1.0;
+    for (int k = 0; k < inner; ++k) {
+        const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
+        betas[k] = (t - 1.0) / tn;
+        t = tn;
+    }
+    const size_t plane3 = 3 * (size_t)H * W;
+    for (int g = 0; g < G; ++g) {
+        const int Zl = sl[g].Zl;
+        const size_t n = (size_t)Zl * H * W;
+        const int blocks = (int)std::min<size_t>((n + 255) / 256, (size_t)sm_count * 16);
+        fgp3d_pack_kernel<<<blocks, 256, 0, st>>>(sl[g].p, sl[g].q, sl[g].w,
+                                                  fgp3d_set(sl[g].work, 0, Zl, H, W),
+                                                  fgp3d_set(sl[g].work, 1, Zl, H, W), Zl, H, W);
+        PT_CHECK_LAUNCH();
+        // ghost planes on the global boundary stay zero (never exchanged)
+        for (int k = 0; k < 4; ++k) {
+            float* set = fgp3d_set(sl[g].work, k, Zl, H, W);
+            if (sl[g].z0 == 0) PT_CHECK_CUDA(cudaMemsetAsync(set, 0, plane3 * 4, st));
+            if (sl[g].z0 + Zl == Zg)
+                PT_CHECK_CUDA(cudaMemsetAsync(set + (size_t)(Zl + 1) * plane3, 0, plane3 * 4, st));
+        }
+    }
+    int rc = fgp3d_exchange(sl, G, H, W, 1, true, halo, st);
+    if (rc) return rc;
+    for (int kk = 0; kk < inner; ++kk) {
+        const int in = (kk & 1) ? 2 : 0, out = (kk & 1) ? 0 : 2;  // P set; R = P + 1
+        for (int g = 0; g < G; ++g) {
+            const int Zl = sl[g].Zl;
+            Fgp3Args a;
+            a.Zl = Zl; a.H = H; a.W = W; a.z0 = sl[g].z0; a.Zg = Zg;
+            a.v = sl[g].v;
+            a.vtop = fgp3d_vtop(sl[g].work, Zl, H, W);
+            a.P = fgp3d_set(sl[g].work, in, Zl, H, W);
+            a.R = fgp3d_set(sl[g].work, in + 1, Zl, H, W);
+            a.Pn = fgp3d_set(sl[g].work, out, Zl, H, W);
+            a.Rn = fgp3d_set(sl[g].work, out + 1, Zl, H, W);
+            a.lam = (float)lam;
+            a.eta = (float)(1.0 / (12.0 * lam));
+            a.beta = (float)betas[kk];
+            a.nonneg = nonneg;
+            rc = tma ? fgp3d_launch<64, 8, 3, true>(a, sm_count, st)
+                     : fgp3d_launch<32, 8, 3, false>(a, sm_count, st);
+            if (rc) return rc;
+        }
+        rc = fgp3d_exchange(sl, G, H, W, out + 1, false, halo, st);
+        if (rc) return rc;
+    }
+    const int fin = (inner & 1) ? 2 : 0;
+    rc = fgp3d_exchange(sl, G, H, W, fin, false, halo, st);  // P ghost below for D^T
+    if (rc) return rc;
+    for (int g = 0; g < G; ++g) {
+        const int Zl = sl[g].Zl;
+        Fgp3Args a;
+        a.Zl = Zl; a.H = H; a.W = W; a.z0 = sl[g].z0; a.Zg = Zg;
+        a.v = sl[g].v;
+        a.P = fgp3d_set(sl[g].work, fin, Zl, H, W);
+        a.lam = (float)lam;
+        a.nonneg = nonneg;
+        const size_t n = (size_t)Zl * H * W;
+        const int blocks = (int)std::min<size_t>((n + 255) / 256, (size_t)sm_count * 16);
+        fgp3d_final_kernel<<<blocks, 256, 0, st>>>(a, sl[g].p, sl[g].q, sl[g].w, sl[g].x_out,
+                                                   sl[g].xhat, sl[g].h, pog,
+                                                   (long long)iteration, (long long*)bad_iter);
+        PT_CHECK_LAUNCH();
+    }
+    return PT_OK;
+}
 
 int launch_tv_prox(pt_plan* plan, const float* v, double lam, int inner, int nonneg, float* p,
                    float* q, float* w, float* x_out, const float* xhat, float* h,
@@ -539,9 +927,14 @@ int launch_tv_prox(pt_plan* plan, const float* v, double lam, int inner, int non
         set_error("inner_iterations must be >= 1");
         return PT_EINVAL;
     }
-    if (plan->Z > 1)
-        return launch_fgp3d(plan, v, lam, inner, nonneg, p, q, w, x_out, xhat, h, p_over_gamma,
-                            iteration, bad_iter, work, st);
+    if (plan->Z > 1) {
+        Fgp3Slab sl;
+        sl.Zl = plan->Z; sl.z0 = 0;
+        sl.v = v; sl.p = p; sl.q = q; sl.w = w;
+        sl.x_out = x_out; sl.xhat = xhat; sl.h = h; sl.work = work;
+        return fgp3d_run(&sl, 1, plan->H, plan->W, plan->Z, lam, inner, nonneg, p_over_gamma,
+                         iteration, bad_iter, nullptr, plan->sm_count, st);
+    }
     if (std::min(plan->H, plan->W) >= 256)
     {
         static const int tmax = [] {

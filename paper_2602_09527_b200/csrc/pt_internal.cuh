@@ -144,6 +144,30 @@ int launch_tv_prox(pt_plan* plan, const float* v, double lam, int inner, int non
                    float* q, float* w, float* x_out, const float* xhat, float* h,
                    float p_over_gamma, int64_t iteration, int64_t* bad_iter, float* work,
                    cudaStream_t st);
+// 3D FGP on z-slabs: a slab owns global planes [z0, z0 + Zl); `work` holds
+// fgp3d_slab_floats(Zl, H, W) floats.  ZHalo moves boundary planes between
+// ranks: send `count` floats from send_lo to rank - 1 and from send_hi to
+// rank + 1, receive into recv_lo from rank - 1 and into recv_hi from rank + 1
+// (null pointers skip a direction; ranks 0 / world - 1 have no outer side).
+struct Fgp3Slab {
+    int Zl = 0, z0 = 0;
+    const float* v = nullptr;
+    float *p = nullptr, *q = nullptr, *w = nullptr;
+    float* x_out = nullptr;
+    const float* xhat = nullptr;
+    float* h = nullptr;
+    float* work = nullptr;
+};
+struct ZHalo {
+    int rank = 0, world = 1;
+    void* ctx = nullptr;
+    int (*exchange)(void* ctx, const float* send_lo, float* recv_lo, const float* send_hi,
+                    float* recv_hi, size_t count, cudaStream_t st) = nullptr;
+};
+int64_t fgp3d_slab_floats(int Zl, int H, int W);
+int fgp3d_run(const Fgp3Slab* slabs, int G, int H, int W, int Zg, double lam, int inner,
+              int nonneg, float pog, int64_t iteration, int64_t* bad_iter, const ZHalo* halo,
+              int sm_count, cudaStream_t st);
 // reduce.cu  (out: device doubles, out[0] = result, out[1 .. PT_RED_DOUBLES) scratch)
 int launch_dot(const float* a, const float* b, int64_t n, double* out, cudaStream_t st);
 int launch_tv_value(const pt_plan* plan, const float* x, double* out, cudaStream_t st);

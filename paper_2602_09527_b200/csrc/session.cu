@@ -35,6 +35,8 @@ typedef int (*fn_init_rank)(nccl_comm*, int, nccl_uid, int);
 typedef int (*fn_allreduce)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t);
 typedef int (*fn_destroy)(nccl_comm);
 typedef const char* (*fn_errstr)(int);
+typedef int (*fn_p2p)(const void*, size_t, int, int, nccl_comm, cudaStream_t);
+typedef int (*fn_group)(void);
 constexpr int kNcclFloat32 = 7;
 constexpr int kNcclSum = 0;
 
@@ -45,6 +47,8 @@ struct NcclApi {
     fn_allreduce allreduce = nullptr;
     fn_destroy destroy = nullptr;
     fn_errstr errstr = nullptr;
+    fn_p2p send = nullptr, recv = nullptr;  // ncclSend / ncclRecv (z-slab halos)
+    fn_group group_start = nullptr, group_end = nullptr;
 };
 
 int nccl_load(const char* path, NcclApi* api)
@@ -59,6 +63,10 @@ int nccl_load(const char* path, NcclApi* api)
     api->allreduce = (fn_allreduce)dlsym(api->so, "ncclAllReduce");
     api->destroy = (fn_destroy)dlsym(api->so, "ncclCommDestroy");
     api->errstr = (fn_errstr)dlsym(api->so, "ncclGetErrorString");
+    api->send = (fn_p2p)dlsym(api->so, "ncclSend");
+    api->recv = (fn_p2p)dlsym(api->so, "ncclRecv");
+    api->group_start = (fn_group)dlsym(api->so, "ncclGroupStart");
+    api->group_end = (fn_group)dlsym(api->so, "ncclGroupEnd");
     if (!api->get_uid || !api->init_rank || !api->allreduce || !api->destroy) {
         pt::set_error("libnccl is missing symbols");
         return PT_ENCCL;
@@ -147,6 +155,16 @@ struct pt_session {
     NcclApi nccl;
     nccl_comm comm = nullptr;
     int rank = 0, world = 1;
+    // z-slab mode (3D): this rank owns global planes [z0, z0 + Z)
+    // of Zg; projector and snapshot are slab-local, the FGP exchanges halos
+    bool zslab = false;
+    int z0 = 0, Zg = 0;
+    float* fgp3_work = nullptr;  // slab FGP workspace (own allocation)
+    float* dw_slab = nullptr;    // third dual when the slab plan is 2D (Z = 1)
+    pt::ZHalo halo;
+    // test hook: G virtual z-slabs of this volume on one device
+    int emu_z = 1;
+    float* emu_z_work = nullptr;
 };
 
 namespace {
@@ -205,15 +223,16 @@ int build_selections(pt_session* s)
 {
     pt_plan* P = s->plan;
     const int A = P->A;
-    const int lo = (int)((long long)A * s->rank / s->world);
-    const int hi = (int)((long long)A * (s->rank + 1) / s->world);
+    const int world = s->zslab ? 1 : s->world, rank = s->zslab ? 0 : s->rank;
+    const int lo = (int)((long long)A * rank / world);
+    const int hi = (int)((long long)A * (rank + 1) / world);
     const int n = (s->d.estimator != PT_EST_FULL) ? s->d.n_subsets : 0;
     return sector_selections(P, n, lo, hi, &s->own_all, &s->subsets);
 }
 
 int allreduce(pt_session* s, float* buf, cudaStream_t st)
 {
-    if (!s->comm) return PT_OK;
+    if (!s->comm || s->zslab) return PT_OK;
     int e = s->nccl.allreduce(buf, buf, s->n, kNcclFloat32, kNcclSum, s->comm, st);
     if (e != 0) {
         pt::set_error("ncclAllReduce: %s", s->nccl.errstr ? s->nccl.errstr(e) : "error");
@@ -259,8 +278,62 @@ int full_gradient(pt_session* s, const float* x, float* out, float* res, cudaStr
 // The snapshot residual indexed by geometry angle (rows [lo, hi) are owned).
 const float* rsnap_by_angle(const pt_session* s)
 {
-    const int lo = (int)((long long)s->plan->A * s->rank / s->world);
+    const int lo = s->zslab ? 0 : (int)((long long)s->plan->A * s->rank / s->world);
     return s->rsnap - (ptrdiff_t)lo * s->plan->Z * s->plan->B;
+}
+
+// Halo exchange with the z-neighbours (ncclSend / ncclRecv in one group).
+int nccl_halo(void* ctx, const float* send_lo, float* recv_lo, const float* send_hi,
+              float* recv_hi, size_t count, cudaStream_t st)
+{
+    pt_session* s = (pt_session*)ctx;
+    const NcclApi& api = s->nccl;
+    const bool lo = s->rank > 0, hi = s->rank + 1 < s->world;
+    int e = api.group_start();
+    if (!e && lo && send_lo) e = api.send(send_lo, count, kNcclFloat32, s->rank - 1, s->comm, st);
+    if (!e && lo && recv_lo) e = api.recv(recv_lo, count, kNcclFloat32, s->rank - 1, s->comm, st);
+    if (!e && hi && send_hi) e = api.send(send_hi, count, kNcclFloat32, s->rank + 1, s->comm, st);
+    if (!e && hi && recv_hi) e = api.recv(recv_hi, count, kNcclFloat32, s->rank + 1, s->comm, st);
+    const int e2 = api.group_end();
+    if (e || e2) {
+        pt::set_error("NCCL halo exchange: %s", api.errstr ? api.errstr(e ? e : e2) : "error");
+        return PT_ENCCL;
+    }
+    return PT_OK;
+}
+
+// The 3D TV prox of a z-slab rank (halos over NCCL), or of G virtual slabs of
+// this volume on one device (halos by device copies).
+int slab_tv_prox(pt_session* s, double lam, float pog, float* xn, int64_t k, cudaStream_t st)
+{
+    pt_plan* P = s->plan;
+    const size_t HW = (size_t)P->H * P->W;
+    float* dw = s->dw ? s->dw : s->dw_slab;
+    std::vector<pt::Fgp3Slab> sl;
+    if (s->zslab) {
+        pt::Fgp3Slab a;
+        a.Zl = P->Z; a.z0 = s->z0;
+        a.v = s->v; a.p = s->dp; a.q = s->dq; a.w = dw;
+        a.x_out = xn; a.xhat = s->xhat; a.h = s->h; a.work = s->fgp3_work;
+        sl.push_back(a);
+    } else {
+        float* work = s->emu_z_work;
+        for (int g = 0; g < s->emu_z; ++g) {
+            const int za = (int)((long long)P->Z * g / s->emu_z);
+            const int zb = (int)((long long)P->Z * (g + 1) / s->emu_z);
+            const size_t off = (size_t)za * HW;
+            pt::Fgp3Slab a;
+            a.Zl = zb - za; a.z0 = za;
+            a.v = s->v + off; a.p = s->dp + off; a.q = s->dq + off; a.w = dw + off;
+            a.x_out = xn + off; a.xhat = s->xhat + off; a.h = s->h + off; a.work = work;
+            work += pt::fgp3d_slab_floats(a.Zl, P->H, P->W);
+            sl.push_back(a);
+        }
+    }
+    const int Zg = s->zslab ? s->Zg : P->Z;
+    return pt::fgp3d_run(sl.data(), (int)sl.size(), P->H, P->W, Zg, lam, s->d.tv_inner,
+                         s->d.tv_nonneg, pog, k, s->bad, s->zslab ? &s->halo : nullptr,
+                         P->sm_count, st);
 }
 
 }  // namespace
@@ -352,6 +425,9 @@ int pt_session_destroy(pt_session* s)
     if (s->bad) cudaFree(s->bad);
     pt::workspace_free(&s->ws);
     if (s->comm && s->nccl.destroy) s->nccl.destroy(s->comm);
+    if (s->fgp3_work) cudaFree(s->fgp3_work);
+    if (s->dw_slab) cudaFree(s->dw_slab);
+    if (s->emu_z_work) cudaFree(s->emu_z_work);
     delete s;
     return PT_OK;
 }
@@ -448,7 +524,7 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
                 if (!rc) rc = pt::launch_adjoint(P, sg, s->r, s->g, 1.f, g > 0, nullptr, st, &s->ws);
             }
             if (!rc) rc = pt::launch_epilogue(P, s->g, &ep, st);
-        } else if (!s->comm) {
+        } else if (!s->comm || s->zslab) {
             rc = pt::launch_adjoint(P, sel, s->r, nullptr, 1.f, 0, &ep, st, &s->ws);
         } else {
             if (sel->n == 0) {
@@ -470,13 +546,18 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
                 const bool warm = d.tv_warm_start && s->have_duals &&
                                   fabs(s->dual_weight - lam) <= 1e-12 * fabs(lam);
                 pt::ProfScope ps(&s->ws, PT_PROF_FGP, st);
+                float* dw = s->dw ? s->dw : s->dw_slab;
                 if (!warm) {
                     PT_CHECK_CUDA(cudaMemsetAsync(s->dp, 0, s->n * 4, st));
                     PT_CHECK_CUDA(cudaMemsetAsync(s->dq, 0, s->n * 4, st));
-                    if (s->dw) PT_CHECK_CUDA(cudaMemsetAsync(s->dw, 0, s->n * 4, st));
+                    if (dw) PT_CHECK_CUDA(cudaMemsetAsync(dw, 0, s->n * 4, st));
                 }
-                rc = pt::launch_tv_prox(P, s->v, lam, d.tv_inner, d.tv_nonneg, s->dp, s->dq,
-                                        s->dw, xn, s->xhat, s->h, pog, k, s->bad, s->fgp_work, st);
+                if (s->zslab || s->emu_z > 1)
+                    rc = slab_tv_prox(s, lam, pog, xn, k, st);
+                else
+                    rc = pt::launch_tv_prox(P, s->v, lam, d.tv_inner, d.tv_nonneg, s->dp, s->dq,
+                                            s->dw, xn, s->xhat, s->h, pog, k, s->bad,
+                                            s->fgp_work, st);
                 s->have_duals = true;
                 s->dual_weight = lam;
             } else {
@@ -525,7 +606,7 @@ float* pt_session_buffer(pt_session* s, int32_t which)
         case 3: return s->saga_table;
         case 4: return s->dp;
         case 5: return s->dq;
-        case 6: return s->dw;
+        case 6: return s->dw ? s->dw : s->dw_slab;
         default: return nullptr;
     }
 }
@@ -558,6 +639,62 @@ int pt_session_emulate_sectors(pt_session* s, int32_t world)
     }
     s->emu = world;
     return PT_OK;
+}
+
+int pt_session_emulate_zslabs(pt_session* s, int32_t slabs)
+{
+    if (!s || slabs < 1) { pt::set_error("bad argument"); return PT_EINVAL; }
+    if (s->comm) { pt::set_error("session already attached to NCCL"); return PT_EINVAL; }
+    pt_plan* P = s->plan;
+    if (slabs > P->Z) { pt::set_error("more slabs (%d) than slices (%d)", slabs, P->Z); return PT_EINVAL; }
+    if (s->d.prox_kind != 1) { pt::set_error("z-slabs only change the TV prox"); return PT_EINVAL; }
+    int64_t total = 0;
+    for (int g = 0; g < slabs; ++g) {
+        const int za = (int)((long long)P->Z * g / slabs), zb = (int)((long long)P->Z * (g + 1) / slabs);
+        total += pt::fgp3d_slab_floats(zb - za, P->H, P->W);
+    }
+    if (s->emu_z_work) cudaFree(s->emu_z_work);
+    s->emu_z_work = nullptr;
+    PT_CHECK_CUDA(cudaMalloc(&s->emu_z_work, (size_t)total * sizeof(float)));
+    s->emu_z = slabs;
+    return PT_OK;
+}
+
+int pt_session_attach_nccl_zslab(pt_session* s, const char* nccl_path, const uint8_t* host_id128,
+                                 int32_t rank, int32_t world, int32_t z_offset, int32_t z_total)
+{
+    if (!s || !host_id128 || world < 1 || rank < 0 || rank >= world) { pt::set_error("bad argument"); return PT_EINVAL; }
+    if (s->comm) { pt::set_error("session already attached"); return PT_EINVAL; }
+    pt_plan* P = s->plan;
+    if (z_offset < 0 || z_total < 2 || z_offset + P->Z > z_total) {
+        pt::set_error("slab [%d, %d) outside a volume of %d planes", z_offset, z_offset + P->Z, z_total);
+        return PT_EINVAL;
+    }
+    int rc = nccl_load(nccl_path, &s->nccl);
+    if (rc) return rc;
+    if (!s->nccl.send || !s->nccl.recv || !s->nccl.group_start || !s->nccl.group_end) {
+        pt::set_error("libnccl lacks ncclSend/ncclRecv");
+        return PT_ENCCL;
+    }
+    if (s->d.prox_kind == 1) {
+        PT_CHECK_CUDA(cudaMalloc(&s->fgp3_work,
+                                 (size_t)pt::fgp3d_slab_floats(P->Z, P->H, P->W) * sizeof(float)));
+        if (!s->dw) PT_CHECK_CUDA(cudaMalloc(&s->dw_slab, s->n * sizeof(float)));
+    }
+    nccl_uid id;
+    memcpy(id.internal, host_id128, 128);
+    int e = s->nccl.init_rank(&s->comm, world, id, rank);
+    if (e != 0) { pt::set_error("ncclCommInitRank failed (%d)", e); return PT_ENCCL; }
+    s->rank = rank;
+    s->world = world;
+    s->zslab = true;
+    s->z0 = z_offset;
+    s->Zg = z_total;
+    s->halo.rank = rank;
+    s->halo.world = world;
+    s->halo.ctx = s;
+    s->halo.exchange = nccl_halo;
+    return build_selections(s);
 }
 
 int pt_session_attach_nccl(pt_session* s, const char* nccl_path, const uint8_t* host_id128,

@@ -1,4 +1,5 @@
-"""Multi-GPU angle-sector data parallelism (one process per GPU).
+"""Multi-GPU data parallelism (one process per GPU): angle sectors (2D) and
+z-slabs (slice-stacked 3D).
 
 Rank g of G owns the contiguous sinogram rows of angles
 [g*A/G, (g+1)*A/G) (geometry.angle_sector).  Staggered subsets therefore
@@ -79,3 +80,79 @@ def replicas_identical(x: torch.Tensor, group=None) -> bool:
     dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
     dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
     return bool(torch.equal(lo, hi))
+
+
+# ---------------------------------------------------------------------------
+# z-slab decomposition of slice-stacked 3D problems
+# ---------------------------------------------------------------------------
+
+def zslab_bounds(n_slices: int, rank: int, world: int) -> tuple[int, int]:
+    """Rank g of G owns planes [g Z / G, (g + 1) Z / G) (contiguous, in rank order)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank / world")
+    if n_slices < world:
+        raise ValueError(f"{n_slices} slices cannot be split over {world} ranks")
+    return n_slices * rank // world, n_slices * (rank + 1) // world
+
+
+def zslab_problem(problem, z0: int, z1: int):
+    """The slab [z0, z1) of a 3D TomoProblem: same geometry and regulariser,
+    its own projector (Z = z1 - z0) and the matching sinogram rows (A, Zl, B)
+    (slices never interact in the projector: rotation is about z)."""
+    from .projector import Projector
+    from .solvers import TomoProblem
+    proj = problem.projector
+    zl = z1 - z0
+    sub = Projector(proj.geometry, proj.width, proj.height, n_slices=zl)
+    data = problem.data
+    if isinstance(data, torch.Tensor):
+        slab = data[:, z0:z1, :].contiguous()
+    else:
+        import numpy as np
+        slab = np.ascontiguousarray(np.asarray(data)[:, z0:z1, :])
+    if zl == 1:
+        slab = slab.reshape(slab.shape[0], slab.shape[2])
+    return TomoProblem(sub, slab, tv=problem.tv, denoiser=problem.denoiser)
+
+
+def attach_zslab(session, z0: int, z_total: int, rank: int | None = None,
+                 world: int | None = None, group=None) -> None:
+    """Attach a slab session to an NCCL communicator for the z halo exchange."""
+    rank = dist.get_rank(group) if rank is None else rank
+    world = dist.get_world_size(group) if world is None else world
+    path = nccl_library_path().encode()
+
+    def make_uid() -> bytes:
+        uid = (ctypes.c_uint8 * 128)()
+        N.check(N.lib().pt_nccl_unique_id(path, uid), "ncclGetUniqueId")
+        return bytes(uid)
+
+    payload = share_unique_id(make_uid, rank, group)
+    uid = (ctypes.c_uint8 * 128)(*payload)
+    N.check(N.lib().pt_session_attach_nccl_zslab(session.handle, path, uid, rank, world,
+                                                 int(z0), int(z_total)), "attach_zslab")
+
+
+def emulate_zslabs(session, slabs: int) -> None:
+    """Single-device emulation of `slabs` z-slab ranks for the 3D TV prox (test hook)."""
+    N.check(N.lib().pt_session_emulate_zslabs(session.handle, int(slabs)), "emulate_zslabs")
+
+
+def gather_zslabs(x_slab: torch.Tensor, n_slices: int, group=None) -> torch.Tensor:
+    """The full (Z, H, W) volume on every rank from each rank's slab (log rows
+    and the final image only; padded all_gather over the process group)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    H, W = x_slab.shape[-2], x_slab.shape[-1]
+    zmax = max(zslab_bounds(n_slices, g, world)[1] - zslab_bounds(n_slices, g, world)[0]
+               for g in range(world))
+    buf = torch.zeros((zmax, H, W), device=x_slab.device, dtype=x_slab.dtype)
+    z0, z1 = zslab_bounds(n_slices, rank, world)
+    buf[:z1 - z0] = x_slab.reshape(z1 - z0, H, W)
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    out = torch.empty((n_slices, H, W), device=x_slab.device, dtype=x_slab.dtype)
+    for g in range(world):
+        a, b = zslab_bounds(n_slices, g, world)
+        out[a:b] = parts[g][:b - a]
+    return out

@@ -204,10 +204,18 @@ class IterateState:
     prox_calls: int = 0
     denoiser_calls: int = 0
     work_seconds: float = 0.0
+    zslab: tuple | None = None  # (z0, z1, Z) when this rank holds a z-slab
 
     @property
     def x(self) -> torch.Tensor:
         return self.session.x
+
+    def full_x(self) -> torch.Tensor:
+        """The whole iterate (a z-slab rank gathers the other slabs)."""
+        if self.zslab is None:
+            return self.session.x
+        from . import distributed as _dist
+        return _dist.gather_zslabs(self.session.x, self.zslab[2])
 
     @property
     def h(self) -> torch.Tensor:
@@ -268,12 +276,13 @@ class RunRecord:
 
 
 def _init_state(config: SolverConfig, problem: TomoProblem, x0, stream=None,
-                data_parallel: bool = False) -> IterateState:
+                data_parallel: bool = False, zslab: tuple | None = None) -> IterateState:
     """solvers.py:159-186: x0 (or zeros), h = 0, three PCG64 streams, the
     staggered partition, SAGA zeros, SVRG initial snapshot (+1 pass).
 
     data_parallel: shard the angles over the torch.distributed ranks (one GPU
-    each; the library's own NCCL communicator, see distributed.py)."""
+    each; the library's own NCCL communicator, see distributed.py); with
+    `zslab` = (z0, z1, Z) the problem is this rank's z-slab instead."""
     shape = problem.projector.shape
     if x0 is not None and tuple(x0.shape) != tuple(shape):
         raise ValueError(f"x0 shape {tuple(x0.shape)} does not match grid {shape}")
@@ -284,13 +293,16 @@ def _init_state(config: SolverConfig, problem: TomoProblem, x0, stream=None,
                                               config.n_subsets)
     stream = stream if stream is not None else torch.cuda.current_stream()
     session = _Session(config, problem, x0, stream)
-    if data_parallel:
+    if zslab is not None:
+        from . import distributed as _dist
+        _dist.attach_zslab(session, zslab[0], zslab[2])
+    elif data_parallel:
         from . import distributed as _dist
         _dist.attach(session)
     state = IterateState(session=session, partition=partition,
                          rng_subset=np.random.default_rng(streams[0]),
                          rng_theta=np.random.default_rng(streams[1]),
-                         rng_refresh=np.random.default_rng(streams[2]))
+                         rng_refresh=np.random.default_rng(streams[2]), zslab=zslab)
     if config.estimator in ("svrg", "lsvrg"):
         if config.estimator == "svrg":
             state.svrg_period = config.n_subsets
@@ -390,7 +402,7 @@ def proxskip_step(state: IterateState, config: SolverConfig, problem: TomoProble
     """One iteration of the skip-capable loop (:230-254), on the device."""
     i, theta, refresh, passes = _draw_one(state, config)
     state.session.run(np.array([i]), np.array([theta]), np.array([refresh]), state.k)
-    bad = state.session.bad_iteration()
+    bad = _bad_iteration(state)
     if bad is not None:
         raise DivergenceError(bad, config.gamma)
     if theta:
@@ -438,11 +450,22 @@ def run(config: SolverConfig, problem: TomoProblem, x0=None, reference=None,
     Rows are logged at every data-pass boundary exactly as :280-324; the
     iterations between two rows are one native segment.  The host syncs only
     at rows that need a metric (or for a time budget) and at the end.
-    data_parallel=True shards the projection angles over the torch.distributed
-    ranks (every rank calls run with the same arguments)."""
+    data_parallel=True shards the work over the torch.distributed ranks (every
+    rank calls run with the same arguments): the projection angles of a 2D
+    problem, the z-slabs of a slice-stacked 3D one (the returned image is the
+    gathered volume on every rank)."""
     stream = stream if stream is not None else torch.cuda.current_stream()
+    work, zs = problem, None
+    if data_parallel and getattr(problem.projector, "n_slices", 1) > 1:
+        import torch.distributed as dist
+        from . import distributed as _dist
+        Z = problem.projector.n_slices
+        z0, z1 = _dist.zslab_bounds(Z, dist.get_rank(), dist.get_world_size())
+        work, zs = _dist.zslab_problem(problem, z0, z1), (z0, z1, Z)
+        if x0 is not None:
+            x0 = as_device(x0)[z0:z1].contiguous().reshape(work.projector.shape)
     with torch.cuda.stream(stream):
-        state = _init_state(config, problem, x0, stream, data_parallel=data_parallel)
+        state = _init_state(config, work, x0, stream, data_parallel=data_parallel, zslab=zs)
         return _run_loop(state, config, problem, reference, ground_truth, record_objective,
                          stream)
 
@@ -456,7 +479,7 @@ def _run_loop(state: IterateState, config, problem, reference, ground_truth,
     events[0].record(stream)
 
     def log_row(wall):
-        x = state.x
+        x = state.full_x()
         row = _metrics_row(state.data_passes, wall, x, reference, ground_truth,
                            state.prox_calls, problem, record_objective)
         record.rows.append(row)
@@ -469,7 +492,7 @@ def _run_loop(state: IterateState, config, problem, reference, ground_truth,
 
     row = log_row(0.0)
     if satisfied(row):
-        record.image = state.x.clone()
+        record.image = state.full_x().clone()
         return record
     last_floor = math.floor(state.data_passes + 1e-12)
     budget = config.time_budget
@@ -489,7 +512,7 @@ def _run_loop(state: IterateState, config, problem, reference, ground_truth,
                                   + events[-2].elapsed_time(events[-1]) / 1e3)
             if budget is not None:
                 exhausted = exhausted or state.work_seconds >= budget
-            bad = state.session.bad_iteration()
+            bad = _bad_iteration(state)
             if bad is not None:
                 raise _diverged(bad, config, record)
         crossed = math.floor(state.data_passes + 1e-12) > last_floor
@@ -514,12 +537,25 @@ def _run_loop(state: IterateState, config, problem, reference, ground_truth,
             r = record.rows[ri]
             record.rows[ri] = (r[0], cum[ei]) + tuple(r[2:])
         state.work_seconds = cum[-1]
-    bad = state.session.bad_iteration()
+    bad = _bad_iteration(state)
     if bad is not None:
         raise _diverged(bad, config, record)
-    record.image = state.x.clone()
+    record.image = state.full_x().clone()
     record.state = state
     return record
+
+
+def _bad_iteration(state: IterateState) -> int | None:
+    """First non-finite iteration (z-slab ranks: the minimum over ranks, so
+    every rank raises together)."""
+    bad = state.session.bad_iteration()
+    if state.zslab is None:
+        return bad
+    import torch.distributed as dist
+    t = torch.tensor([INT64_MAX if bad is None else bad], device="cuda", dtype=torch.int64)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    v = int(t.item())
+    return None if v == INT64_MAX else v
 
 
 def _diverged(bad: int, config: SolverConfig, record: RunRecord) -> DivergenceError:

@@ -91,3 +91,143 @@ def test_two_rank_sector_logic_over_gloo():
         assert results[r]["uid_ok"]
         assert results[r]["schedule_ok"]
         assert results[r]["sector_sum_err"] <= 1e-12
+
+
+# ---------------------------------------------------------------------------
+# z-slab decomposition (3D): the halo protocol of csrc/fgp.cu fgp3d_run,
+# restated in float64 numpy per rank with gloo send/recv for the ghost planes,
+# must reproduce the single-volume 3D FGP of the oracle.
+# ---------------------------------------------------------------------------
+
+def _slab_fgp(v_loc, z0, Zg, lam, inner, nonneg, rank, world):
+    import torch
+    zl, H, W = v_loc.shape
+
+    def exchange(S, send_lo, send_hi):
+        """ghost planes of S ([zl + 2, ...]): plane 0 from rank - 1, plane zl + 1 from rank + 1"""
+        reqs = []
+        if rank > 0:
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(send_lo)), rank - 1))
+            lo = torch.empty(send_lo.shape, dtype=torch.float64)
+            reqs.append(dist.irecv(lo, rank - 1))
+        if rank + 1 < world:
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(send_hi)), rank + 1))
+            hi = torch.empty(send_hi.shape, dtype=torch.float64)
+            reqs.append(dist.irecv(hi, rank + 1))
+        for r in reqs:
+            r.wait()
+        if rank > 0:
+            S[0] = lo.numpy()
+        if rank + 1 < world:
+            S[zl + 1] = hi.numpy()
+
+    def dt(R, z):  # D^T of R at local plane z (global guards)
+        zg = z0 + z
+        p, q, w = R[z + 1, 0], R[z + 1, 1], R[z + 1, 2]
+        x = np.zeros((H, W))
+        x[:-1] -= p[:-1]
+        x[1:] += p[:-1]
+        x[:, :-1] -= q[:, :-1]
+        x[:, 1:] += q[:, :-1]
+        if zg < Zg - 1:
+            x -= w
+        if zg > 0:
+            x += R[z, 2]
+        return x
+
+    vt = np.zeros((H, W))  # ghost v above
+    tmp = np.zeros((zl + 2, H, W))
+    tmp[1:zl + 1] = v_loc
+    exchange(tmp, v_loc[0], v_loc[-1])
+    vt = tmp[zl + 1]
+    P = np.zeros((zl + 2, 3, H, W))
+    Q = P.copy()
+    t, beta_r = 1.0, 0.0
+    for k in range(inner):
+        R = P + beta_r * (P - Q)
+        U = np.zeros((zl + 1, H, W))
+        for z in range(zl + 1):
+            if z0 + z >= Zg:
+                continue
+            vz = v_loc[z] if z < zl else vt
+            U[z] = vz - lam * dt(R, z)
+            if nonneg:
+                U[z] = np.maximum(U[z], 0.0)
+        Pn = np.zeros_like(P)
+        eta = 1.0 / (12.0 * lam)
+        for z in range(zl):
+            u = U[z]
+            gv = np.zeros((H, W)); gv[:-1] = u[1:] - u[:-1]
+            gh = np.zeros((H, W)); gh[:, :-1] = u[:, 1:] - u[:, :-1]
+            gz = (U[z + 1] - u) if z0 + z < Zg - 1 else np.zeros((H, W))
+            ph = R[z + 1, 0] + eta * gv
+            qh = R[z + 1, 1] + eta * gh
+            wh = R[z + 1, 2] + eta * gz
+            nrm = np.maximum(1.0, np.sqrt(ph * ph + qh * qh + wh * wh))
+            Pn[z + 1] = np.stack([ph / nrm, qh / nrm, wh / nrm])
+        exchange(Pn, Pn[1], Pn[zl])
+        tn = (1.0 + np.sqrt(1.0 + 4.0 * t * t)) / 2.0
+        beta_r = (t - 1.0) / tn
+        t = tn
+        Q, P = P, Pn
+    x = np.stack([v_loc[z] - lam * dt(P, z) for z in range(zl)])
+    return np.maximum(x, 0.0) if nonneg else x
+
+
+def _zworker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch
+        import oracle as O
+        from paper_2602_09527_b200 import Projector, TomoProblem
+        from paper_2602_09527_b200.distributed import gather_zslabs, zslab_bounds, zslab_problem
+        out = {}
+        Z, H, W = 7, 9, 11
+        z0, z1 = zslab_bounds(Z, rank, world)
+        # (1) slab bounds tile the volume in rank order
+        spans = [zslab_bounds(Z, g, world) for g in range(world)]
+        out["tiles"] = spans[0][0] == 0 and spans[-1][1] == Z and all(
+            spans[g][1] == spans[g + 1][0] for g in range(world - 1))
+        # (2) the slab problem: own sinogram rows, own projector depth
+        g = ParallelGeometry.uniform(12, 15)
+        data = np.arange(12 * Z * 15, dtype=np.float64).reshape(12, Z, 15)
+        sp = zslab_problem(TomoProblem(Projector(g, W, H, n_slices=Z), data), z0, z1)
+        want = data[:, z0:z1, :]
+        if z1 - z0 == 1:
+            want = want.reshape(12, 15)
+        out["slab_ok"] = (sp.projector.n_slices == z1 - z0 and np.array_equal(sp.data, want))
+        # (3) gathered volume
+        vol = torch.arange(Z * H * W, dtype=torch.float32).reshape(Z, H, W)
+        full = gather_zslabs(vol[z0:z1].clone(), Z)
+        out["gather_ok"] = bool(torch.equal(full, vol))
+        # (4) the halo protocol of the slab FGP = the single-volume 3D FGP
+        rng = np.random.default_rng(2)
+        v = rng.standard_normal((Z, H, W))
+        for nn in (False, True):
+            xs = _slab_fgp(v[z0:z1], z0, Z, 0.3, 12, nn, rank, world)
+            xt = gather_zslabs(torch.from_numpy(xs), Z).numpy()
+            xo, _ = O.tv_prox(v, 1.0, 0.3, 12, nn)
+            out[f"fgp_err_{int(nn)}"] = float(np.abs(xt - xo).max())
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_zslab_logic_and_halo_protocol_over_gloo(world):
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_zworker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        res = results[r]
+        assert res["tiles"] and res["slab_ok"] and res["gather_ok"], res
+        assert res["fgp_err_0"] <= 1e-12 and res["fgp_err_1"] <= 1e-12, res

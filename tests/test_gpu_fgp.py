@@ -62,6 +62,18 @@ def test_fgp_3d_matches_oracle(oracle):
         assert st.w is not None
 
 
+@pytest.mark.parametrize("shape,inner", [((37, 45, 70), 11), ((2, 8, 33), 4), ((64, 64, 64), 30)])
+def test_fgp_3d_ragged_and_chunked(oracle, shape, inner):
+    """The z-marching 3D kernel across tile edges, z-run boundaries and ragged extents."""
+    rng = np.random.default_rng(sum(shape))
+    v = rng.standard_normal(shape).cumsum(axis=0) * 0.1 + 0.2
+    xo, sto = oracle.tv_prox(v, 1.0, 0.25, inner, True)
+    x, st = tv_prox(v, 1.0, TvProxConfig(alpha=0.25, inner_iterations=inner))
+    assert rel_l2(cpu(x), xo) <= 1e-5
+    assert rel_l2(cpu(st.w), sto.w) <= 1e-4
+    assert rel_l2(xo, v) > 1e-3
+
+
 def test_fgp_properties():
     rng = np.random.default_rng(5)
     u = rng.standard_normal((40, 40))
