@@ -233,12 +233,13 @@ def build_gpu_problem(cfg, torch):
 
 def algorithmic_bytes(cfg, proj, state):
     """SURVEY.md 8d per-launch algorithmic bytes of each launch category."""
-    n_px = cfg.n_pixels
+    depth = getattr(proj, "n_slices", 1)  # this rank's planes (z-slab) or the volume
+    n_px = cfg.size * cfg.size * depth
     plan = proj.plan
     part = state.partition
     sub0 = part.subsets[0] if part else None
     nnz = plan.nnz(sub0) if sub0 else plan.nnz(None)
-    rays = (len(sub0) if sub0 else cfg.n_angles) * cfg.n_bins * cfg.depth
+    rays = (len(sub0) if sub0 else cfg.n_angles) * cfg.n_bins * depth
     e = 4 if cfg.estimator in ("svrg", "lsvrg") else (7 if cfg.estimator == "saga" else 3)
     return {
         "fwd_band": 4 * nnz + 4 * rays,
@@ -277,9 +278,14 @@ def gpu_arm(args, cfg, rank, world, local):
     scfg = SolverConfig(gamma=gamma, skip_probability=cfg.p, n_subsets=cfg.n_subsets,
                         estimator=cfg.estimator, max_data_passes=1e18, seed=cfg.solver_seed)
     stream = torch.cuda.Stream()
+    # multi-GPU: angle sectors (2D) or z-slabs (slice-stacked 3D)
+    zs, work = None, problem
+    if world > 1 and cfg.depth > 1:
+        z0, z1 = D.zslab_bounds(cfg.depth, rank, world)
+        zs, work = (z0, z1, cfg.depth), D.zslab_problem(problem, z0, z1)
     with torch.cuda.stream(stream):
-        state = _init_state(scfg, problem, None, stream)
-    if world > 1:
+        state = _init_state(scfg, work, None, stream, zslab=zs)
+    if world > 1 and zs is None:
         D.attach(state.session)
         # re-initialise the snapshot with the sharded full gradient
         state.session.init()
@@ -330,7 +336,7 @@ def gpu_arm(args, cfg, rank, world, local):
     value = args.steps / (ms / 1e3)
 
     # replica check across ranks
-    replicas_ok = D.replicas_identical(sess.x) if world > 1 else True
+    replicas_ok = D.replicas_identical(sess.x) if (world > 1 and zs is None) else None
 
     # live per-kernel timing: a second timed pass with CUDA events per launch
     roofline = None
@@ -347,7 +353,7 @@ def gpu_arm(args, cfg, rank, world, local):
         kernel_times = {name: {"ms": round(msa[i], 3), "calls": int(cnt[i]),
                                "share": round(msa[i] / tot, 4) if tot else None}
                         for i, name in enumerate(N.PROF_NAMES)}
-        alg, nnz = algorithmic_bytes(cfg, proj, state)
+        alg, nnz = algorithmic_bytes(cfg, work.projector, state)  # per rank
         cands = [k for k in ("gather_step", "fwd_band", "fgp_call") if alg[k] and cnt[N.PROF_NAMES.index(k)]]
         top = max(cands, key=lambda k: msa[N.PROF_NAMES.index(k)])
         i = N.PROF_NAMES.index(top)
@@ -414,7 +420,8 @@ def gpu_arm(args, cfg, rank, world, local):
             "config": {"workload": workload_name(cfg), "step": "1 epoch = snapshot + N iterations",
                        "epochs_timed": args.steps, "iterations_timed": n_iter,
                        "prox_calls_timed": n_prox,
-                       "parallelism": f"angle-sector dp{world}" if world > 1 else "1 GPU",
+                       "parallelism": ("1 GPU" if world == 1 else
+                                       f"z-slab dp{world}" if zs else f"angle-sector dp{world}"),
                        "l2": "working set > L2 (band partials + state > 126 MB); no flush",
                        "L": lip, "gamma": gamma, "alpha": alpha},
             "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
