@@ -74,6 +74,20 @@ def test_fgp_3d_ragged_and_chunked(oracle, shape, inner):
     assert rel_l2(xo, v) > 1e-3
 
 
+def test_fgp_3d_config3_scale(oracle):
+    """128^3 (half of config 3 per axis), 30 iterations, against the oracle;
+    and the dual feasibility / nonnegativity properties at 256 x 256 x 32."""
+    rng = np.random.default_rng(7)
+    v = rng.standard_normal((128, 128, 128)).cumsum(axis=2) * 0.05
+    xo, _ = oracle.tv_prox(v, 1.0, 0.1, 30, True)
+    x, st = tv_prox(v, 1.0, TvProxConfig(alpha=0.1, inner_iterations=30))
+    assert rel_l2(cpu(x), xo) <= 1e-5
+    big = torch.randn((32, 256, 256), device="cuda")
+    xb, sb = tv_prox(big, 1.0, TvProxConfig(alpha=0.2, inner_iterations=40))
+    assert float(xb.min()) >= 0.0
+    assert float((sb.p ** 2 + sb.q ** 2 + sb.w ** 2).max()) <= 1.0 + 1e-5
+
+
 def test_fgp_properties():
     rng = np.random.default_rng(5)
     u = rng.standard_normal((40, 40))
