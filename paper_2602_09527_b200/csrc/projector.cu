@@ -281,6 +281,7 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
     __shared__ int s_pref[CH + 1];
     __shared__ int2 s_bk[CH];       // {first owned ray, selection slot}
     __shared__ float4 s_ray[CH];    // {tile-local lane of ray blo at st 0, sigma, m, 1/m}
+    __shared__ float* s_out[CH];    // partial of ray blo in this band
 
     const int tid = threadIdx.x;
     const FwdItem it = decode_item(P, blockIdx.x);
@@ -303,6 +304,11 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
     const int32_t* bpos = branch ? P.bpos1 : P.bpos0;
     const bool first_tile = (l0 == 0);
     const bool last_tile = (l0 + TX >= n_lanes);
+    // owned rays drift at most TY/2 lanes (|m| <= 1) from their band-middle
+    // position in [l0, l0 + TX): away from the image edges no ray leaves the
+    // image inside the band, so the per-ray step clipping is skipped
+    const bool interior = !first_tile && !last_tile && l0 >= TY / 2 + 2 &&
+                          l0 + TX + TY / 2 + 2 <= n_lanes;
     const double smid = s0 + 0.5 * (ty_valid - 1);
     bool waited = false;
 
@@ -328,6 +334,9 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
                 bhi = min(bhi, (long long)P.B);
                 cnt = (int)max(0LL, bhi - blo);
                 s_bk[tid] = make_int2((int)blo, k);
+                s_out[tid] = P.partial +
+                             ((((size_t)it.band * P.n_k + (size_t)(k - P.k_begin)) * P.Z + it.z) *
+                                  P.B + (size_t)blo);
                 // tile-local lane position of ray blo at step 0 (float64 -> float32;
                 // per ray only (b - blo) * sigma, |.| <~ TX, is added in float32)
                 s_ray[tid] = make_float4(
@@ -353,9 +362,7 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
         for (int w = tid; w < total; w += NT) {
             while (w >= s_pref[j + 1]) ++j;
             const int db = w - s_pref[j];
-            const int2 bk = s_bk[j];
             const float4 ry = s_ray[j];
-            const int b = bk.x + db;
             const float mf = ry.z;
             const float pl = fmaf((float)db, ry.y, ry.x);  // tile-local lane at st = 0
             // steps where pos in [-1.5, n_lanes + 0.5] (global lanes): outside,
@@ -363,7 +370,8 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
             const float P0 = pl + (float)lane_org;
             int st_a = 0, st_b = ty_valid;
             const float im = ry.w;
-            if (im == 0.f) {
+            if (interior) {
+            } else if (im == 0.f) {
                 if (P0 < -1.5f || P0 > n_lanes + 0.5f) st_b = 0;
             } else {
                 const float e1 = (-1.5f - P0) * im, e2 = ((float)n_lanes + 0.5f - P0) * im;
@@ -374,8 +382,7 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
             const float acc = branch == 0
                 ? ray_band_sum<4, T::PITCH_R * 4>(tile_u32, st_a, st_b, pl, mf)
                 : ray_band_sum<T::PITCH_C * 4, 4>(tile_u32, st_a, st_b, pl, mf);
-            const size_t kk = (size_t)(bk.y - P.k_begin);
-            P.partial[(((size_t)it.band * P.n_k + kk) * P.Z + it.z) * P.B + b] = acc;
+            s_out[j][db] = acc;
         }
         if (cbeg + CH < a_end) __syncthreads();  // chunk tables are rewritten next
     }
