@@ -78,10 +78,6 @@ __device__ __forceinline__ uint32_t opaque(uint32_t v)
     X(5, 16, 256, 256, 4)        \
     X(6, 32, 256, 128, 8)        \
     X(7, 32, 128, 128, 8)        \
-    X(8, 128, 128, 512, 1)       \
-    X(9, 128, 256, 512, 1)       \
-    X(10, 64, 512, 512, 1)       \
-    X(11, 64, 256, 1024, 1)      \
     X(100, 32, 128, 256, 4)      \
     X(101, 16, 64, 128, 8)
 
