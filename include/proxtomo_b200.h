@@ -235,6 +235,17 @@ int pt_session_profile(pt_session* s, double* host_ms, int64_t* host_calls);
  * the session stream before the epilogue (world == 1 runs that path on a
  * one-rank communicator). */
 int pt_nccl_unique_id(const char* nccl_path, uint8_t* host_out128);
+/* A process-level communicator shared by several sessions (one
+ * ncclCommInitRank per process group instead of one per solve); destroy it
+ * after the last session that uses it. */
+typedef struct pt_comm pt_comm;
+int pt_nccl_comm_create(const char* nccl_path, const uint8_t* host_id128, int32_t rank,
+                        int32_t world, pt_comm** out);
+int pt_nccl_comm_destroy(pt_comm* comm);
+/* attach a session to a shared communicator: angle sectors / z-slabs */
+int pt_session_attach_comm(pt_session* s, pt_comm* comm);
+int pt_session_attach_comm_zslab(pt_session* s, pt_comm* comm, int32_t z_offset,
+                                 int32_t z_total);
 int pt_session_attach_nccl(pt_session* s, const char* nccl_path, const uint8_t* host_id128,
                            int32_t rank, int32_t world);
 /* Test hook: run the angle-sector decomposition of `world` ranks on this one

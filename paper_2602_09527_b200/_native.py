@@ -92,6 +92,11 @@ _SIGS = {
                                                     ctypes.POINTER(ctypes.c_uint8), c_i32, c_i32,
                                                     c_i32, c_i32]),
     "pt_session_emulate_zslabs": (ctypes.c_int, [c_vp, c_i32]),
+    "pt_nccl_comm_create": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint8), c_i32,
+                                           c_i32, ctypes.POINTER(c_vp)]),
+    "pt_nccl_comm_destroy": (ctypes.c_int, [c_vp]),
+    "pt_session_attach_comm": (ctypes.c_int, [c_vp, c_vp]),
+    "pt_session_attach_comm_zslab": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

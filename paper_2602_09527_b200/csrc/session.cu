@@ -76,6 +76,14 @@ int nccl_load(const char* path, NcclApi* api)
 
 }  // namespace
 
+// A process-level NCCL communicator that several sessions can share (one
+// ncclCommInitRank per process group instead of one per solve).
+struct pt_comm {
+    NcclApi api;
+    nccl_comm comm = nullptr;
+    int rank = 0, world = 1;
+};
+
 namespace pt {
 
 cudaEvent_t Profiler::ev()
@@ -154,6 +162,7 @@ struct pt_session {
     // NCCL
     NcclApi nccl;
     nccl_comm comm = nullptr;
+    bool owns_comm = false;  // created by pt_session_attach_nccl*(), destroyed with the session
     int rank = 0, world = 1;
     // z-slab mode (3D): this rank owns global planes [z0, z0 + Z)
     // of Zg; projector and snapshot are slab-local, the FGP exchanges halos
@@ -424,7 +433,7 @@ int pt_session_destroy(pt_session* s)
     if (s->slab) cudaFree(s->slab);
     if (s->bad) cudaFree(s->bad);
     pt::workspace_free(&s->ws);
-    if (s->comm && s->nccl.destroy) s->nccl.destroy(s->comm);
+    if (s->comm && s->owns_comm && s->nccl.destroy) s->nccl.destroy(s->comm);
     if (s->fgp3_work) cudaFree(s->fgp3_work);
     if (s->dw_slab) cudaFree(s->dw_slab);
     if (s->emu_z_work) cudaFree(s->emu_z_work);
@@ -660,19 +669,56 @@ int pt_session_emulate_zslabs(pt_session* s, int32_t slabs)
     return PT_OK;
 }
 
-int pt_session_attach_nccl_zslab(pt_session* s, const char* nccl_path, const uint8_t* host_id128,
-                                 int32_t rank, int32_t world, int32_t z_offset, int32_t z_total)
+int pt_nccl_comm_create(const char* nccl_path, const uint8_t* host_id128, int32_t rank,
+                        int32_t world, pt_comm** out)
 {
-    if (!s || !host_id128 || world < 1 || rank < 0 || rank >= world) { pt::set_error("bad argument"); return PT_EINVAL; }
-    if (s->comm) { pt::set_error("session already attached"); return PT_EINVAL; }
+    if (!host_id128 || !out || world < 1 || rank < 0 || rank >= world) { pt::set_error("bad argument"); return PT_EINVAL; }
+    pt_comm* c = new pt_comm();
+    int rc = nccl_load(nccl_path, &c->api);
+    if (rc) { delete c; return rc; }
+    nccl_uid id;
+    memcpy(id.internal, host_id128, 128);
+    int e = c->api.init_rank(&c->comm, world, id, rank);
+    if (e != 0) {
+        pt::set_error("ncclCommInitRank failed (%d)", e);
+        delete c;
+        return PT_ENCCL;
+    }
+    c->rank = rank;
+    c->world = world;
+    *out = c;
+    return PT_OK;
+}
+
+int pt_nccl_comm_destroy(pt_comm* c)
+{
+    if (!c) return PT_OK;
+    cudaDeviceSynchronize();
+    if (c->comm && c->api.destroy) c->api.destroy(c->comm);
+    delete c;
+    return PT_OK;
+}
+
+namespace {
+
+int attach_sector(pt_session* s, const NcclApi& api, nccl_comm comm, int rank, int world)
+{
+    s->nccl = api;
+    s->comm = comm;
+    s->rank = rank;
+    s->world = world;
+    return build_selections(s);
+}
+
+int attach_zslab(pt_session* s, const NcclApi& api, nccl_comm comm, int rank, int world,
+                 int32_t z_offset, int32_t z_total)
+{
     pt_plan* P = s->plan;
     if (z_offset < 0 || z_total < 2 || z_offset + P->Z > z_total) {
         pt::set_error("slab [%d, %d) outside a volume of %d planes", z_offset, z_offset + P->Z, z_total);
         return PT_EINVAL;
     }
-    int rc = nccl_load(nccl_path, &s->nccl);
-    if (rc) return rc;
-    if (!s->nccl.send || !s->nccl.recv || !s->nccl.group_start || !s->nccl.group_end) {
+    if (!api.send || !api.recv || !api.group_start || !api.group_end) {
         pt::set_error("libnccl lacks ncclSend/ncclRecv");
         return PT_ENCCL;
     }
@@ -681,10 +727,8 @@ int pt_session_attach_nccl_zslab(pt_session* s, const char* nccl_path, const uin
                                  (size_t)pt::fgp3d_slab_floats(P->Z, P->H, P->W) * sizeof(float)));
         if (!s->dw) PT_CHECK_CUDA(cudaMalloc(&s->dw_slab, s->n * sizeof(float)));
     }
-    nccl_uid id;
-    memcpy(id.internal, host_id128, 128);
-    int e = s->nccl.init_rank(&s->comm, world, id, rank);
-    if (e != 0) { pt::set_error("ncclCommInitRank failed (%d)", e); return PT_ENCCL; }
+    s->nccl = api;
+    s->comm = comm;
     s->rank = rank;
     s->world = world;
     s->zslab = true;
@@ -697,6 +741,42 @@ int pt_session_attach_nccl_zslab(pt_session* s, const char* nccl_path, const uin
     return build_selections(s);
 }
 
+}  // namespace
+
+int pt_session_attach_comm(pt_session* s, pt_comm* c)
+{
+    if (!s || !c) { pt::set_error("null argument"); return PT_EINVAL; }
+    if (s->comm) { pt::set_error("session already attached"); return PT_EINVAL; }
+    return attach_sector(s, c->api, c->comm, c->rank, c->world);
+}
+
+int pt_session_attach_comm_zslab(pt_session* s, pt_comm* c, int32_t z_offset, int32_t z_total)
+{
+    if (!s || !c) { pt::set_error("null argument"); return PT_EINVAL; }
+    if (s->comm) { pt::set_error("session already attached"); return PT_EINVAL; }
+    return attach_zslab(s, c->api, c->comm, c->rank, c->world, z_offset, z_total);
+}
+
+int pt_session_attach_nccl_zslab(pt_session* s, const char* nccl_path, const uint8_t* host_id128,
+                                 int32_t rank, int32_t world, int32_t z_offset, int32_t z_total)
+{
+    if (!s || !host_id128 || world < 1 || rank < 0 || rank >= world) { pt::set_error("bad argument"); return PT_EINVAL; }
+    if (s->comm) { pt::set_error("session already attached"); return PT_EINVAL; }
+    pt_comm* c = nullptr;
+    int rc = pt_nccl_comm_create(nccl_path, host_id128, rank, world, &c);
+    if (rc) return rc;
+    rc = attach_zslab(s, c->api, c->comm, rank, world, z_offset, z_total);
+    if (rc) {
+        pt_nccl_comm_destroy(c);
+        s->comm = nullptr;
+        s->zslab = false;
+        return rc;
+    }
+    s->owns_comm = true;
+    delete c;  // the session owns the communicator now
+    return PT_OK;
+}
+
 int pt_session_attach_nccl(pt_session* s, const char* nccl_path, const uint8_t* host_id128,
                            int32_t rank, int32_t world)
 {
@@ -704,15 +784,18 @@ int pt_session_attach_nccl(pt_session* s, const char* nccl_path, const uint8_t* 
     if (s->comm) { pt::set_error("session already attached"); return PT_EINVAL; }
     // world == 1 is accepted: a one-rank communicator exercises the whole
     // sharded data path (partial gradient -> ncclAllReduce -> epilogue)
-    int rc = nccl_load(nccl_path, &s->nccl);
+    pt_comm* c = nullptr;
+    int rc = pt_nccl_comm_create(nccl_path, host_id128, rank, world, &c);
     if (rc) return rc;
-    nccl_uid id;
-    memcpy(id.internal, host_id128, 128);
-    int e = s->nccl.init_rank(&s->comm, world, id, rank);
-    if (e != 0) { pt::set_error("ncclCommInitRank failed (%d)", e); return PT_ENCCL; }
-    s->rank = rank;
-    s->world = world;
-    return build_selections(s);
+    rc = attach_sector(s, c->api, c->comm, rank, world);
+    if (rc) {
+        pt_nccl_comm_destroy(c);
+        s->comm = nullptr;
+        return rc;
+    }
+    s->owns_comm = true;
+    delete c;  // the session owns the communicator now
+    return PT_OK;
 }
 
 }  // extern "C"

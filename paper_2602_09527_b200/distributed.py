@@ -37,23 +37,47 @@ def nccl_library_path() -> str:
     return "libnccl.so.2"
 
 
-def attach(session, rank: int | None = None, world: int | None = None,
-           group=None) -> None:
-    """Attach a native solver session to an NCCL communicator over the
-    torch.distributed process group (the ranks of one node, one GPU each)."""
+_COMMS: dict = {}  # (process group, rank, world) -> pt_comm handle
+
+
+def communicator(rank: int | None = None, world: int | None = None, group=None):
+    """The library's NCCL communicator for this process group, created once
+    per process (rank 0 makes the unique id, torch.distributed ships it) and
+    shared by every session; ``release_communicators`` frees them."""
     rank = dist.get_rank(group) if rank is None else rank
     world = dist.get_world_size(group) if world is None else world
-    path = nccl_library_path().encode()
+    key = (id(group) if group is not None else 0, rank, world)
+    handle = _COMMS.get(key)
+    if handle is None:
+        path = nccl_library_path().encode()
 
-    def make_uid() -> bytes:
-        uid = (ctypes.c_uint8 * 128)()
-        N.check(N.lib().pt_nccl_unique_id(path, uid), "ncclGetUniqueId")
-        return bytes(uid)
+        def make_uid() -> bytes:
+            uid = (ctypes.c_uint8 * 128)()
+            N.check(N.lib().pt_nccl_unique_id(path, uid), "ncclGetUniqueId")
+            return bytes(uid)
 
-    payload = share_unique_id(make_uid, rank, group)
-    uid = (ctypes.c_uint8 * 128)(*payload)
-    N.check(N.lib().pt_session_attach_nccl(session.handle, path, uid, rank, world),
-            "attach_nccl")
+        payload = share_unique_id(make_uid, rank, group)
+        uid = (ctypes.c_uint8 * 128)(*payload)
+        handle = ctypes.c_void_p()
+        N.check(N.lib().pt_nccl_comm_create(path, uid, rank, world, ctypes.byref(handle)),
+                "nccl_comm_create")
+        _COMMS[key] = handle
+    return handle
+
+
+def release_communicators() -> None:
+    """Destroy the cached communicators (after the last session using them)."""
+    while _COMMS:
+        _, handle = _COMMS.popitem()
+        N.lib().pt_nccl_comm_destroy(handle)
+
+
+def attach(session, rank: int | None = None, world: int | None = None,
+           group=None) -> None:
+    """Attach a native solver session to the process group's NCCL
+    communicator (angle sectors: rank g owns angles [gA/G, (g+1)A/G))."""
+    N.check(N.lib().pt_session_attach_comm(session.handle, communicator(rank, world, group)),
+            "attach")
 
 
 def share_unique_id(make_uid, rank: int, group=None) -> bytes:
@@ -74,7 +98,7 @@ def emulate_sectors(session, world: int) -> None:
 def replicas_identical(x: torch.Tensor, group=None) -> bool:
     """Replica check: every rank's iterate has the same bytes (max == min of a
     bit-pattern checksum over ranks)."""
-    v = x.contiguous().view(torch.int32).to(torch.int64)
+    v = x.contiguous().view(torch.int32).reshape(-1).to(torch.int64)
     chk = torch.stack([v.sum(), (v * torch.arange(v.numel(), device=v.device) % 1000003).sum()])
     lo, hi = chk.clone(), chk.clone()
     dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
@@ -117,20 +141,11 @@ def zslab_problem(problem, z0: int, z1: int):
 
 def attach_zslab(session, z0: int, z_total: int, rank: int | None = None,
                  world: int | None = None, group=None) -> None:
-    """Attach a slab session to an NCCL communicator for the z halo exchange."""
-    rank = dist.get_rank(group) if rank is None else rank
-    world = dist.get_world_size(group) if world is None else world
-    path = nccl_library_path().encode()
-
-    def make_uid() -> bytes:
-        uid = (ctypes.c_uint8 * 128)()
-        N.check(N.lib().pt_nccl_unique_id(path, uid), "ncclGetUniqueId")
-        return bytes(uid)
-
-    payload = share_unique_id(make_uid, rank, group)
-    uid = (ctypes.c_uint8 * 128)(*payload)
-    N.check(N.lib().pt_session_attach_nccl_zslab(session.handle, path, uid, rank, world,
-                                                 int(z0), int(z_total)), "attach_zslab")
+    """Attach a slab session to the process group's communicator for the z
+    halo exchange (ranks hold consecutive slabs in rank order)."""
+    N.check(N.lib().pt_session_attach_comm_zslab(session.handle,
+                                                 communicator(rank, world, group), int(z0),
+                                                 int(z_total)), "attach_zslab")
 
 
 def emulate_zslabs(session, slabs: int) -> None:
