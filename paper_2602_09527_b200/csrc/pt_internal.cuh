@@ -179,5 +179,4 @@ int launch_identity_prox(const float* v, const float* xhat, float* x_out, float*
 int launch_scale_by_rsqrt(float* v, const float* u, const double* sumsq, int64_t n,
                           cudaStream_t st);
 int launch_fill_i64(int64_t* p, int64_t value, cudaStream_t st);
-int launch_sub(const float* a, const float* b, float* out, int64_t n, cudaStream_t st);
 }  // namespace pt

@@ -185,19 +185,4 @@ int launch_fill_i64(int64_t* p, int64_t value, cudaStream_t st)
     return PT_OK;
 }
 
-__global__ void sub_kernel(const float* a, const float* b, float* out, int64_t n)
-{
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = a[i] - b[i];
-}
-
-int launch_sub(const float* a, const float* b, float* out, int64_t n, cudaStream_t st)
-{
-    const int g = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
-    sub_kernel<<<g, 256, 0, st>>>(a, b, out, n);
-    PT_CHECK_LAUNCH();
-    return PT_OK;
-}
-
 }  // namespace pt

@@ -178,12 +178,6 @@ struct pt_session {
 
 namespace {
 
-int alloc_f(float** p, size_t n)
-{
-    PT_CHECK_CUDA(cudaMalloc(p, std::max<size_t>(1, n) * sizeof(float)));
-    return PT_OK;
-}
-
 // Selections of angles [lo, hi): subset k = {k, k+N, ...} (geometry.py:75-82)
 // restricted to the sector; cached in the plan (a session or a rank reuses them).
 int sector_selections(pt_plan* P, int n_subsets, int lo, int hi, pt_selection** all_out,
