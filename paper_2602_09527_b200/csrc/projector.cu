@@ -872,7 +872,7 @@ __global__ void epilogue_kernel(const float* g, size_t n, pt_step_epilogue ep)
 {
     for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
          p += (size_t)gridDim.x * blockDim.x)
-        step_epilogue(ep, p, g[p]);
+        step_epilogue(ep, p, g ? g[p] : 0.f);  // g == null: a zero gradient difference
 }
 
 static constexpr int kTR = 32, kTC = 64, kNT = 256, kNA = 32;

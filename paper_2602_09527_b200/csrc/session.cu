@@ -457,7 +457,8 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
     for (int j = 0; j < n_steps; ++j) {
         const int64_t k = k0 + j;
         int rc = PT_OK;
-        if (vr && host_refresh && host_refresh[j]) {
+        const bool refreshed = vr && host_refresh && host_refresh[j];
+        if (refreshed) {
             // refresh_svrg_state (estimators.py:126-130)
             {
                 pt::ProfScope ps(&s->ws, PT_PROF_OTHER, st);
@@ -480,9 +481,13 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
         float* xn = s->x[1 - s->cur];
         const int theta = (p >= 1.0) ? 1 : (host_theta ? host_theta[j] : 0);
 
+        // Right after a refresh x == x_snap bitwise, so the reference's
+        // N (g_i(x) - g_i(x_snap)) is exactly 0 (two identical float64
+        // evaluations) and the estimate is the snapshot gradient itself: no
+        // subset projection, the epilogue runs on a zero difference.
         // forward: residual rows of the (own part of the) selection
-        if (s->emu > 1)
-            ;  // per virtual sector below
+        if (refreshed || s->emu > 1)
+            ;  // none / per virtual sector below
         else if (vr)  // A_i (x - x_snap) = (A_i x - b_i) - (A_i x_snap - b_i)
             rc = pt::launch_forward(P, &s->ws, sel, xc, nullptr, s->data, s->r, nullptr, st,
                                     rsnap_by_angle(s));
@@ -510,7 +515,10 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
         ep.v_out = s->v;
         ep.xhat_out = s->xhat;
         ep.bad_iter = s->bad;
-        if (s->emu > 1) {
+        if (refreshed) {
+            pt::ProfScope ps(&s->ws, PT_PROF_OTHER, st);
+            rc = pt::launch_epilogue(P, nullptr, &ep, st);
+        } else if (s->emu > 1) {
             // virtual ranks: partial A_i^T r per sector, summed in g, then the epilogue
             for (int g = 0; g < s->emu && !rc; ++g) {
                 const pt_selection* sg = (d.estimator == PT_EST_FULL) ? s->emu_all[g]
