@@ -197,6 +197,15 @@ typedef struct {
  * session.  x0 may be NULL (zeros, solvers.py:161). */
 int pt_session_create(pt_plan* plan, const pt_solver_desc* desc, const float* data,
                       const float* x0, pt_session** out, void* stream);
+/* The same with caller-provided device memory for every session buffer (state,
+ * divergence flag, projector workspace): `workspace` of at least
+ * pt_session_workspace_bytes() bytes, 256-byte aligned, owned by the caller and
+ * kept alive until pt_session_destroy (e.g. from a caching allocator, so
+ * repeated solves do not cudaMalloc). */
+int64_t pt_session_workspace_bytes(pt_plan* plan, const pt_solver_desc* desc);
+int pt_session_create_in(pt_plan* plan, const pt_solver_desc* desc, const float* data,
+                         const float* x0, void* workspace, int64_t workspace_bytes,
+                         pt_session** out, void* stream);
 int pt_session_destroy(pt_session* s);
 /* SVRG/LSVRG initial snapshot + full gradient (estimators.py:117-123). */
 int pt_session_init(pt_session* s, void* stream);

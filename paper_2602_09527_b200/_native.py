@@ -69,6 +69,9 @@ _SIGS = {
     "pt_operator_norm_sq": (ctypes.c_int, [c_vp, c_vp, c_i32, ctypes.POINTER(c_f64), c_vp]),
     "pt_session_create": (ctypes.c_int, [c_vp, ctypes.POINTER(SolverDesc), c_vp, c_vp,
                                          ctypes.POINTER(c_vp), c_vp]),
+    "pt_session_workspace_bytes": (c_i64, [c_vp, ctypes.POINTER(SolverDesc)]),
+    "pt_session_create_in": (ctypes.c_int, [c_vp, ctypes.POINTER(SolverDesc), c_vp, c_vp, c_vp,
+                                            c_i64, ctypes.POINTER(c_vp), c_vp]),
     "pt_session_destroy": (ctypes.c_int, [c_vp]),
     "pt_session_init": (ctypes.c_int, [c_vp, c_vp]),
     "pt_session_run": (ctypes.c_int, [c_vp, c_i32, ctypes.POINTER(c_i32),

@@ -26,13 +26,19 @@ void set_error(const char* fmt, ...)
     va_end(ap);
 }
 
+void workspace_sizes(const pt_plan* plan, size_t* partial_floats, size_t* red_doubles,
+                     size_t* image_floats)
+{
+    *partial_floats =
+        (size_t)plan->n_bands * plan->Z * plan->B * (size_t)plan->max_angles_per_launch;
+    const size_t chunks = (plan->A + plan->max_angles_per_launch - 1) / plan->max_angles_per_launch;
+    *red_doubles = ((size_t)plan->A * plan->Z * plan->B + 255) / 256 + chunks + 16;
+    *image_floats = (size_t)plan->Z * plan->H * plan->W;
+}
+
 int workspace_alloc(const pt_plan* plan, Workspace* ws)
 {
-    ws->partial_floats =
-        (size_t)plan->n_bands * plan->Z * plan->B * (size_t)plan->max_angles_per_launch;
-    size_t chunks = (plan->A + plan->max_angles_per_launch - 1) / plan->max_angles_per_launch;
-    ws->red_doubles = ((size_t)plan->A * plan->Z * plan->B + 255) / 256 + chunks + 16;
-    ws->image_floats = (size_t)plan->Z * plan->H * plan->W;
+    workspace_sizes(plan, &ws->partial_floats, &ws->red_doubles, &ws->image_floats);
     PT_CHECK_CUDA(cudaMalloc(&ws->partial, ws->partial_floats * sizeof(float)));
     PT_CHECK_CUDA(cudaMalloc(&ws->red, ws->red_doubles * sizeof(double)));
     PT_CHECK_CUDA(cudaMalloc(&ws->image, ws->image_floats * sizeof(float)));

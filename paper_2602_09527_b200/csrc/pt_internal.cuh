@@ -102,6 +102,8 @@ struct ProfScope {
     }
     ~ProfScope() { if (p) p->end(st); }
 };
+void workspace_sizes(const pt_plan* plan, size_t* partial_floats, size_t* red_doubles,
+                     size_t* image_floats);
 int workspace_alloc(const pt_plan* plan, Workspace* ws);
 void workspace_free(Workspace* ws);
 }  // namespace pt

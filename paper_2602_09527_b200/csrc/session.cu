@@ -147,7 +147,8 @@ struct pt_session {
     float* r = nullptr;      // residual rows (largest selection)
     float* rsnap = nullptr;  // SVRG: A x_snap - b over the owned angles (snapshot residual)
     float* g = nullptr;  // partial gradient (multi-GPU)
-    float* slab = nullptr;  // backing allocation of the buffers above
+    float* slab = nullptr;  // backing allocation of the buffers above (+ flag, workspace)
+    bool owns_slab = true;  // false: caller-provided memory (pt_session_create_in)
     int64_t* bad = nullptr;
     pt::Workspace ws;
     pt::Profiler prof;
@@ -343,10 +344,10 @@ int slab_tv_prox(pt_session* s, double lam, float pog, float* xn, int64_t k, cud
 
 extern "C" {
 
-int pt_session_create(pt_plan* plan, const pt_solver_desc* desc, const float* data,
-                      const float* x0, pt_session** out, void* stream)
+namespace {
+
+int check_desc(const pt_plan* plan, const pt_solver_desc* desc)
 {
-    if (!plan || !desc || !data || !out) { pt::set_error("null argument"); return PT_EINVAL; }
     if (!(desc->gamma > 0.0)) { pt::set_error("gamma must be positive"); return PT_EINVAL; }
     if (!(desc->skip_probability > 0.0 && desc->skip_probability <= 1.0)) {
         pt::set_error("skip_probability must be in (0, 1]");
@@ -361,6 +362,82 @@ int pt_session_create(pt_plan* plan, const pt_solver_desc* desc, const float* da
         pt::set_error("bad TV configuration");
         return PT_EINVAL;
     }
+    return PT_OK;
+}
+
+// Carve every session buffer out of one allocation (256-byte aligned
+// pieces): the state, the divergence flag and the projector workspace.
+// base == nullptr: only count.  Returns the bytes needed.
+size_t session_layout(const pt_plan* plan, const pt_solver_desc* desc, pt_session* s, char* base)
+{
+    const size_t n = (size_t)plan->Z * plan->H * plan->W;
+    const size_t sino = (size_t)plan->A * plan->Z * plan->B;
+    size_t off = 0;
+    auto take = [&](size_t bytes) -> char* {
+        char* p = base ? base + off : nullptr;
+        off += (std::max<size_t>(bytes, 1) + 255) & ~size_t(255);
+        return p;
+    };
+    auto F = [&](float** dst, size_t cnt) {
+        char* p = take(cnt * sizeof(float));
+        if (dst) *dst = (float*)p;
+    };
+    const bool vr = desc->estimator == PT_EST_SVRG || desc->estimator == PT_EST_LSVRG;
+    F(s ? &s->x[0] : nullptr, n); F(s ? &s->x[1] : nullptr, n);
+    F(s ? &s->h : nullptr, n); F(s ? &s->v : nullptr, n); F(s ? &s->xhat : nullptr, n);
+    if (vr) { F(s ? &s->snap : nullptr, n); F(s ? &s->fg : nullptr, n); F(s ? &s->rsnap : nullptr, sino); }
+    if (desc->estimator == PT_EST_SAGA) {
+        F(s ? &s->saga_table : nullptr, n * desc->n_subsets);
+        F(s ? &s->saga_sum : nullptr, n);
+    }
+    if (desc->prox_kind == 1) {
+        F(s ? &s->dp : nullptr, n); F(s ? &s->dq : nullptr, n);
+        if (plan->Z > 1) F(s ? &s->dw : nullptr, n);
+        F(s ? &s->fgp_work : nullptr, (size_t)pt::fgp_workspace_floats(plan));
+    }
+    F(s ? &s->r : nullptr, sino);
+    F(s ? &s->g : nullptr, n);
+    {
+        char* p = take(sizeof(int64_t));
+        if (s) s->bad = (int64_t*)p;
+    }
+    // projector workspace (band partials, reduction scratch, image temp)
+    size_t pf, rd, imf;
+    pt::workspace_sizes(plan, &pf, &rd, &imf);
+    {
+        char* a = take(pf * sizeof(float));
+        char* b = take(rd * sizeof(double));
+        char* c = take(imf * sizeof(float));
+        if (s) {
+            s->ws.partial = (float*)a; s->ws.partial_floats = pf;
+            s->ws.red = (double*)b; s->ws.red_doubles = rd;
+            s->ws.image = (float*)c; s->ws.image_floats = imf;
+        }
+    }
+    return off;
+}
+
+}  // namespace
+
+int64_t pt_session_workspace_bytes(pt_plan* plan, const pt_solver_desc* desc)
+{
+    if (!plan || !desc) { pt::set_error("null argument"); return -1; }
+    return (int64_t)session_layout(plan, desc, nullptr, nullptr);
+}
+
+int pt_session_create_in(pt_plan* plan, const pt_solver_desc* desc, const float* data,
+                         const float* x0, void* workspace, int64_t workspace_bytes,
+                         pt_session** out, void* stream)
+{
+    if (!plan || !desc || !data || !out) { pt::set_error("null argument"); return PT_EINVAL; }
+    int rc = check_desc(plan, desc);
+    if (rc) return rc;
+    const size_t need = session_layout(plan, desc, nullptr, nullptr);
+    if (workspace && (workspace_bytes < 0 || (size_t)workspace_bytes < need ||
+                      ((uintptr_t)workspace & 255))) {
+        pt::set_error("session workspace: need %zu bytes, 256-byte aligned", need);
+        return PT_EINVAL;
+    }
     cudaStream_t st = (cudaStream_t)stream;
     pt_session* s = new pt_session();
     s->plan = plan;
@@ -368,41 +445,21 @@ int pt_session_create(pt_plan* plan, const pt_solver_desc* desc, const float* da
     s->data = data;
     s->n = (size_t)plan->Z * plan->H * plan->W;
     const size_t n = s->n;
-    int rc = PT_OK;
-    // one slab for all state buffers (256-byte aligned carve-outs)
-    std::vector<std::pair<float**, size_t>> req;
-    auto A = [&](float** p, size_t cnt) { req.push_back({p, (std::max<size_t>(1, cnt) + 63) & ~size_t(63)}); };
-    A(&s->x[0], n); A(&s->x[1], n); A(&s->h, n); A(&s->v, n); A(&s->xhat, n);
-    if (desc->estimator == PT_EST_SVRG || desc->estimator == PT_EST_LSVRG) {
-        A(&s->snap, n); A(&s->fg, n);
-        A(&s->rsnap, (size_t)plan->A * plan->Z * plan->B);
-    }
-    if (desc->estimator == PT_EST_SAGA) { A(&s->saga_table, n * desc->n_subsets); A(&s->saga_sum, n); }
-    if (desc->prox_kind == 1) {
-        A(&s->dp, n); A(&s->dq, n);
-        if (plan->Z > 1) A(&s->dw, n);
-        A(&s->fgp_work, (size_t)pt::fgp_workspace_floats(plan));
-    }
-    A(&s->r, (size_t)plan->A * plan->Z * plan->B);
-    A(&s->g, n);
-    {
-        size_t total = 0;
-        for (auto& q : req) total += q.second;
-        if (cudaMalloc(&s->slab, total * sizeof(float)) != cudaSuccess) {
-            pt::set_error("session allocation of %zu bytes failed", total * sizeof(float));
-            rc = PT_ECUDA;
-        } else {
-            size_t off = 0;
-            for (auto& q : req) {
-                *q.first = s->slab + off;
-                off += q.second;
-            }
+    char* base = (char*)workspace;
+    if (!base) {
+        if (cudaMalloc(&base, need) != cudaSuccess) {
+            pt::set_error("session allocation of %zu bytes failed", need);
+            delete s;
+            return PT_ECUDA;
         }
+        s->owns_slab = true;
+    } else {
+        s->owns_slab = false;
     }
-    if (rc == PT_OK && cudaMalloc(&s->bad, sizeof(int64_t)) != cudaSuccess) rc = PT_ECUDA;
-    if (rc == PT_OK) rc = pt::workspace_alloc(plan, &s->ws);
+    s->slab = (float*)base;
+    session_layout(plan, desc, s, base);
     s->ws.prof = &s->prof;
-    if (rc == PT_OK) rc = build_selections(s);
+    rc = build_selections(s);
     if (rc == PT_OK) {
         // solvers.py:161,172,178-179: x0 (or zeros), h = 0, SAGA table/sum = 0
         if (x0) rc = cudaMemcpyAsync(s->x[0], x0, n * 4, cudaMemcpyDeviceToDevice, st) ? PT_ECUDA : PT_OK;
@@ -420,13 +477,17 @@ int pt_session_create(pt_plan* plan, const pt_solver_desc* desc, const float* da
     return PT_OK;
 }
 
+int pt_session_create(pt_plan* plan, const pt_solver_desc* desc, const float* data,
+                      const float* x0, pt_session** out, void* stream)
+{
+    return pt_session_create_in(plan, desc, data, x0, nullptr, 0, out, stream);
+}
+
 int pt_session_destroy(pt_session* s)
 {
     if (!s) return PT_OK;
     cudaDeviceSynchronize();
-    if (s->slab) cudaFree(s->slab);
-    if (s->bad) cudaFree(s->bad);
-    pt::workspace_free(&s->ws);
+    if (s->slab && s->owns_slab) cudaFree(s->slab);  // state, flag and workspace
     if (s->comm && s->owns_comm && s->nccl.destroy) s->nccl.destroy(s->comm);
     if (s->fgp3_work) cudaFree(s->fgp3_work);
     if (s->dw_slab) cudaFree(s->dw_slab);

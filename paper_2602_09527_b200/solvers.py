@@ -134,10 +134,18 @@ class _Session:
                             int(bool(tv.warm_start)) if tv else 0,
                             int(bool(tv.nonneg)) if tv else 0)
         self.x0 = None if x0 is None else as_device(x0)
+        # every session buffer comes from torch's caching allocator (on the solver
+        # stream), so repeated solves reuse memory instead of cudaMalloc-ing ~1 GB
+        nbytes = int(lib.pt_session_workspace_bytes(self.plan.handle, ctypes.byref(desc)))
+        if nbytes <= 0:
+            N.check(N.PT_EINVAL, "session workspace size")
+        with torch.cuda.stream(stream):
+            self._memory = torch.empty(nbytes + 256, dtype=torch.uint8, device="cuda")
+        base = (self._memory.data_ptr() + 255) & ~255
         handle = ctypes.c_void_p()
-        N.check(lib.pt_session_create(self.plan.handle, ctypes.byref(desc), N.ptr(self.data),
-                                      N.ptr(self.x0), ctypes.byref(handle),
-                                      N.stream_handle(stream)), "session")
+        N.check(lib.pt_session_create_in(self.plan.handle, ctypes.byref(desc), N.ptr(self.data),
+                                         N.ptr(self.x0), base, nbytes, ctypes.byref(handle),
+                                         N.stream_handle(stream)), "session")
         self.handle = handle
         self.shape = problem.projector.shape
         self.n = int(np.prod(self.shape))
