@@ -605,6 +605,7 @@ struct AdjArgs {
     int32_t n_sel;
     int32_t H, W, Z, B;
     int32_t slot;
+    int32_t vec;      // 16-byte staging: rows start at 4-aligned bins (B % 4 == 0, y 16B-aligned)
     int32_t cand_half;
     int32_t nbuf;     // staging buffers (2: chunk pipeline)
     int32_t n_epi;    // epilogue operand planes prefetched into shared memory
@@ -720,23 +721,35 @@ __global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
             const double e0 = bf00 - bref;
             const double lo = e0 + fmin(0.0, gbr) * (TR - 1) + fmin(0.0, gbc) * (TC - 1);
             const int jlo = (int)floor(lo) - P.cand_half - 1;
+            const int bb = (int)bref + jlo;
+            // vec: the staged row starts at the 4-aligned bin below bb
+            const int shift = P.vec ? bb - (bb & ~3) : 0;
             if (lane == 0) {
                 const float stp = t.step_len;
                 s_p4[buf][a] = make_float4((float)gbr, (float)gbc, (float)e0,
                                            (float)fabs(t.sigma));
                 // shared byte address of local bin 0 minus the floor-trick offset
-                const uint32_t ya = stage_u32 + (uint32_t)((buf * NA + a) * P.slot - jlo) * 4u -
+                const uint32_t ya = stage_u32 +
+                                    (uint32_t)((buf * NA + a) * P.slot - jlo + shift) * 4u -
                                     (uint32_t)kMagicBits * 4u;
                 s_p2[buf][a] = make_float2(stp, __uint_as_float(ya));
-                s_off[buf][a] = -jlo;
+                s_off[buf][a] = shift - jlo;
             }
-            const int bb = (int)bref + jlo;
             const float* yrow = P.y + ((size_t)k * P.Z + z) * P.B;
             const uint32_t dst = stage_u32 + (uint32_t)((buf * NA + a) * P.slot) * 4u;
-            for (int j = lane; j < P.slot; j += 32) {
-                const int bj = bb + j;
-                const bool ok = bj >= 0 && bj < P.B;
-                cp_async4(dst + (uint32_t)j * 4u, yrow + (ok ? bj : 0), ok);
+            if (P.vec) {
+                const int bb0 = bb & ~3;
+                for (int c = lane; c < (P.slot >> 2); c += 32) {
+                    const int bj = bb0 + 4 * c;  // chunks lie fully inside or outside [0, B)
+                    const bool ok = bj >= 0 && bj < P.B;
+                    cp_async16(dst + (uint32_t)c * 16u, yrow + (ok ? bj : 0), ok ? 16 : 0);
+                }
+            } else {
+                for (int j = lane; j < P.slot; j += 32) {
+                    const int bj = bb + j;
+                    const bool ok = bj >= 0 && bj < P.B;
+                    cp_async4(dst + (uint32_t)j * 4u, yrow + (ok ? bj : 0), ok);
+                }
             }
         }
         cp_async_commit();
@@ -771,7 +784,16 @@ __global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
         for (int a = warp; a < nc; a += NW) {
             const float stp = s_p2[buf][a].x;
             float* row = smem + (size_t)(buf * NA + a) * P.slot;
-            for (int j = lane; j < P.slot; j += 32) row[j] *= stp;
+            if (P.vec) {
+                float4* row4 = reinterpret_cast<float4*>(row);
+                for (int c = lane; c < (P.slot >> 2); c += 32) {
+                    float4 q = row4[c];
+                    q.x *= stp; q.y *= stp; q.z *= stp; q.w *= stp;
+                    row4[c] = q;
+                }
+            } else {
+                for (int j = lane; j < P.slot; j += 32) row[j] *= stp;
+            }
         }
         __syncthreads();
         if (TWO_TAP) {
@@ -905,7 +927,8 @@ int launch_adjoint(pt_plan* plan, const pt_selection* sel, const float* y, float
     a.sel_angle = sel->d_angle;
     a.n_sel = sel->n;
     a.H = plan->H; a.W = plan->W; a.Z = plan->Z; a.B = plan->B;
-    a.slot = plan->gather_slot;
+    a.vec = (plan->B % 4 == 0) && (((uintptr_t)y & 15) == 0);
+    a.slot = a.vec ? ((plan->gather_slot + 3 + 3) & ~3) : plan->gather_slot;
     a.cand_half = plan->cand_half;
     a.nbuf = sel->n > kNA ? 2 : 1;
     a.alpha = alpha;
