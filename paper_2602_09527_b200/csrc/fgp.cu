@@ -128,6 +128,13 @@ __device__ __forceinline__ float rsqrt_ftz(float x)
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
+// max that propagates NaN (max.NaN): the divergence check must see NaN duals
+__device__ __forceinline__ float max_nan(float a, float b)
+{
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
 __device__ __forceinline__ f2 ld2(const float2* p)
 {
     f2 r;
@@ -165,7 +172,7 @@ __device__ __forceinline__ void fgp2d_iteration_packed(
         if (nonneg) {
             float ua, ub;
             upk(u, ua, ub);
-            u = pk((ua < 0.f) ? 0.f : ua, (ub < 0.f) ? 0.f : ub);  // NaN propagates
+            u = pk(max_nan(ua, 0.f), max_nan(ub, 0.f));  // NaN propagates
         }
         U[j] = u;
         st2(&S_u2[prow0 + j][tx], u);
@@ -185,8 +192,8 @@ __device__ __forceinline__ void fgp2d_iteration_packed(
         const f2 n2 = fma2(ph, ph, mul2(qh, qh));
         float na, nb;
         upk(n2, na, nb);
-        // max(1, |.|): the projection only rescales when |.| > 1 (no denormals there)
-        const f2 inv = pk((na > 1.f) ? rsqrt_ftz(na) : 1.f, (nb > 1.f) ? rsqrt_ftz(nb) : 1.f);
+        // 1 / max(1, |.|): rsqrt of max(n2, 1) (exactly 1 at 1; NaN propagates)
+        const f2 inv = pk(rsqrt_ftz(max_nan(na, 1.f)), rsqrt_ftz(max_nan(nb, 1.f)));
         const f2 pn = mul2(ph, inv), qn = mul2(qh, inv);
         R[j] = fma2(beta2, sub2(pn, Pp[j]), pn);
         S[j] = fma2(beta2, sub2(qn, Q[j]), qn);
