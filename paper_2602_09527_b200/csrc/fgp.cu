@@ -255,11 +255,21 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
         S[j] = pk(sv[0], sv[1]);
         U[j] = pk(0.f, 0.f);
     }
-    for (int it = 0; it < P.n_iter; ++it) {
-        if (!edge) {
+    if (!edge) {
+        // two iterations per trip: the compiler alternates register roles instead of moving
+        int it = 0;
+        for (; it + 1 < P.n_iter; it += 2) {
             fgp2d_iteration_packed<RW, RH, STRIP>(V, Pp, Q, R, S, U, S_s2, S_u2, S_r, S_ut, tx, ty,
                                                   P.lam, P.eta, P.beta[it], P.nonneg);
-        } else {
+            fgp2d_iteration_packed<RW, RH, STRIP>(V, Pp, Q, R, S, U, S_s2, S_u2, S_r, S_ut, tx, ty,
+                                                  P.lam, P.eta, P.beta[it + 1], P.nonneg);
+        }
+        if (it < P.n_iter)
+            fgp2d_iteration_packed<RW, RH, STRIP>(V, Pp, Q, R, S, U, S_s2, S_u2, S_r, S_ut, tx, ty,
+                                                  P.lam, P.eta, P.beta[it], P.nonneg);
+    }
+    for (int it = 0; edge && it < P.n_iter; ++it) {
+        {
             float v[STRIP], p[STRIP], q[STRIP], r[STRIP], s[STRIP], u[STRIP];
 #pragma unroll
             for (int j = 0; j < H2; ++j) {
