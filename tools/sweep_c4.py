@@ -96,6 +96,10 @@ def main():
     ap.add_argument("--fista", type=int, default=2000)
     ap.add_argument("--epochs", type=int, default=100)
     ap.add_argument("--out", default="profiles/sweep_c4.json")
+    ap.add_argument("--harness-dir", default=None,
+                    help="also run the reference-schema sweep harness (sweep.run_sweep: per-cell "
+                         "CSVs, summary.csv, speedups.csv) with rel_err against the FISTA image")
+    ap.add_argument("--harness-tol", type=float, default=1e-3)
     args = ap.parse_args()
     torch.cuda.set_device(0)
     cfg, proj, problem, lip, alpha = build_problem()
@@ -132,6 +136,19 @@ def main():
     with open(args.out, "w") as fh:
         json.dump(result, fh, indent=1)
     print(json.dumps(result["projector_4096"]))
+    if args.harness_dir:
+        # the reference's sweep harness semantics (bench.py:234-262): time to a
+        # squared relative error tolerance against a reference image
+        from paper_2602_09527_b200.metrics import StoppingRule
+        from paper_2602_09527_b200.sweep import SweepGrid, run_sweep
+        grid = SweepGrid(("fista", "ista", "sgd", "saga", "svrg", "lsvrg"),
+                         n_subsets=(cfg.n_subsets,), probabilities=(1.0, 0.5, 0.1, 0.05, 0.01),
+                         inner_iterations=(cfg.fgp_inner,), seeds=(0,))
+        rows = run_sweep(grid, problem, ref.image, args.harness_dir,
+                         StoppingRule(tolerance=args.harness_tol, max_data_passes=args.epochs),
+                         lipschitz=lip)
+        print(json.dumps({"harness_cells": len(rows),
+                          "reached": sum(1 for r in rows if r["reached"])}))
 
 
 if __name__ == "__main__":
