@@ -800,7 +800,7 @@ __global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
             f2 acc2[PIX / 2];
 #pragma unroll
             for (int jj = 0; jj < PIX / 2; ++jj) acc2[jj] = pk(0.f, 0.f);
-#pragma unroll 1
+#pragma unroll 8
             for (int a = 0; a < nc; ++a) {
                 const float4 q4 = s_p4[buf][a];
                 const float2 q2 = s_p2[buf][a];
