@@ -164,7 +164,6 @@ int pt_plan_create(const pt_geometry_desc* d, pt_plan** out)
         min_abs_sigma = std::min(min_abs_sigma, fabs(t.sigma));
     }
     p->cand_half = std::max(1, (int)ceil(1.0 / min_abs_sigma - 1e-12));
-    p->gather_slot = (int)ceil(31 * max_br + 63 * max_bc) + 2 * p->cand_half + 8;
     const int mn = std::min(p->H, p->W);
     // forward tile configuration (band height TY x lane tile TX), see projector.cu
     static const int cfg_env = [] {
@@ -183,6 +182,22 @@ int pt_plan_create(const pt_geometry_desc* d, pt_plan** out)
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) { set_error("cudaGetDevice: %s", cudaGetErrorString(e)); delete p; return PT_ECUDA; }
+    // gather tile: the largest whose CTA count still fills ~4 waves of SMs
+    {
+        static const int env = [] {
+            const char* v = getenv("PT_GATHER_TILE");
+            return v ? atoi(v) : -1;
+        }();
+        int pick = 2;
+        for (int t = 0; t < 3; ++t) {
+            const long long ctas = (long long)((p->W + kGatherTiles[t][1] - 1) / kGatherTiles[t][1]) *
+                                   ((p->H + kGatherTiles[t][0] - 1) / kGatherTiles[t][0]) * p->Z;
+            if (ctas >= 4LL * p->sm_count) { pick = t; break; }
+        }
+        p->gather_tile = (env >= 0 && env < 3) ? env : pick;
+        const int tr = kGatherTiles[p->gather_tile][0], tc = kGatherTiles[p->gather_tile][1];
+        p->gather_slot = (int)ceil((tr - 1) * max_br + (tc - 1) * max_bc) + 2 * p->cand_half + 8;
+    }
     if (cudaMalloc(&p->d_tab, sizeof(AngleTab) * p->A) != cudaSuccess ||
         cudaMemcpy(p->d_tab, p->h_tab.data(), sizeof(AngleTab) * p->A, cudaMemcpyHostToDevice) != cudaSuccess) {
         set_error("angle table upload failed");

@@ -654,7 +654,7 @@ __device__ __forceinline__ void step_epilogue(const pt_step_epilogue& ep, size_t
 }
 
 template <int TR, int TC, int NT, int NA, bool TWO_TAP>
-__global__ void __launch_bounds__(NT, 4) adj_gather_kernel(AdjArgs P)
+__global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_kernel(AdjArgs P)
 {
     constexpr int PIX = TR * TC / NT;  // pixels per thread
     constexpr int ROWSTEP = NT / TC;
@@ -897,23 +897,36 @@ __global__ void epilogue_kernel(const float* g, size_t n, pt_step_epilogue ep)
         step_epilogue(ep, p, g ? g[p] : 0.f);  // g == null: a zero gradient difference
 }
 
-static constexpr int kTR = 32, kTC = 64, kNT = 256, kNA = 32;
+static constexpr int kNT = 256, kNA = 32;
 
-template <bool TWO>
-static int run_gather(pt_plan* plan, const AdjArgs& a, cudaStream_t st)
+template <int TR, int TC, bool TWO>
+static int run_gather_t(pt_plan* plan, const AdjArgs& a, cudaStream_t st)
 {
-    const size_t smem = (size_t)(a.nbuf * kNA * a.slot + a.n_epi * kTR * kTC) * sizeof(float);
+    const size_t smem = (size_t)(a.nbuf * kNA * a.slot + a.n_epi * TR * TC) * sizeof(float);
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
-        PT_CHECK_CUDA(cudaFuncSetAttribute(adj_gather_kernel<kTR, kTC, kNT, kNA, TWO>,
+        PT_CHECK_CUDA(cudaFuncSetAttribute(adj_gather_kernel<TR, TC, kNT, kNA, TWO>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem));
         attr = smem;
     }
-    dim3 grid((plan->W + kTC - 1) / kTC, (plan->H + kTR - 1) / kTR, plan->Z);
-    adj_gather_kernel<kTR, kTC, kNT, kNA, TWO><<<grid, kNT, smem, st>>>(a);
+    dim3 grid((plan->W + TC - 1) / TC, (plan->H + TR - 1) / TR, plan->Z);
+    adj_gather_kernel<TR, TC, kNT, kNA, TWO><<<grid, kNT, smem, st>>>(a);
     PT_CHECK_LAUNCH();
     return PT_OK;
+}
+
+template <bool TWO>
+static int run_gather(pt_plan* plan, const AdjArgs& a, cudaStream_t st)
+{
+    static_assert(kGatherTiles[0][0] == 32 && kGatherTiles[0][1] == 128 &&
+                  kGatherTiles[1][0] == 32 && kGatherTiles[1][1] == 64 &&
+                  kGatherTiles[2][0] == 16 && kGatherTiles[2][1] == 64, "gather tiles");
+    switch (plan->gather_tile) {
+        case 0: return run_gather_t<32, 128, TWO>(plan, a, st);
+        case 1: return run_gather_t<32, 64, TWO>(plan, a, st);
+        default: return run_gather_t<16, 64, TWO>(plan, a, st);
+    }
 }
 
 int launch_adjoint(pt_plan* plan, const pt_selection* sel, const float* y, float* x_out,

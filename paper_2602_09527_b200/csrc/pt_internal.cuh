@@ -64,6 +64,12 @@ struct pt_selection {
 };
 
 namespace pt {
+// Gather pixel tiles (rows x columns), 256 threads each: 0 = 32 x 128 (16
+// pixels per thread, large images), 1 = 32 x 64 (8), 2 = 16 x 64 (4, small
+// images: enough CTAs).  The plan picks one and sizes its staged-bin slot per
+// angle for that tile (capi.cu).
+constexpr int kGatherTiles[3][2] = {{32, 128}, {32, 64}, {16, 64}};
+
 // Per-caller scratch for the forward band partials and reductions.  The plan
 // owns one (used by the standalone C-ABI calls, which must therefore be
 // stream-serialised per plan, like a cuFFT plan); every session owns its own.
@@ -116,6 +122,7 @@ struct pt_plan {
     pt::AngleTab* d_tab = nullptr;
     int32_t cand_half = 1;     // gather candidates per side: ceil(h/ds) (1 = two-tap)
     int32_t gather_slot = 0;   // floats of staged sinogram per angle in the gather
+    int32_t gather_tile = 0;   // index into kGatherTiles
     int32_t fwd_cfg = 0, fwd_ty = 64, fwd_tx = 256;
     int32_t n_bands = 0;
     int32_t max_angles_per_launch = 0;

@@ -198,3 +198,33 @@ def test_native_launch_counter_moves():
     forward_project(np.ones((16, 16)), ParallelGeometry.uniform(4, 9))
     torch.cuda.synchronize()
     assert N.launch_count() > before
+
+
+_TILE_SNIPPET = r"""
+import sys, numpy as np
+sys.path.insert(0, {repo!r})
+import oracle as O
+from paper_2602_09527_b200 import ParallelGeometry, back_project
+g = ParallelGeometry.uniform(37, 301)
+rng = np.random.default_rng(3)
+y = rng.standard_normal((37, 301))
+sub = tuple(range(0, 37, 2))
+ys = y[list(sub)]
+got = back_project(ys, g, (190, 211), sub).double().cpu().numpy()
+O.set_mode("fast")
+ref = O.back_project(ys, g, (190, 211), sub)
+print(float(np.linalg.norm(got - ref) / np.linalg.norm(ref)))
+"""
+
+
+@pytest.mark.parametrize("tile", [0, 1, 2])
+def test_every_gather_tile_matches_oracle(tile):
+    """Each gather tile shape (the plan picks one by image size) against the oracle."""
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PT_GATHER_TILE=str(tile))
+    out = subprocess.run([sys.executable, "-c", _TILE_SNIPPET.format(repo=repo)], env=env,
+                         check=True, capture_output=True, text=True, timeout=300)
+    assert float(out.stdout.strip().splitlines()[-1]) <= 1e-5
