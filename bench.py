@@ -44,7 +44,7 @@ sys.path.insert(0, REPO)
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2", choices=["c0", "c1", "c2", "c3"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
