@@ -452,6 +452,7 @@ struct Fgp3Args {
     float* Pn;          // P_{k+1}
     float* Rn;          // R_{k+1}
     float lam, eta, beta;  // beta = beta_k (momentum of the output)
+    float beta_r;          // PQ form: R_k = P_k + beta_r (P_k - P_{k-1}) formed on chip
     int nonneg;
 };
 
@@ -477,24 +478,30 @@ __device__ __forceinline__ void cpa4(uint32_t dst, const float* src, bool valid)
 
 // Stage layout of one plane: R box [3][TY+2][TX+8] (rows i0-1 .., columns
 // j0-4 ..), v box [TY+2][TX+8] (same window), P box [3][TY][TX].
-template <int TX, int TY, int NS>
+// PQ form: the R box holds P_k, a second window box (same shape, at QOFF)
+// holds P_{k-1}, and R is formed on chip; no P box.  40 B per voxel of HBM
+// traffic instead of 52, more shared-memory reads and FMAs.
+template <int TX, int TY, int NS, bool PQ = false>
 struct Fgp3Tile {
     static constexpr int NT = TX * TY / 2;      // 2 output rows per thread
     static constexpr int RW = TX + 8, RR = TY + 2, ARR = RR * RW;
-    static constexpr int VOFF = (3 * ARR + 31) & ~31;
-    static constexpr int POFF = (VOFF + ARR + 31) & ~31;
+    static constexpr int WIN3 = (3 * ARR + 31) & ~31;
+    static constexpr int QOFF = WIN3;                      // PQ only
+    static constexpr int VOFF = PQ ? 2 * WIN3 : WIN3;
+    static constexpr int POFF = (VOFF + ARR + 31) & ~31;   // R form only
     static constexpr int PARR = TX * TY;
-    static constexpr int STAGE = (POFF + 3 * PARR + 31) & ~31;
+    static constexpr int STAGE = PQ ? ((VOFF + ARR + 31) & ~31) : ((POFF + 3 * PARR + 31) & ~31);
     static constexpr int NWW = (TY + 1) * (TX + 1);   // u window
     static constexpr int SMEM_FLOATS = NS * STAGE + 2 * NWW;
-    static constexpr int TMA_BYTES_RV = 4 * ARR * 4, TMA_BYTES_P = 3 * PARR * 4;
+    static constexpr int TMA_BYTES_RV = 4 * ARR * 4;
+    static constexpr int TMA_BYTES_P = PQ ? 3 * ARR * 4 : 3 * PARR * 4;
 };
 
-template <int TX, int TY, int NS, bool TMA>
+template <int TX, int TY, int NS, bool TMA, bool PQ>
 __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
                                                                  const __grid_constant__ Fgp3Maps m)
 {
-    using T = Fgp3Tile<TX, TY, NS>;
+    using T = Fgp3Tile<TX, TY, NS, PQ>;
     constexpr int NT = T::NT, RW = T::RW, RR = T::RR, ARR = T::ARR, NWW = T::NWW;
     constexpr int KU = (NWW + NT - 1) / NT;
     extern __shared__ __align__(128) float fsm[];
@@ -532,10 +539,16 @@ __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
                 "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
                 " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb),
                 "l"(&m.R), "r"(j0 - 4), "r"(i0 - 1), "r"(0), "r"(p + 1), "r"(bar) : "memory");
-            asm volatile(
-                "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-                " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb + (uint32_t)T::POFF * 4u),
-                "l"(&m.P), "r"(j0), "r"(i0), "r"(0), "r"(p + 1), "r"(bar) : "memory");
+            if (PQ)  // P_{k-1} window
+                asm volatile(
+                    "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb + (uint32_t)T::QOFF * 4u),
+                    "l"(&m.P), "r"(j0 - 4), "r"(i0 - 1), "r"(0), "r"(p + 1), "r"(bar) : "memory");
+            else     // P_k centre
+                asm volatile(
+                    "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb + (uint32_t)T::POFF * 4u),
+                    "l"(&m.P), "r"(j0), "r"(i0), "r"(0), "r"(p + 1), "r"(bar) : "memory");
             if (withv && p < a.Zl)
                 asm volatile(
                     "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
@@ -560,13 +573,25 @@ __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
                 cpa4(sb + (uint32_t)((arr < 3 ? arr * ARR : T::VOFF) + r * RW + 3 + c) * 4u,
                      src + (ok ? gi * W + gj : 0), ok);
             }
-            for (int idx = tid; idx < 3 * T::PARR; idx += NT) {
-                const int comp = idx / T::PARR, rem = idx - comp * T::PARR;
-                const int r = rem / TX, c = rem - r * TX;
-                const int gi = i0 + r, gj = j0 + c;
-                const bool ok = gi < H && gj < W;
-                cpa4(sb + (uint32_t)(T::POFF + idx) * 4u,
-                     a.P + b0 + comp * HW + (ok ? gi * W + gj : 0), ok);
+            if (PQ) {
+                constexpr int NQ = 3 * RR * CW;  // P_{k-1} windows
+                for (int idx = tid; idx < NQ; idx += NT) {
+                    const int arr = idx / (RR * CW), rem = idx - arr * (RR * CW);
+                    const int r = rem / CW, c = rem - r * CW;
+                    const int gi = i0 - 1 + r, gj = j0 - 1 + c;
+                    const bool ok = gi >= 0 && gi < H && gj >= 0 && gj < W;
+                    cpa4(sb + (uint32_t)(T::QOFF + arr * ARR + r * RW + 3 + c) * 4u,
+                         a.P + b0 + arr * HW + (ok ? gi * W + gj : 0), ok);
+                }
+            } else {
+                for (int idx = tid; idx < 3 * T::PARR; idx += NT) {
+                    const int comp = idx / T::PARR, rem = idx - comp * T::PARR;
+                    const int r = rem / TX, c = rem - r * TX;
+                    const int gi = i0 + r, gj = j0 + c;
+                    const bool ok = gi < H && gj < W;
+                    cpa4(sb + (uint32_t)(T::POFF + idx) * 4u,
+                         a.P + b0 + comp * HW + (ok ? gi * W + gj : 0), ok);
+                }
             }
             asm volatile("cp.async.commit_group;");
         }
@@ -593,6 +618,16 @@ __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
                                ((gj > 0) << 3) | ((gi < H && gj < W) << 4))
                             : -1;
     }
+    // R at staged offset o (PQ: formed from P_k and P_{k-1}, the same
+    // expression the R-state form stores, so both forms give identical bits)
+    const float br = a.beta_r;
+    auto rv = [&](const float* st, int o) -> float {
+        if (PQ) {
+            const float pv = st[o];
+            return pv + br * (pv - st[T::QOFF + o]);
+        }
+        return st[o];
+    };
     // u of plane z (its stage s) into sU[z & 1]; R_w of z - 1 from stage s1
     auto compute_U = [&](int z, int s, int s1) {
         const int zg = a.z0 + z;
@@ -608,12 +643,12 @@ __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
             float u = 0.f;
             if (gd & 16) {
                 // D^T(R) in the order of the reference's _diff_adjoint (+ z)
-                float x = (gd & 1) ? -st[o] : 0.f;
-                if (gd & 2) x += st[o - RW];
-                if (gd & 4) x -= st[ARR + o];
-                if (gd & 8) x += st[ARR + o - 1];
-                if (zhi) x -= st[2 * ARR + o];
-                if (zlo) x += st1[2 * ARR + o];
+                float x = (gd & 1) ? -rv(st, o) : 0.f;
+                if (gd & 2) x += rv(st, o - RW);
+                if (gd & 4) x -= rv(st, ARR + o);
+                if (gd & 8) x += rv(st, ARR + o - 1);
+                if (zhi) x -= rv(st, 2 * ARR + o);
+                if (zlo) x += rv(st1, 2 * ARR + o);
                 u = st[T::VOFF + o] - a.lam * x;
                 if (a.nonneg) u = (u < 0.f) ? 0.f : u;
             }
@@ -646,7 +681,7 @@ __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
         const float* U0 = sU + (z & 1) * NWW;
         const float* U1 = sU + ((z + 1) & 1) * NWW;
         float* __restrict__ pn = a.Pn + ((size_t)(z + 1) * 3) * HW;
-        float* __restrict__ rn = a.Rn + ((size_t)(z + 1) * 3) * HW;
+        float* __restrict__ rn = PQ ? nullptr : a.Rn + ((size_t)(z + 1) * 3) * HW;
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
             const int r = ty + rr * RSTEP, gi = i0 + r;
@@ -657,21 +692,22 @@ __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
             const float gv = (gi < H - 1) ? U0[wi + TX + 1] - uo : 0.f;
             const float gh = (gj < W - 1) ? U0[wi + 1] - uo : 0.f;
             const float gz = top ? U1[wi] - uo : 0.f;
-            const float ph = st[o] + a.eta * gv;
-            const float qh = st[ARR + o] + a.eta * gh;
-            const float wh = st[2 * ARR + o] + a.eta * gz;
+            const float ph = rv(st, o) + a.eta * gv;
+            const float qh = rv(st, ARR + o) + a.eta * gh;
+            const float wh = rv(st, 2 * ARR + o) + a.eta * gz;
             const float n2 = ph * ph + qh * qh + wh * wh;
             const float inv = (n2 > 1.f) ? rsqrt_ftz(n2) : 1.f;
             const float p0 = ph * inv, p1 = qh * inv, p2 = wh * inv;
-            const int po = T::POFF + r * TX + tx;
-            const float* pc = st + po;
             const int g = gi * W + gj;
             pn[g] = p0;
             pn[HW + g] = p1;
             pn[2 * HW + g] = p2;
-            rn[g] = p0 + a.beta * (p0 - pc[0]);
-            rn[HW + g] = p1 + a.beta * (p1 - pc[T::PARR]);
-            rn[2 * HW + g] = p2 + a.beta * (p2 - pc[2 * T::PARR]);
+            if (!PQ) {
+                const float* pc = st + T::POFF + r * TX + tx;
+                rn[g] = p0 + a.beta * (p0 - pc[0]);
+                rn[HW + g] = p1 + a.beta * (p1 - pc[T::PARR]);
+                rn[2 * HW + g] = p2 + a.beta * (p2 - pc[2 * T::PARR]);
+            }
         }
     }
     if (!TMA) asm volatile("cp.async.wait_group 0;");
@@ -819,14 +855,14 @@ static int make_map(CUtensorMap* m, const float* base, int rank, const cuuint64_
     return PT_OK;
 }
 
-template <int TX, int TY, int NS, bool TMA>
+template <int TX, int TY, int NS, bool TMA, bool PQ>
 static int fgp3d_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
 {
-    using T = Fgp3Tile<TX, TY, NS>;
+    using T = Fgp3Tile<TX, TY, NS, PQ>;
     const size_t smem = (size_t)T::SMEM_FLOATS * 4;
     static bool attr = false;
     if (!attr) {
-        PT_CHECK_CUDA(cudaFuncSetAttribute(fgp3d_iter_kernel<TX, TY, NS, TMA>,
+        PT_CHECK_CUDA(cudaFuncSetAttribute(fgp3d_iter_kernel<TX, TY, NS, TMA, PQ>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
@@ -840,7 +876,7 @@ static int fgp3d_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
         const cuuint64_t d3[3] = {W, H, (cuuint64_t)a.Zl};
         const cuuint32_t b3[3] = {(cuuint32_t)T::RW, (cuuint32_t)T::RR, 1};
         int rc = make_map(&m.R, a.R, 4, d4, bR);
-        if (!rc) rc = make_map(&m.P, a.P, 4, d4, bP);
+        if (!rc) rc = make_map(&m.P, a.P, 4, d4, PQ ? bR : bP);
         if (!rc) rc = make_map(&m.V, a.v, 3, d3, b3);
         if (!rc) rc = make_map(&m.Vt, a.vtop, 2, d3, b3);
         if (rc) return rc;
@@ -854,7 +890,7 @@ static int fgp3d_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
     // 8 -> 155 us, 16 -> 153 us, 32 -> 165 us, 64 -> 189 us per iteration
     a.zchunk = zc_env ? zc_env : 16;
     dim3 grid(gx, gy, (a.Zl + a.zchunk - 1) / a.zchunk);
-    fgp3d_iter_kernel<TX, TY, NS, TMA><<<grid, T::NT, smem, st>>>(a, m);
+    fgp3d_iter_kernel<TX, TY, NS, TMA, PQ><<<grid, T::NT, smem, st>>>(a, m);
     PT_CHECK_LAUNCH();
     return PT_OK;
 }
@@ -865,6 +901,13 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
 {
     // TMA needs 16-byte row pitch; 64 x 8 tiles, 3-stage ring
     const bool tma = (W % 4) == 0 && encode_tiled() != nullptr;
+    // PQ form (40 B/voxel, R formed on chip) by default: 14.1 vs 15.35 ms per
+    // FGP-100 at 256^3 for the R-state form (52 B/voxel); PT_FGP3_PQ=0 selects it
+    static const int pq_env = [] {
+        const char* e = getenv("PT_FGP3_PQ");
+        return e ? atoi(e) : 1;
+    }();
+    const bool pq = pq_env != 0;
     std::vector<double> betas(inner);
     double t = 1.0;
     for (int k = 0; k < inner; ++k) {
@@ -889,34 +932,54 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
                 PT_CHECK_CUDA(cudaMemsetAsync(set + (size_t)(Zl + 1) * plane3, 0, plane3 * 4, st));
         }
     }
-    int rc = fgp3d_exchange(sl, G, H, W, 1, true, halo, st);
+    // R form: sets 0/1 = P, R of even iterations, 2/3 of odd ones.
+    // PQ form: sets 0, 1, 2 rotate P_{k-1}, P_k -> P_{k+1} (set 1 starts as a copy of P_0).
+    int rc = fgp3d_exchange(sl, G, H, W, pq ? 0 : 1, true, halo, st);
     if (rc) return rc;
     for (int kk = 0; kk < inner; ++kk) {
-        const int in = (kk & 1) ? 2 : 0, out = (kk & 1) ? 0 : 2;  // P set; R = P + 1
+        int set_p, set_r, set_pn, set_rn;
+        if (pq) {
+            set_r = kk % 3;                          // P_k (windows)
+            set_p = kk == 0 ? 0 : (kk + 2) % 3;      // P_{k-1}
+            set_pn = (kk + 1) % 3;
+            set_rn = -1;
+        } else {
+            set_p = (kk & 1) ? 2 : 0;
+            set_r = set_p + 1;
+            set_pn = (kk & 1) ? 0 : 2;
+            set_rn = set_pn + 1;
+        }
         for (int g = 0; g < G; ++g) {
             const int Zl = sl[g].Zl;
             Fgp3Args a;
             a.Zl = Zl; a.H = H; a.W = W; a.z0 = sl[g].z0; a.Zg = Zg;
             a.v = sl[g].v;
             a.vtop = fgp3d_vtop(sl[g].work, Zl, H, W);
-            a.P = fgp3d_set(sl[g].work, in, Zl, H, W);
-            a.R = fgp3d_set(sl[g].work, in + 1, Zl, H, W);
-            a.Pn = fgp3d_set(sl[g].work, out, Zl, H, W);
-            a.Rn = fgp3d_set(sl[g].work, out + 1, Zl, H, W);
+            a.P = fgp3d_set(sl[g].work, set_p, Zl, H, W);
+            a.R = fgp3d_set(sl[g].work, set_r, Zl, H, W);
+            a.Pn = fgp3d_set(sl[g].work, set_pn, Zl, H, W);
+            a.Rn = set_rn >= 0 ? fgp3d_set(sl[g].work, set_rn, Zl, H, W) : nullptr;
             a.lam = (float)lam;
             a.eta = (float)(1.0 / (12.0 * lam));
             a.beta = (float)betas[kk];
+            a.beta_r = kk == 0 ? 0.f : (float)betas[kk - 1];
             a.nonneg = nonneg;
-            rc = tma ? fgp3d_launch<64, 8, 3, true>(a, sm_count, st)
-                     : fgp3d_launch<32, 8, 3, false>(a, sm_count, st);
+            if (pq)
+                rc = tma ? fgp3d_launch<64, 8, 3, true, true>(a, sm_count, st)
+                         : fgp3d_launch<32, 8, 3, false, true>(a, sm_count, st);
+            else
+                rc = tma ? fgp3d_launch<64, 8, 3, true, false>(a, sm_count, st)
+                         : fgp3d_launch<32, 8, 3, false, false>(a, sm_count, st);
             if (rc) return rc;
         }
-        rc = fgp3d_exchange(sl, G, H, W, out + 1, false, halo, st);
+        rc = fgp3d_exchange(sl, G, H, W, pq ? set_pn : set_rn, false, halo, st);
         if (rc) return rc;
     }
-    const int fin = (inner & 1) ? 2 : 0;
-    rc = fgp3d_exchange(sl, G, H, W, fin, false, halo, st);  // P ghost below for D^T
-    if (rc) return rc;
+    const int fin = pq ? inner % 3 : ((inner & 1) ? 2 : 0);
+    if (!pq) {
+        rc = fgp3d_exchange(sl, G, H, W, fin, false, halo, st);  // P ghost below for D^T
+        if (rc) return rc;
+    }
     for (int g = 0; g < G; ++g) {
         const int Zl = sl[g].Zl;
         Fgp3Args a;
