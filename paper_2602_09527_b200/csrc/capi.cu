@@ -36,6 +36,15 @@ void workspace_sizes(const pt_plan* plan, size_t* partial_floats, size_t* red_do
     *image_floats = (size_t)plan->Z * plan->H * plan->W;
 }
 
+bool pdl_enabled()
+{
+    static const bool on = [] {
+        const char* e = getenv("PT_PDL");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return on;
+}
+
 int workspace_alloc(const pt_plan* plan, Workspace* ws)
 {
     workspace_sizes(plan, &ws->partial_floats, &ws->red_doubles, &ws->image_floats);

@@ -205,6 +205,7 @@ __device__ __forceinline__ void fgp2d_iteration_packed(
 template <int RW, int RH, int STRIP>
 __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
 {
+    pdl_wait();
     constexpr int H2 = STRIP / 2;
     // the scalar (edge / epilogue) and the pair (interior) exchange planes
     // share one buffer: a CTA uses one layout at a time
@@ -347,6 +348,7 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
             P.s_out[idx] = s[k];
         }
     }
+    pdl_trigger();
 }
 
 int64_t fgp_workspace_floats(const pt_plan* plan)
@@ -411,7 +413,8 @@ static int run_fgp2d(pt_plan* plan, const float* v, double lam, int inner, int n
         a.bad_iter = (long long*)bad_iter;
         const int IW = RW - 2 * a.halo, IH = RH - 2 * a.halo;
         dim3 grid((plan->W + IW - 1) / IW, (plan->H + IH - 1) / IH);
-        fgp2d_kernel<RW, RH, STRIP><<<grid, RW * (RH / STRIP), 0, st>>>(a);
+        PT_CHECK_CUDA(launch_pdl(fgp2d_kernel<RW, RH, STRIP>, grid, dim3(RW * (RH / STRIP)), 0,
+                                 st, a));
         PT_CHECK_LAUNCH();
         if (!fin) {
             sp = D[0]; sq = D[1]; sr = D[2]; ss = D[3];

@@ -283,6 +283,7 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
     const FwdItem it = decode_item(P, blockIdx.x);
     if (!item_valid(P, it, TY, TX)) return;
     const uint32_t tile_u32 = smem_u32(sm);
+    pdl_wait();  // the image is the predecessor's output
     stage_tile<TY, TX, NT>(P, it, tile_u32);
     cp_async_commit();
 
@@ -382,6 +383,7 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
         }
         if (cbeg + CH < a_end) __syncthreads();  // chunk tables are rewritten next
     }
+    pdl_trigger();
 }
 
 __global__ void sub_images_kernel(const float* a, const float* b, float* out, size_t n)
@@ -405,6 +407,7 @@ struct RedArgs {
 
 __global__ void __launch_bounds__(256) fwd_reduce_kernel(RedArgs P)
 {
+    pdl_wait();
     const size_t total = (size_t)P.n_k * P.Z * P.B;
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     double sq = 0.0;
@@ -450,6 +453,7 @@ __global__ void __launch_bounds__(256) fwd_reduce_kernel(RedArgs P)
             P.block_sums[blockIdx.x] = s;
         }
     }
+    pdl_trigger();
 }
 
 template <int TY, int TX, int NT, int MINB>
@@ -533,7 +537,8 @@ static int run_forward_cfg(pt_plan* plan, Workspace* ws, const pt_selection* sel
                                              (long long)INT32_MAX);
         {
             ProfScope ps(ws, PT_PROF_FWD_BAND, st);
-            fwd_band_kernel<TY, TX, NT, MINB><<<a.n_items, NT, T::SMEM, st>>>(a);
+            PT_CHECK_CUDA(launch_pdl(fwd_band_kernel<TY, TX, NT, MINB>, dim3(a.n_items), dim3(NT),
+                                     (size_t)T::SMEM, st, a));
             PT_CHECK_LAUNCH();
         }
 
@@ -555,7 +560,7 @@ static int run_forward_cfg(pt_plan* plan, Workspace* ws, const pt_selection* sel
         const int nblk = (int)((tot + 255) / 256);
         {
             ProfScope ps(ws, PT_PROF_FWD_REDUCE, st);
-            fwd_reduce_kernel<<<nblk, 256, 0, st>>>(r);
+            PT_CHECK_CUDA(launch_pdl(fwd_reduce_kernel, dim3(nblk), dim3(256), 0, st, r));
             PT_CHECK_LAUNCH();
         }
         red_off += nblk;
@@ -766,6 +771,7 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
     const f2 mg2 = pk(kMagic, kMagic);
 
     const int n_chunks = (P.n_sel + NA - 1) / NA;
+    pdl_wait();  // the residual rows are the predecessor's output
     if (n_chunks > 0) prepare(0, 0);
     for (int ci = 0; ci < n_chunks; ++ci) {
         const int buf = (P.nbuf == 2) ? (ci & 1) : 0;
@@ -869,7 +875,10 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
     }
 
     const int c = c0 + cl;
-    if (c >= P.W) return;
+    if (c >= P.W) {
+        pdl_trigger();
+        return;
+    }
     const float* epi = smem + P.nbuf * NA * P.slot;
 #pragma unroll
     for (int j = 0; j < PIX; ++j) {
@@ -888,13 +897,16 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
                                P.n_epi > 3 ? epi[3 * TR * TC + e] : 0.f);
         }
     }
+    pdl_trigger();
 }
 
 __global__ void epilogue_kernel(const float* g, size_t n, pt_step_epilogue ep)
 {
+    pdl_wait();
     for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
          p += (size_t)gridDim.x * blockDim.x)
         step_epilogue(ep, p, g ? g[p] : 0.f);  // g == null: a zero gradient difference
+    pdl_trigger();
 }
 
 static constexpr int kNT = 256, kNA = 32;
@@ -911,7 +923,8 @@ static int run_gather_t(pt_plan* plan, const AdjArgs& a, cudaStream_t st)
         attr = smem;
     }
     dim3 grid((plan->W + TC - 1) / TC, (plan->H + TR - 1) / TR, plan->Z);
-    adj_gather_kernel<TR, TC, kNT, kNA, TWO><<<grid, kNT, smem, st>>>(a);
+    PT_CHECK_CUDA(launch_pdl(adj_gather_kernel<TR, TC, kNT, kNA, TWO>, grid, dim3(kNT), smem, st,
+                             a));
     PT_CHECK_LAUNCH();
     return PT_OK;
 }
@@ -964,7 +977,7 @@ int launch_epilogue(pt_plan* plan, const float* g, const pt_step_epilogue* ep, c
 {
     const size_t n = (size_t)plan->Z * plan->H * plan->W;
     const int blocks = (int)std::min<size_t>((n + 255) / 256, (size_t)plan->sm_count * 8);
-    epilogue_kernel<<<blocks, 256, 0, st>>>(g, n, *ep);
+    PT_CHECK_CUDA(launch_pdl(epilogue_kernel, dim3(blocks), dim3(256), 0, st, g, n, *ep));
     PT_CHECK_LAUNCH();
     return PT_OK;
 }

@@ -52,6 +52,38 @@ extern std::atomic<long long> g_launches;  // kernels launched by this library
         PT_CHECK_CUDA(cudaGetLastError()); \
     } while (0)
 
+// Programmatic dependent launch (PDL).  The solver's kernels are launched
+// with programmatic stream serialisation: a kernel may start while its
+// predecessor drains, runs only predecessor-independent prologue work, then
+// pdl_wait() (griddepcontrol.wait: the predecessor grid has completed and its
+// writes are visible).  Every such kernel calls pdl_trigger() only after its
+// last global write, so when kernel N+1 is released, kernels <= N-1 are
+// complete -- N+1's prologue may read their outputs, never kernel N's.
+// Kernels launched without the attribute see both as no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger()
+{
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 }  // namespace pt
 
 struct pt_selection {
