@@ -528,6 +528,7 @@ __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
         }
         __syncthreads();
     }
+    pdl_wait();  // the dual sets are the predecessor's output
     // plane p (local; -1 / Zl are ghosts) into stage s
     auto stage = [&](int p, int s) {
         const uint32_t sb = fsm_u32 + (uint32_t)(s * T::STAGE) * 4u;
@@ -714,6 +715,7 @@ __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
         }
     }
     if (!TMA) asm volatile("cp.async.wait_group 0;");
+    pdl_trigger();
 }
 
 // caller duals (three [Zl][H][W] arrays) -> interiors of the P and R sets
@@ -736,6 +738,7 @@ __global__ void fgp3d_final_kernel(Fgp3Args a, float* p_out, float* q_out, float
                                    float* x_out, const float* xhat, float* h, float pog,
                                    long long iteration, long long* bad_iter)
 {
+    pdl_wait();
     const int H = a.H, W = a.W;
     const size_t HW = (size_t)H * W, n = (size_t)a.Zl * HW;
     for (size_t o = (size_t)blockIdx.x * blockDim.x + threadIdx.x; o < n;
@@ -761,6 +764,7 @@ __global__ void fgp3d_final_kernel(Fgp3Args a, float* p_out, float* q_out, float
         w_out[o] = wc;
         if (!isfinite(xv) && bad_iter) atomicMin(bad_iter, iteration);
     }
+    pdl_trigger();
 }
 
 int64_t fgp3d_slab_floats(int Zl, int H, int W)
@@ -893,7 +897,8 @@ static int fgp3d_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
     // 8 -> 155 us, 16 -> 153 us, 32 -> 165 us, 64 -> 189 us per iteration
     a.zchunk = zc_env ? zc_env : 16;
     dim3 grid(gx, gy, (a.Zl + a.zchunk - 1) / a.zchunk);
-    fgp3d_iter_kernel<TX, TY, NS, TMA, PQ><<<grid, T::NT, smem, st>>>(a, m);
+    PT_CHECK_CUDA(launch_pdl(fgp3d_iter_kernel<TX, TY, NS, TMA, PQ>, grid, dim3(T::NT), smem, st,
+                             a, m));
     PT_CHECK_LAUNCH();
     return PT_OK;
 }
@@ -993,9 +998,9 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
         a.nonneg = nonneg;
         const size_t n = (size_t)Zl * H * W;
         const int blocks = (int)std::min<size_t>((n + 255) / 256, (size_t)sm_count * 16);
-        fgp3d_final_kernel<<<blocks, 256, 0, st>>>(a, sl[g].p, sl[g].q, sl[g].w, sl[g].x_out,
-                                                   sl[g].xhat, sl[g].h, pog,
-                                                   (long long)iteration, (long long*)bad_iter);
+        PT_CHECK_CUDA(launch_pdl(fgp3d_final_kernel, dim3(blocks), dim3(256), 0, st, a, sl[g].p,
+                                 sl[g].q, sl[g].w, sl[g].x_out, sl[g].xhat, sl[g].h, pog,
+                                 (long long)iteration, (long long*)bad_iter));
         PT_CHECK_LAUNCH();
     }
     return PT_OK;
