@@ -163,12 +163,14 @@ __device__ __forceinline__ bool item_valid(const FwdArgs& P, const FwdItem& it, 
     return hi > lo;
 }
 
+// Threads [t0, t0 + nthr) (whole warps) copy the tile.
 template <int TY, int TX, int NT>
-__device__ __forceinline__ void stage_tile(const FwdArgs& P, const FwdItem& it, uint32_t buf)
+__device__ __forceinline__ void stage_tile(const FwdArgs& P, const FwdItem& it, uint32_t buf,
+                                           int t0, int nthr)
 {
     using T = FwdTile<TY, TX>;
-    constexpr int NW = NT / 32;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int NW = nthr >> 5;
+    const int warp = (threadIdx.x - t0) >> 5, lane = threadIdx.x & 31;
     const int s0 = it.band * TY;
     const int lane_org = it.tile * TX - T::HL;
     const float* img = P.x + (size_t)it.z * P.H * P.W;
@@ -176,7 +178,7 @@ __device__ __forceinline__ void stage_tile(const FwdArgs& P, const FwdItem& it, 
         // [st][ll] = img[s0 + st][lane_org + ll]: 16-byte copies (lane_org and
         // W are multiples of 4), zero-filled outside the image
         constexpr int NQ = T::NL / 4;
-        for (int idx = threadIdx.x; idx < TY * NQ; idx += NT) {
+        for (int idx = threadIdx.x - t0; idx < TY * NQ; idx += nthr) {
             const int st = idx / NQ, qq = idx - st * NQ;
             const int r = s0 + st, c = lane_org + 4 * qq;
             const int nvalid = (r < P.H && c >= 0) ? max(0, min(4, P.W - c)) : 0;
@@ -283,9 +285,14 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
     const FwdItem it = decode_item(P, blockIdx.x);
     if (!item_valid(P, it, TY, TX)) return;
     const uint32_t tile_u32 = smem_u32(sm);
-    pdl_wait();  // the image is the predecessor's output
-    stage_tile<TY, TX, NT>(P, it, tile_u32);
-    cp_async_commit();
+    // warp 0 builds the first chunk's ray tables (static data) while the
+    // predecessor drains; the other warps wait for it and stage the image tile
+    const bool stager = tid >= 32;
+    if (stager) {
+        pdl_wait();  // the image is the predecessor's output
+        stage_tile<TY, TX, NT>(P, it, tile_u32, 32, NT - 32);
+        cp_async_commit();
+    }
 
     const int branch = it.branch;
     const int n_steps = branch ? P.W : P.H;
@@ -350,7 +357,8 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
             if (tid == 0) s_pref[0] = 0;
         }
         if (!waited) {
-            cp_async_wait_all();
+            if (stager) cp_async_wait_all();
+            else pdl_wait();
             waited = true;
         }
         __syncthreads();
