@@ -677,6 +677,7 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
     __shared__ float4 s_p4[2][NA];
     __shared__ float2 s_p2[2][NA];
     __shared__ int s_off[2][NA];
+    __shared__ int s_bb[2][NA];
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -719,14 +720,16 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
 
     // per-chunk preparation: angle parameters in the tile frame (float64 ->
     // float32) and the touched sinogram bins (cp.async, zero outside [0, B))
-    auto prepare = [&](int kb, int buf) {
+    // per-chunk preparation, split so the chunk's tile-frame parameters
+    // (static data) can be formed before the PDL wait and only the staging of
+    // the residual bins (the predecessor's output) after it.  One warp per
+    // angle: every lane evaluates the parameters (float64 -> float32,
+    // identical across lanes), lane 0 publishes them, the same warp's lanes
+    // later stage the touched bins -- no CTA barrier.
+    auto prepare_params = [&](int kb, int buf) {
         const int nc = min(NA, P.n_sel - kb);
-        // one warp per angle: every lane evaluates the angle's tile-frame
-        // parameters (float64 -> float32, identical across lanes), lane 0
-        // publishes them, the lanes stage the touched bins -- no CTA barrier
         for (int a = warp; a < nc; a += NW) {
-            const int k = kb + a;
-            const AngleTab& t = P.tab[P.sel_angle[k]];
+            const AngleTab& t = P.tab[P.sel_angle[kb + a]];
             const double gbr = t.gbr, gbc = t.gbc;
             // crossing bin b_f(r, c) = gbr r + gbc c + gg (pos(b_f) == lane)
             const double bf00 = gbr * r0 + gbc * c0 + t.gg;
@@ -747,7 +750,16 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
                                     (uint32_t)kMagicBits * 4u;
                 s_p2[buf][a] = make_float2(stp, __uint_as_float(ya));
                 s_off[buf][a] = shift - jlo;
+                s_bb[buf][a] = bb;
             }
+        }
+    };
+    auto prepare_stage = [&](int kb, int buf) {
+        const int nc = min(NA, P.n_sel - kb);
+        __syncwarp();  // this warp's lane 0 published s_bb
+        for (int a = warp; a < nc; a += NW) {
+            const int k = kb + a;
+            const int bb = s_bb[buf][a];
             const float* yrow = P.y + ((size_t)k * P.Z + z) * P.B;
             const uint32_t dst = stage_u32 + (uint32_t)((buf * NA + a) * P.slot) * 4u;
             if (P.vec) {
@@ -767,6 +779,10 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
         }
         cp_async_commit();
     };
+    auto prepare = [&](int kb, int buf) {
+        prepare_params(kb, buf);
+        prepare_stage(kb, buf);
+    };
 
     float acc_o[PIX];
 #pragma unroll
@@ -779,8 +795,9 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
     const f2 mg2 = pk(kMagic, kMagic);
 
     const int n_chunks = (P.n_sel + NA - 1) / NA;
+    if (n_chunks > 0) prepare_params(0, 0);
     pdl_wait();  // the residual rows are the predecessor's output
-    if (n_chunks > 0) prepare(0, 0);
+    if (n_chunks > 0) prepare_stage(0, 0);
     for (int ci = 0; ci < n_chunks; ++ci) {
         const int buf = (P.nbuf == 2) ? (ci & 1) : 0;
         const int kb = ci * NA;
