@@ -45,6 +45,22 @@ bool pdl_enabled()
     return on;
 }
 
+int ensure_smem(const void* kernel, size_t bytes)
+{
+    if (bytes <= 48 * 1024) return PT_OK;
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    int dev = 0;
+    PT_CHECK_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& have = done[{kernel, dev}];
+    if (have >= bytes) return PT_OK;
+    PT_CHECK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)bytes));
+    have = bytes;
+    return PT_OK;
+}
+
 int workspace_alloc(const pt_plan* plan, Workspace* ws)
 {
     workspace_sizes(plan, &ws->partial_floats, &ws->red_doubles, &ws->image_floats);

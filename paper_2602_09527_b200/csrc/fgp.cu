@@ -867,11 +867,9 @@ static int fgp3d_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
 {
     using T = Fgp3Tile<TX, TY, NS, PQ>;
     const size_t smem = (size_t)T::SMEM_FLOATS * 4;
-    static bool attr = false;
-    if (!attr) {
-        PT_CHECK_CUDA(cudaFuncSetAttribute(fgp3d_iter_kernel<TX, TY, NS, TMA, PQ>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
+    {
+        const int rc = ensure_smem((const void*)fgp3d_iter_kernel<TX, TY, NS, TMA, PQ>, smem);
+        if (rc) return rc;
     }
     Fgp3Maps m;
     memset(&m, 0, sizeof(m));

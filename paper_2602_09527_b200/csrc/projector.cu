@@ -470,11 +470,9 @@ static int run_forward_cfg(pt_plan* plan, Workspace* ws, const pt_selection* sel
                            double* sumsq, cudaStream_t st, const float* data2)
 {
     using T = FwdTile<TY, TX>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        PT_CHECK_CUDA(cudaFuncSetAttribute(fwd_band_kernel<TY, TX, NT, MINB>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM));
-        attr_set = true;
+    {
+        const int rc = ensure_smem((const void*)fwd_band_kernel<TY, TX, NT, MINB>, T::SMEM);
+        if (rc) return rc;
     }
     if (x2) {
         // A (x - x2): difference image first (standalone API path; the solver
@@ -940,12 +938,9 @@ template <int TR, int TC, bool TWO>
 static int run_gather_t(pt_plan* plan, const AdjArgs& a, cudaStream_t st)
 {
     const size_t smem = (size_t)(a.nbuf * kNA * a.slot + a.n_epi * TR * TC) * sizeof(float);
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
-        PT_CHECK_CUDA(cudaFuncSetAttribute(adj_gather_kernel<TR, TC, kNT, kNA, TWO>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem));
-        attr = smem;
+    {
+        const int rc = ensure_smem((const void*)adj_gather_kernel<TR, TC, kNT, kNA, TWO>, smem);
+        if (rc) return rc;
     }
     dim3 grid((plan->W + TC - 1) / TC, (plan->H + TR - 1) / TR, plan->Z);
     PT_CHECK_CUDA(launch_pdl(adj_gather_kernel<TR, TC, kNT, kNA, TWO>, grid, dim3(kNT), smem, st,

@@ -67,6 +67,10 @@ __device__ __forceinline__ void pdl_trigger()
 }
 bool pdl_enabled();
 
+// Raise a kernel's dynamic shared-memory limit to `bytes` on the current
+// device (once per (kernel, device, size); thread-safe, multi-device safe).
+int ensure_smem(const void* kernel, size_t bytes);
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                        cudaStream_t st, Args... args)
