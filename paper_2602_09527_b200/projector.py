@@ -113,8 +113,10 @@ _plans_lock = threading.Lock()
 
 
 def get_plan(geometry: ParallelGeometry, width: int, height: int, n_slices: int = 1) -> Plan:
-    """lru_cache(maxsize=8) over (geometry, grid), like projector.py:100-102."""
-    key = (geometry, int(width), int(height), int(n_slices))
+    """lru_cache(maxsize=8) over (geometry, grid), like projector.py:100-102;
+    plans hold device tables, so the current CUDA device is part of the key."""
+    device = torch.cuda.current_device() if torch.cuda.is_available() else -1
+    key = (geometry, int(width), int(height), int(n_slices), device)
     with _plans_lock:
         plan = _plans.get(key)
         if plan is not None:
