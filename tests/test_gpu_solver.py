@@ -322,3 +322,40 @@ def test_zslab_nccl_on_one_rank_is_bitwise_identical():
         assert a.iterations == b.iterations
     finally:
         dist.destroy_process_group()
+
+
+_PDL_SNIPPET = r"""
+import sys, numpy as np
+sys.path.insert(0, {repo!r})
+from paper_2602_09527_b200 import (ParallelGeometry, Projector, SolverConfig, TomoProblem,
+                                   TvProxConfig, default_gamma, problems, run)
+g = ParallelGeometry.uniform(120, 181)
+proj = Projector(g, 128, 128)
+x = problems.ellipse_phantom(128, 6, 1)
+b = proj.forward(x).double().cpu().numpy() + 0.01 * np.random.default_rng(1).standard_normal((120, 181))
+lip = proj.norm_sq(20, 0)
+out = []
+for est in ("svrg", "saga", "full"):
+    cfg = SolverConfig(gamma=default_gamma(est, lip), skip_probability=0.3,
+                       n_subsets=10 if est != "full" else 1, estimator=est,
+                       max_data_passes=9, seed=2)
+    out.append(run(cfg, TomoProblem(proj, b, tv=TvProxConfig(alpha=0.05, inner_iterations=20))).image.cpu().numpy())
+np.save(sys.argv[1], np.stack(out))
+"""
+
+
+def test_programmatic_dependent_launch_is_bitwise_neutral(tmp_path):
+    """Overlapping kernel prologues with the predecessor's drain (PDL) must not
+    change a single bit of the trajectory (PT_PDL=0 launches serially)."""
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0", "1"):
+        path = tmp_path / f"pdl{flag}_{len(outs)}.npy"
+        env = dict(os.environ, PT_PDL=flag)
+        subprocess.run([sys.executable, "-c", _PDL_SNIPPET.format(repo=repo), str(path)],
+                       check=True, env=env, timeout=300)
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
