@@ -105,7 +105,6 @@ struct FwdArgs {
     int32_t n_groups;
     int32_t n_bands;  // bands per slice (max over branches)
     int32_t n_tiles;  // lane tiles (max over branches)
-    int32_t n_items;
 };
 
 template <int TY, int TX>
@@ -136,18 +135,23 @@ struct FwdItem {
     int z, branch, band, tile, group;
 };
 
-__device__ __forceinline__ FwdItem decode_item(const FwdArgs& P, int item)
+// grid = (tile, band + n_bands * group, branch + 2 * z): one runtime division
+__device__ __forceinline__ FwdItem decode_item(const FwdArgs& P)
 {
     FwdItem it;
-    it.tile = item % P.n_tiles;
-    int t = item / P.n_tiles;
-    it.band = t % P.n_bands;
-    t /= P.n_bands;
-    it.group = t % P.n_groups;
-    t /= P.n_groups;
-    it.branch = t & 1;
-    it.z = t >> 1;
+    it.tile = blockIdx.x;
+    it.group = blockIdx.y / (unsigned)P.n_bands;
+    it.band = blockIdx.y - it.group * P.n_bands;
+    it.branch = blockIdx.z & 1;
+    it.z = blockIdx.z >> 1;
     return it;
+}
+
+// [lo, hi) of the group's angles within the branch list (nb * n_groups < 2^31
+// is checked on the host)
+__device__ __forceinline__ int group_begin(int nb, int group, int n_groups)
+{
+    return (int)((unsigned)(nb * group) / (unsigned)n_groups);
 }
 
 // true when the item has work (band / tile inside the branch's extent, angles in the group)
@@ -156,11 +160,8 @@ __device__ __forceinline__ bool item_valid(const FwdArgs& P, const FwdItem& it, 
     const int n_steps = it.branch ? P.W : P.H;
     const int n_lanes = it.branch ? P.H : P.W;
     if (it.band * TY >= n_steps || it.tile * TX >= n_lanes) return false;
-    const int bb = it.branch ? P.bbeg[1] : P.bbeg[0];
-    const int nb = (it.branch ? P.bend[1] : P.bend[0]) - bb;
-    const long long lo = (long long)nb * it.group / P.n_groups;
-    const long long hi = (long long)nb * (it.group + 1) / P.n_groups;
-    return hi > lo;
+    const int nb = it.branch ? P.bend[1] - P.bbeg[1] : P.bend[0] - P.bbeg[0];
+    return group_begin(nb, it.group + 1, P.n_groups) > group_begin(nb, it.group, P.n_groups);
 }
 
 // Threads [t0, t0 + nthr) (whole warps) copy the tile.
@@ -178,12 +179,17 @@ __device__ __forceinline__ void stage_tile(const FwdArgs& P, const FwdItem& it, 
         // [st][ll] = img[s0 + st][lane_org + ll]: 16-byte copies (lane_org and
         // W are multiples of 4), zero-filled outside the image
         constexpr int NQ = T::NL / 4;
-        for (int idx = threadIdx.x - t0; idx < TY * NQ; idx += nthr) {
-            const int st = idx / NQ, qq = idx - st * NQ;
+        const int i0 = threadIdx.x - t0;
+        int st = i0 / NQ, qq = i0 - st * NQ;
+        const int dst_ = nthr / NQ, dq = nthr - dst_ * NQ;
+        while (st < TY) {
             const int r = s0 + st, c = lane_org + 4 * qq;
-            const int nvalid = (r < P.H && c >= 0) ? max(0, min(4, P.W - c)) : 0;
+            const bool ok = r < P.H && c >= 0 && c < P.W;  // whole 4-lane chunks
             cp_async16(buf + (uint32_t)(st * T::PITCH_R + 4 * qq) * 4u,
-                       img + (nvalid ? (size_t)r * P.W + c : 0), 4 * nvalid);
+                       img + (ok ? r * P.W + c : 0), ok ? 16 : 0);
+            st += dst_;
+            qq += dq;
+            if (qq >= NQ) { qq -= NQ; ++st; }
         }
     } else if (it.branch == 0) {
         // [st][ll] = img[s0 + st][lane_org + ll]: a warp per tile row
@@ -201,15 +207,17 @@ __device__ __forceinline__ void stage_tile(const FwdArgs& P, const FwdItem& it, 
         }
     } else {
         // [ll][st] = img[lane_org + ll][s0 + st]: a warp per image-row segment
+        const int nst = min(TY, P.W - s0);  // steps inside the image
+        const int r_lo = max(0, -lane_org), r_hi = min(T::NL, P.H - lane_org);
         for (int ll = warp; ll < T::NL; ll += NW) {
-            const int r = lane_org + ll;
-            const bool rin = r >= 0 && r < P.H;
-            const float* src = img + (size_t)(rin ? r : 0) * P.W + s0;
-            const uint32_t dst = buf + (uint32_t)(ll * T::PITCH_C) * 4u;
+            const bool rin = ll >= r_lo && ll < r_hi;
+            const float* src = img + (rin ? (lane_org + ll) * P.W + s0 : 0);
+            const uint32_t dst = buf + (uint32_t)(ll * T::PITCH_C + lane) * 4u;
 #pragma unroll
-            for (int st = lane; st < TY; st += 32) {
-                const bool ok = rin && s0 + st < P.W;
-                cp_async4(dst + (uint32_t)st * 4u, src + (ok ? st : 0), ok);
+            for (int u = 0; u < (TY + 31) / 32; ++u) {
+                if (TY % 32 != 0 && lane + 32 * u >= TY) break;
+                const bool ok = rin && lane + 32 * u < nst;
+                cp_async4(dst + 128u * u, src + (ok ? lane + 32 * u : 0), ok);
             }
         }
     }
@@ -282,7 +290,7 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
     __shared__ float* s_out[CH];    // partial of ray blo in this band
 
     const int tid = threadIdx.x;
-    const FwdItem it = decode_item(P, blockIdx.x);
+    const FwdItem it = decode_item(P);
     if (!item_valid(P, it, TY, TX)) return;
     const uint32_t tile_u32 = smem_u32(sm);
     // warp 0 builds the first chunk's ray tables (static data) while the
@@ -303,8 +311,8 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
     const int ty_valid = min(TY, n_steps - s0);
     const int bb = branch ? P.bbeg[1] : P.bbeg[0];
     const int nb = (branch ? P.bend[1] : P.bend[0]) - bb;
-    const int a_begin = bb + (int)(((long long)nb * it.group) / P.n_groups);
-    const int a_end = bb + (int)(((long long)nb * (it.group + 1)) / P.n_groups);
+    const int a_begin = bb + group_begin(nb, it.group, P.n_groups);
+    const int a_end = bb + group_begin(nb, it.group + 1, P.n_groups);
     const int32_t* bpos = branch ? P.bpos1 : P.bpos0;
     const bool first_tile = (l0 == 0);
     const bool last_tile = (l0 + TX >= n_lanes);
@@ -539,11 +547,15 @@ static int run_forward_cfg(pt_plan* plan, Workspace* ws, const pt_selection* sel
         long long groups = (slots * waves + base_items - 1) / base_items;
         groups = std::max(1LL, std::min<long long>(groups, std::max(1, max_branch / 2)));
         a.n_groups = (int)groups;
-        a.n_items = (int)std::min<long long>((long long)n_tiles * n_bands * plan->Z * 2 * groups,
-                                             (long long)INT32_MAX);
+        if ((long long)max_branch * (groups + 1) >= INT32_MAX ||
+            (long long)n_bands * groups > 65535 || 2LL * plan->Z > 65535) {
+            set_error("forward launch grid out of range");
+            return PT_EINVAL;
+        }
+        const dim3 grid(n_tiles, (unsigned)(n_bands * groups), 2 * plan->Z);
         {
             ProfScope ps(ws, PT_PROF_FWD_BAND, st);
-            PT_CHECK_CUDA(launch_pdl(fwd_band_kernel<TY, TX, NT, MINB>, dim3(a.n_items), dim3(NT),
+            PT_CHECK_CUDA(launch_pdl(fwd_band_kernel<TY, TX, NT, MINB>, grid, dim3(NT),
                                      (size_t)T::SMEM, st, a));
             PT_CHECK_LAUNCH();
         }
