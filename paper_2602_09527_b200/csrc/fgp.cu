@@ -54,23 +54,22 @@ struct FgpArgs {
 
 // One FGP inner iteration on the register strips.  EDGE = the region touches
 // the image border (masks needed); interior regions skip every boundary test.
-template <int RW, int RH, int STRIP, bool EDGE>
+template <int RW, int RH, int STRIP, bool EDGE, bool NONNEG>
 __device__ __forceinline__ void fgp2d_iteration(
     float (&v)[STRIP], float (&p)[STRIP], float (&q)[STRIP], float (&r)[STRIP],
-    float (&s)[STRIP], float (&u)[STRIP], float (*S_s)[RW + 1], float (*S_u)[RW + 1],
+    float (&s)[STRIP], float (&u)[STRIP], float (*S_s)[RW + 2], float (*S_u)[RW + 2],
     float (*S_r)[RW], float (*S_ut)[RW], int tx, int ty, int i0, int H, bool not_last_col,
-    unsigned in_mask, float lam, float eta, float beta, int nonneg)
+    unsigned in_mask, float lam, float eta, float beta)
 {
-    constexpr int NS = RH / STRIP;
     const int row0 = ty * STRIP;
 #pragma unroll
-    for (int k = 0; k < STRIP; ++k) S_s[row0 + k][tx] = s[k];
-    S_r[ty][tx] = r[STRIP - 1];
+    for (int k = 0; k < STRIP; ++k) S_s[row0 + k][tx + 1] = s[k];
+    S_r[ty + 1][tx] = r[STRIP - 1];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < STRIP; ++k) {
-        const float r_up = k ? r[k - 1] : (ty ? S_r[ty - 1][tx] : 0.f);
-        const float s_left = tx ? S_s[row0 + k][tx - 1] : 0.f;
+        const float r_up = k ? r[k - 1] : S_r[ty][tx];
+        const float s_left = S_s[row0 + k][tx];
         // _diff_adjoint (regularizers.py:70-76), numpy statement order
         float o;
         if (EDGE) {
@@ -85,17 +84,17 @@ __device__ __forceinline__ void fgp2d_iteration(
         }
         o += s_left;
         float uu = v[k] - lam * o;
-        if (nonneg) uu = (uu < 0.f) ? 0.f : uu;
+        if (NONNEG) uu = (uu < 0.f) ? 0.f : uu;
         if (EDGE) uu = ((in_mask >> k) & 1u) ? uu : 0.f;
         u[k] = uu;
-        S_u[row0 + k][tx] = uu;
+        S_u[row0 + k][tx + 1] = uu;
     }
     S_ut[ty][tx] = u[0];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < STRIP; ++k) {
-        const float u_down = (k < STRIP - 1) ? u[k + 1] : (ty < NS - 1 ? S_ut[ty + 1][tx] : 0.f);
-        const float u_right = (tx < RW - 1) ? S_u[row0 + k][tx + 1] : 0.f;
+        const float u_down = (k < STRIP - 1) ? u[k + 1] : S_ut[ty + 1][tx];
+        const float u_right = S_u[row0 + k][tx + 2];
         float gv = u_down - u[k], gh = u_right - u[k];
         if (EDGE) {
             const int gi = i0 + row0 + k;
@@ -146,45 +145,42 @@ __device__ __forceinline__ void st2(float2* p, f2 v)
     asm volatile("st.shared.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "l"(v.v));
 }
 
-template <int RW, int RH, int STRIP>
+template <int RW, int RH, int STRIP, bool NONNEG>
 __device__ __forceinline__ void fgp2d_iteration_packed(
     f2 (&V)[STRIP / 2], f2 (&Pp)[STRIP / 2], f2 (&Q)[STRIP / 2], f2 (&R)[STRIP / 2],
-    f2 (&S)[STRIP / 2], f2 (&U)[STRIP / 2], float2 (*S_s2)[RW + 1], float2 (*S_u2)[RW + 1],
-    float (*S_r)[RW], float (*S_ut)[RW], int tx, int ty, float lam, float eta, float beta,
-    int nonneg)
+    f2 (&S)[STRIP / 2], f2 (&U)[STRIP / 2], float2 (*S_s2)[RW + 2], float2 (*S_u2)[RW + 2],
+    float (*S_r)[RW], float (*S_ut)[RW], int tx, int ty, float lam, float eta, float beta)
 {
-    constexpr int NS = RH / STRIP;
     constexpr int H2 = STRIP / 2;
     const int prow0 = ty * H2;
     const f2 nlam2 = pk(-lam, -lam), eta2 = pk(eta, eta), beta2 = pk(beta, beta);
-    const f2 zero2 = pk(0.f, 0.f);
 #pragma unroll
-    for (int j = 0; j < H2; ++j) st2(&S_s2[prow0 + j][tx], S[j]);
-    S_r[ty][tx] = hi_of(R[H2 - 1]);
+    for (int j = 0; j < H2; ++j) st2(&S_s2[prow0 + j][tx + 1], S[j]);
+    S_r[ty + 1][tx] = hi_of(R[H2 - 1]);
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < H2; ++j) {
-        const f2 r_up = j ? R[j - 1] : pk(ty ? S_r[ty - 1][tx] : 0.f, lo_of(R[H2 - 1]));
-        const f2 s_left = tx ? ld2(&S_s2[prow0 + j][tx - 1]) : zero2;
+        // zero padding (row 0 of S_r, column 0 of S_s2) stands for the region edge
+        const f2 r_up = j ? R[j - 1] : pk(S_r[ty][tx], lo_of(R[H2 - 1]));
+        const f2 s_left = ld2(&S_s2[prow0 + j][tx]);
         // _diff_adjoint (regularizers.py:70-76): ((-r + r_up) - s) + s_left
         const f2 o = add2(sub2(sub2(r_up, R[j]), S[j]), s_left);
         f2 u = fma2(nlam2, o, V[j]);
-        if (nonneg) {
+        if (NONNEG) {
             float ua, ub;
             upk(u, ua, ub);
             u = pk(max_nan(ua, 0.f), max_nan(ub, 0.f));  // NaN propagates
         }
         U[j] = u;
-        st2(&S_u2[prow0 + j][tx], u);
+        st2(&S_u2[prow0 + j][tx + 1], u);
     }
     S_ut[ty][tx] = lo_of(U[0]);
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < H2; ++j) {
         // rows (j+1, j+1+H2); for the last pair: (pair 0 hi, next strip's first row)
-        const f2 u_down = (j < H2 - 1) ? U[j + 1]
-                                       : pk(hi_of(U[0]), ty < NS - 1 ? S_ut[ty + 1][tx] : 0.f);
-        const f2 u_right = (tx < RW - 1) ? ld2(&S_u2[prow0 + j][tx + 1]) : zero2;
+        const f2 u_down = (j < H2 - 1) ? U[j + 1] : pk(hi_of(U[0]), S_ut[ty + 1][tx]);
+        const f2 u_right = ld2(&S_u2[prow0 + j][tx + 2]);
         const f2 gv = sub2(u_down, U[j]);
         const f2 gh = sub2(u_right, U[j]);
         const f2 ph = fma2(eta2, gv, R[j]);
@@ -202,20 +198,23 @@ __device__ __forceinline__ void fgp2d_iteration_packed(
     }
 }
 
-template <int RW, int RH, int STRIP>
+template <int RW, int RH, int STRIP, bool NONNEG>
 __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
 {
-    pdl_wait();
-    constexpr int H2 = STRIP / 2;
-    // the scalar (edge / epilogue) and the pair (interior) exchange planes
-    // share one buffer: a CTA uses one layout at a time
-    __shared__ __align__(16) float S_buf[2 * RH * (RW + 1)];
-    float (*S_s)[RW + 1] = reinterpret_cast<float (*)[RW + 1]>(S_buf);
-    float (*S_u)[RW + 1] = reinterpret_cast<float (*)[RW + 1]>(S_buf + RH * (RW + 1));
-    float2 (*S_s2)[RW + 1] = reinterpret_cast<float2 (*)[RW + 1]>(S_buf);
-    float2 (*S_u2)[RW + 1] = reinterpret_cast<float2 (*)[RW + 1]>(S_buf + RH * (RW + 1));
-    __shared__ float S_r[RH / STRIP][RW];
-    __shared__ float S_ut[RH / STRIP][RW];
+    constexpr int H2 = STRIP / 2, NS = RH / STRIP, PW = RW + 2;
+    // exchange planes, pitch RW + 2: a thread's column at tx + 1, columns 0 and
+    // RW + 1 hold zeros (the region edge).  The scalar (edge / epilogue) and the
+    // pair (interior) layouts share one buffer; a CTA uses one at a time and
+    // re-zeroes the padding when it switches.
+    __shared__ __align__(16) float S_buf[2 * RH * PW];
+    float (*S_s)[PW] = reinterpret_cast<float (*)[PW]>(S_buf);
+    float (*S_u)[PW] = reinterpret_cast<float (*)[PW]>(S_buf + RH * PW);
+    float2 (*S_s2)[PW] = reinterpret_cast<float2 (*)[PW]>(S_buf);
+    float2 (*S_u2)[PW] = reinterpret_cast<float2 (*)[PW]>(S_buf + RH * PW);
+    // strip-end rows: S_r row ty + 1 = last r of strip ty (row 0 zero),
+    // S_ut row ty = first u of strip ty (row NS zero)
+    __shared__ float S_r[NS + 1][RW];
+    __shared__ float S_ut[NS + 1][RW];
 
     const int tid = threadIdx.x;
     const int tx = tid % RW;
@@ -230,44 +229,101 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
     // the whole region, and one point beyond it, strictly inside the image
     const bool edge = !(i0 >= 0 && j0 >= 0 && i0 + RH < P.H && j0 + RW < P.W);
 
+    auto zero_pads = [&](bool packed) {
+        // rows of the active layout: RH scalar rows or RH / 2 pair rows, 2 planes
+        const int rows = packed ? RH / 2 : RH;
+        for (int i = tid; i < 4 * rows; i += RW * NS) {
+            const int plane = i / (2 * rows), rr = (i >> 1) % rows, side = i & 1;
+            float* base = S_buf + plane * RH * PW;
+            if (packed) {
+                float2* row = reinterpret_cast<float2*>(base) + rr * PW;
+                row[side ? RW + 1 : 0] = make_float2(0.f, 0.f);
+            } else {
+                base[rr * PW + (side ? RW + 1 : 0)] = 0.f;
+            }
+        }
+    };
+    zero_pads(!edge);
+    if (tid < RW) {
+        S_r[0][tid] = 0.f;
+        S_ut[NS][tid] = 0.f;
+    }
+
+    pdl_wait();
     // packed state: pair j = strip rows (j, j + H2)
     f2 V[H2], Pp[H2], Q[H2], R[H2], S[H2], U[H2];
     unsigned in_mask = 0;
+    if (!edge) {
+        // every point inside the image: unpredicated loads, all in flight
+        in_mask = (1u << STRIP) - 1u;
+        const size_t base = (size_t)(i0 + row0) * P.W + gj;
+        const size_t W = P.W;
+        float vv[STRIP], pv[STRIP], qv[STRIP], rv[STRIP], sv[STRIP];
 #pragma unroll
-    for (int j = 0; j < H2; ++j) {
-        float vv[2], pv[2], qv[2], rv[2], sv[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int k = j + h * H2;
-            const int gi = i0 + row0 + k;
-            const bool in = col_in && gi >= 0 && gi < P.H;
-            if (in) in_mask |= 1u << k;
-            const size_t o = in ? (size_t)gi * P.W + gj : 0;
-            vv[h] = in ? P.v[o] : 0.f;
-            pv[h] = in ? P.p_in[o] : 0.f;
-            qv[h] = in ? P.q_in[o] : 0.f;
-            rv[h] = in ? (P.r_in ? P.r_in[o] : pv[h]) : 0.f;
-            sv[h] = in ? (P.s_in ? P.s_in[o] : qv[h]) : 0.f;
+        for (int k = 0; k < STRIP; ++k) {
+            vv[k] = P.v[base + k * W];
+            pv[k] = P.p_in[base + k * W];
+            qv[k] = P.q_in[base + k * W];
         }
-        V[j] = pk(vv[0], vv[1]);
-        Pp[j] = pk(pv[0], pv[1]);
-        Q[j] = pk(qv[0], qv[1]);
-        R[j] = pk(rv[0], rv[1]);
-        S[j] = pk(sv[0], sv[1]);
-        U[j] = pk(0.f, 0.f);
+        if (P.r_in) {
+#pragma unroll
+            for (int k = 0; k < STRIP; ++k) {
+                rv[k] = P.r_in[base + k * W];
+                sv[k] = P.s_in[base + k * W];
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < STRIP; ++k) {
+                rv[k] = pv[k];
+                sv[k] = qv[k];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < H2; ++j) {
+            V[j] = pk(vv[j], vv[j + H2]);
+            Pp[j] = pk(pv[j], pv[j + H2]);
+            Q[j] = pk(qv[j], qv[j + H2]);
+            R[j] = pk(rv[j], rv[j + H2]);
+            S[j] = pk(sv[j], sv[j + H2]);
+            U[j] = pk(0.f, 0.f);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < H2; ++j) {
+            float vv[2], pv[2], qv[2], rv[2], sv[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int k = j + h * H2;
+                const int gi = i0 + row0 + k;
+                const bool in = col_in && gi >= 0 && gi < P.H;
+                if (in) in_mask |= 1u << k;
+                const size_t o = in ? (size_t)gi * P.W + gj : 0;
+                vv[h] = in ? P.v[o] : 0.f;
+                pv[h] = in ? P.p_in[o] : 0.f;
+                qv[h] = in ? P.q_in[o] : 0.f;
+                rv[h] = in ? (P.r_in ? P.r_in[o] : pv[h]) : 0.f;
+                sv[h] = in ? (P.s_in ? P.s_in[o] : qv[h]) : 0.f;
+            }
+            V[j] = pk(vv[0], vv[1]);
+            Pp[j] = pk(pv[0], pv[1]);
+            Q[j] = pk(qv[0], qv[1]);
+            R[j] = pk(rv[0], rv[1]);
+            S[j] = pk(sv[0], sv[1]);
+            U[j] = pk(0.f, 0.f);
+        }
     }
     if (!edge) {
         // two iterations per trip: the compiler alternates register roles instead of moving
         int it = 0;
         for (; it + 1 < P.n_iter; it += 2) {
-            fgp2d_iteration_packed<RW, RH, STRIP>(V, Pp, Q, R, S, U, S_s2, S_u2, S_r, S_ut, tx, ty,
-                                                  P.lam, P.eta, P.beta[it], P.nonneg);
-            fgp2d_iteration_packed<RW, RH, STRIP>(V, Pp, Q, R, S, U, S_s2, S_u2, S_r, S_ut, tx, ty,
-                                                  P.lam, P.eta, P.beta[it + 1], P.nonneg);
+            fgp2d_iteration_packed<RW, RH, STRIP, NONNEG>(V, Pp, Q, R, S, U, S_s2, S_u2, S_r, S_ut,
+                                                          tx, ty, P.lam, P.eta, P.beta[it]);
+            fgp2d_iteration_packed<RW, RH, STRIP, NONNEG>(V, Pp, Q, R, S, U, S_s2, S_u2, S_r, S_ut,
+                                                          tx, ty, P.lam, P.eta, P.beta[it + 1]);
         }
         if (it < P.n_iter)
-            fgp2d_iteration_packed<RW, RH, STRIP>(V, Pp, Q, R, S, U, S_s2, S_u2, S_r, S_ut, tx, ty,
-                                                  P.lam, P.eta, P.beta[it], P.nonneg);
+            fgp2d_iteration_packed<RW, RH, STRIP, NONNEG>(V, Pp, Q, R, S, U, S_s2, S_u2, S_r, S_ut,
+                                                          tx, ty, P.lam, P.eta, P.beta[it]);
     }
     for (int it = 0; edge && it < P.n_iter; ++it) {
         {
@@ -281,9 +337,9 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
                 upk(S[j], s[j], s[j + H2]);
                 upk(U[j], u[j], u[j + H2]);
             }
-            fgp2d_iteration<RW, RH, STRIP, true>(v, p, q, r, s, u, S_s, S_u, S_r, S_ut, tx, ty, i0,
-                                                 P.H, not_last_col, in_mask, P.lam, P.eta,
-                                                 P.beta[it], P.nonneg);
+            fgp2d_iteration<RW, RH, STRIP, true, NONNEG>(v, p, q, r, s, u, S_s, S_u, S_r, S_ut, tx,
+                                                         ty, i0, P.H, not_last_col, in_mask, P.lam,
+                                                         P.eta, P.beta[it]);
 #pragma unroll
             for (int j = 0; j < H2; ++j) {
                 Pp[j] = pk(p[j], p[j + H2]);
@@ -304,29 +360,32 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
         upk(R[j], r[j], r[j + H2]);
         upk(S[j], s[j], s[j + H2]);
     }
-    const bool col_inner = tx >= P.halo && tx < RW - P.halo;
+    // exact points: the region minus its halo, inside the image
+    const bool col_inner = tx >= P.halo && tx < RW - P.halo && col_in;
+    const int k_lo = max(0, P.halo - row0), k_hi = min(STRIP, RH - P.halo - row0);
+    const size_t obase = (size_t)(i0 + row0) * P.W + gj;
     const float lam = P.lam;
     if (P.final_) {
         // x = max(v - lam D^T(p, q), 0), then the ProxSkip h update
         __syncthreads();
+        if (!edge) zero_pads(false);
 #pragma unroll
-        for (int k = 0; k < STRIP; ++k) S_s[row0 + k][tx] = q[k];
-        S_r[ty][tx] = p[STRIP - 1];
+        for (int k = 0; k < STRIP; ++k) S_s[row0 + k][tx + 1] = q[k];
+        S_r[ty + 1][tx] = p[STRIP - 1];
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < STRIP; ++k) {
-            const int li = row0 + k;
-            const int gi = i0 + li;
-            if (!col_inner || li < P.halo || li >= RH - P.halo || !((in_mask >> k) & 1u)) continue;
-            const float p_up = k ? p[k - 1] : (ty ? S_r[ty - 1][tx] : 0.f);
-            const float q_left = tx ? S_s[li][tx - 1] : 0.f;
+            const int gi = i0 + row0 + k;
+            if (!col_inner || k < k_lo || k >= k_hi || !((in_mask >> k) & 1u)) continue;
+            const float p_up = k ? p[k - 1] : S_r[ty][tx];
+            const float q_left = S_s[row0 + k][tx];
             float o = (gi < P.H - 1) ? -p[k] : 0.f;
             o += p_up;
             o = not_last_col ? o - q[k] : o;
             o += q_left;
             float x = v[k] - lam * o;
-            if (P.nonneg) x = (x < 0.f) ? 0.f : x;
-            const size_t idx = (size_t)gi * P.W + gj;
+            if (NONNEG) x = (x < 0.f) ? 0.f : x;
+            const size_t idx = obase + (size_t)k * P.W;
             P.x_out[idx] = x;
             P.p_out[idx] = p[k];
             P.q_out[idx] = q[k];
@@ -338,10 +397,8 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
     } else {
 #pragma unroll
         for (int k = 0; k < STRIP; ++k) {
-            const int li = row0 + k;
-            const int gi = i0 + li;
-            if (!col_inner || li < P.halo || li >= RH - P.halo || !((in_mask >> k) & 1u)) continue;
-            const size_t idx = (size_t)gi * P.W + gj;
+            if (!col_inner || k < k_lo || k >= k_hi || !((in_mask >> k) & 1u)) continue;
+            const size_t idx = obase + (size_t)k * P.W;
             P.p_out[idx] = p[k];
             P.q_out[idx] = q[k];
             P.r_out[idx] = r[k];
@@ -413,8 +470,9 @@ static int run_fgp2d(pt_plan* plan, const float* v, double lam, int inner, int n
         a.bad_iter = (long long*)bad_iter;
         const int IW = RW - 2 * a.halo, IH = RH - 2 * a.halo;
         dim3 grid((plan->W + IW - 1) / IW, (plan->H + IH - 1) / IH);
-        PT_CHECK_CUDA(launch_pdl(fgp2d_kernel<RW, RH, STRIP>, grid, dim3(RW * (RH / STRIP)), 0,
-                                 st, a));
+        PT_CHECK_CUDA(launch_pdl(nonneg ? fgp2d_kernel<RW, RH, STRIP, true>
+                                        : fgp2d_kernel<RW, RH, STRIP, false>,
+                                 grid, dim3(RW * (RH / STRIP)), 0, st, a));
         PT_CHECK_LAUNCH();
         if (!fin) {
             sp = D[0]; sq = D[1]; sr = D[2]; ss = D[3];
