@@ -1083,7 +1083,7 @@ int launch_tv_prox(pt_plan* plan, const float* v, double lam, int inner, int non
     {
         static const int tmax = [] {
             const char* e = getenv("PT_FGP_T");
-            return e ? std::max(1, std::min(8, atoi(e))) : 6;
+            return e ? std::max(1, std::min(8, atoi(e))) : 8;
         }();
         return run_fgp2d<64, 64, 8>(plan, v, lam, inner, nonneg, p, q, x_out, xhat, h,
                                     p_over_gamma, iteration, bad_iter, work, st, tmax);

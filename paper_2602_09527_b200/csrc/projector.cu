@@ -424,14 +424,15 @@ struct RedArgs {
 __global__ void __launch_bounds__(256) fwd_reduce_kernel(RedArgs P)
 {
     pdl_wait();
-    const size_t total = (size_t)P.n_k * P.Z * P.B;
-    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // n_k * Z * B < 2^31 (checked on the host): 32-bit index math
+    const unsigned total = (unsigned)P.n_k * P.Z * P.B;
+    const unsigned idx = blockIdx.x * blockDim.x + threadIdx.x;
     double sq = 0.0;
     if (idx < total) {
-        const int b = (int)(idx % P.B);
-        const size_t t = idx / P.B;
-        const int z = (int)(t % P.Z);
-        const int kk = (int)(t / P.Z);
+        const unsigned t = idx / (unsigned)P.B;
+        const int b = (int)(idx - t * P.B);
+        const int kk = (int)(t / (unsigned)P.Z);
+        const int z = (int)(t - kk * P.Z);
         const int k = kk + P.k_begin;
         const int ang = P.sel_angle[k];
         const AngleTab at = P.tab[ang];
@@ -441,6 +442,7 @@ __global__ void __launch_bounds__(256) fwd_reduce_kernel(RedArgs P)
         const float* pp = P.partial + idx;
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
         int band = 0;
+#pragma unroll 4
         for (; band + 4 <= nb; band += 4) {
             const float a = __ldcs(pp + (size_t)band * stride);
             const float b2 = __ldcs(pp + (size_t)(band + 1) * stride);
@@ -575,6 +577,10 @@ static int run_forward_cfg(pt_plan* plan, Workspace* ws, const pt_selection* sel
         r.y = y;
         r.block_sums = sumsq ? ws->red + red_off : nullptr;
         const size_t tot = (size_t)(ke - kb) * plan->Z * plan->B;
+        if (tot >= (size_t)INT32_MAX) {
+            set_error("forward chunk too large for the band reduction");
+            return PT_EINVAL;
+        }
         const int nblk = (int)((tot + 255) / 256);
         {
             ProfScope ps(ws, PT_PROF_FWD_REDUCE, st);
