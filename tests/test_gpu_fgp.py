@@ -118,3 +118,40 @@ def test_tv_value_and_nonneg(oracle):
     assert tv_value(vol) == pytest.approx(oracle.tv_value(vol), rel=1e-6)
     assert tv_value(np.full((6, 6), 2.5)) == 0.0
     assert np.array_equal(cpu(nonneg_prox(np.array([-1.0, 2.0, 0.0]))), [0.0, 2.0, 0.0])
+
+
+_PAIR_SNIPPET = """
+import sys
+sys.path.insert(0, {repo!r})
+import numpy as np
+import torch
+from paper_2602_09527_b200 import TvProxConfig, tv_prox
+out = []
+for shape, inner, nn in [((37, 44, 68), 11, True), ((64, 64, 64), 30, True), ((5, 16, 200), 2, False),
+                         ((17, 9, 8), 7, True), ((40, 33, 132), 16, False)]:
+    rng = np.random.default_rng(sum(shape))
+    v = rng.standard_normal(shape).cumsum(axis=0) * 0.1 + 0.2
+    x, st = tv_prox(v, 1.0, TvProxConfig(alpha=0.25, inner_iterations=inner, nonneg=nn))
+    torch.cuda.synchronize()
+    for t in (x, st.p, st.q, st.w):
+        out.append(t.detach().float().cpu().numpy().ravel())
+np.save(sys.argv[1], np.concatenate(out))
+"""
+
+
+def test_fgp_3d_pair_pass_bitwise(tmp_path):
+    """Two iterations per HBM pass (PT_FGP3_PAIR=1, the default for one slab)
+    give the same bits as one iteration per pass; odd counts, ragged tiles and
+    z-runs included."""
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag, zc in (("1", ""), ("0", ""), ("2", "16")):
+        path = tmp_path / f"pair{flag}.npy"
+        env = dict(os.environ, PT_FGP3_PAIR=flag, PT_FGP3_ZCHUNK=zc)
+        subprocess.run([sys.executable, "-c", _PAIR_SNIPPET.format(repo=repo), str(path)],
+                       check=True, env=env, timeout=300)
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
