@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--decomposition", default="rows", choices=["rows", "sectors"],
+                    help="2D multi-GPU layout: image rows (default) or angle sectors")
     ap.add_argument("--dp-one-rank", action="store_true",
                     help="test hook: run the multi-GPU data path (NCCL process group, sharded "
                          "session) with a single rank")
@@ -237,7 +239,7 @@ def build_gpu_problem(cfg, torch):
 def algorithmic_bytes(cfg, proj, state):
     """SURVEY.md 8d per-launch algorithmic bytes of each launch category."""
     depth = getattr(proj, "n_slices", 1)  # this rank's planes (z-slab) or the volume
-    n_px = cfg.size * cfg.size * depth
+    n_px = proj.width * proj.height * depth  # this rank's pixels (row / z slab or all)
     plan = proj.plan
     part = state.partition
     sub0 = part.subsets[0] if part else None
@@ -282,14 +284,18 @@ def gpu_arm(args, cfg, rank, world, local):
     scfg = SolverConfig(gamma=gamma, skip_probability=cfg.p, n_subsets=cfg.n_subsets,
                         estimator=cfg.estimator, max_data_passes=1e18, seed=cfg.solver_seed)
     stream = torch.cuda.Stream()
-    # multi-GPU: angle sectors (2D) or z-slabs (slice-stacked 3D)
-    zs, work = None, problem
+    # multi-GPU: image rows or angle sectors (2D), z-slabs (slice-stacked 3D);
+    # SURVEY.md 8e, DESIGN.md "Multi-GPU"
+    zs, rs, work = None, None, problem
     if dp and cfg.depth > 1:
         z0, z1 = D.zslab_bounds(cfg.depth, rank, world)
         zs, work = (z0, z1, cfg.depth), D.zslab_problem(problem, z0, z1)
+    elif dp and args.decomposition == "rows":
+        r0, r1 = D.rowslab_bounds(cfg.size, rank, world)
+        rs, work = (r0, r1, cfg.size), D.rowslab_problem(problem, r0, r1)
     with torch.cuda.stream(stream):
-        state = _init_state(scfg, work, None, stream, zslab=zs)
-    if dp and zs is None:
+        state = _init_state(scfg, work, None, stream, zslab=zs, rowslab=rs)
+    if dp and zs is None and rs is None:
         D.attach(state.session)
         # re-initialise the snapshot with the sharded full gradient
         state.session.init()
@@ -340,7 +346,8 @@ def gpu_arm(args, cfg, rank, world, local):
     value = args.steps / (ms / 1e3)
 
     # replica check across ranks
-    replicas_ok = D.replicas_identical(sess.x) if (dp and zs is None) else None
+    # replicas exist only in the angle-sector layout (slab layouts own disjoint parts)
+    replicas_ok = D.replicas_identical(sess.x) if (dp and zs is None and rs is None) else None
 
     # live per-kernel timing: a second timed pass with CUDA events per launch
     roofline = None
@@ -388,7 +395,8 @@ def gpu_arm(args, cfg, rank, world, local):
                             estimator=cfg.estimator,
                             max_data_passes=3.0 if cfg.estimator in ("svrg", "lsvrg") else 1.0,
                             seed=cfg.solver_seed)
-        warm = run(wcfg, TomoProblem(proj, b_host, tv=problem.tv), data_parallel=dp)
+        warm = run(wcfg, TomoProblem(proj, b_host, tv=problem.tv), data_parallel=dp,
+                   decomposition=args.decomposition)
         del warm
         import gc
         gc.collect()
@@ -396,7 +404,7 @@ def gpu_arm(args, cfg, rank, world, local):
         barrier()
         t0 = time.perf_counter()
         prob_h = TomoProblem(proj, b_host, tv=problem.tv)
-        rec = run(ecfg, prob_h, data_parallel=dp)
+        rec = run(ecfg, prob_h, data_parallel=dp, decomposition=args.decomposition)
         host_out.copy_(rec.image, non_blocking=True)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
@@ -436,7 +444,9 @@ def gpu_arm(args, cfg, rank, world, local):
                        "epochs_timed": args.steps, "iterations_timed": n_iter,
                        "prox_calls_timed": n_prox,
                        "parallelism": ("1 GPU" if not dp else
-                                       f"z-slab dp{world}" if zs else f"angle-sector dp{world}"),
+                                       f"z-slab dp{world}" if zs else
+                                       f"image-row dp{world}" if rs else
+                                       f"angle-sector dp{world}"),
                        "l2": "working set > L2 (band partials + state > 126 MB); no flush",
                        "L": lip, "gamma": gamma, "alpha": alpha},
             "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

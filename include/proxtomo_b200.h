@@ -51,6 +51,12 @@ typedef struct {
     int32_t n_angles, n_bins;
     double bin_spacing, pixel_size;
     const double* host_angles;
+    /* Row slab (multi-GPU rows decomposition): the plan's grid is rows
+     * [row_offset, row_offset + height) of a rows_total-row image; the
+     * projector's A and A^T are the whole image's restricted to those rows
+     * (forward partial sums add up over the slabs).  rows_total = 0: the
+     * grid is the whole image. */
+    int32_t row_offset, rows_total;
 } pt_geometry_desc;
 
 const char* pt_last_error(void);
@@ -144,6 +150,14 @@ int pt_tv_prox(pt_plan* plan, const float* v, double lam, int32_t inner_iteratio
                int32_t nonneg, float* p, float* q, float* w, float* x_out, const float* xhat,
                float* h, float p_over_gamma, int64_t iteration, int64_t* bad_iter, float* work,
                void* stream);
+
+/* Test hook of the multi-GPU row decomposition: the 2D TV prox of the
+ * whole image run as `slabs` row slabs on this device (ghost-row copies
+ * standing in for the NCCL halo exchange).  Arguments as
+ * pt_tv_prox on whole-image arrays; the result equals pt_tv_prox bitwise. */
+int pt_tv_prox_emulate_rows(pt_plan* plan, int32_t slabs, const float* v, double lam,
+                            int32_t inner_iterations, int32_t nonneg, float* p, float* q,
+                            float* x_out, void* stream);
 
 /* Reductions into device doubles (deterministic: fixed grid and combine
  * order, float64 accumulation).  `out` must hold PT_RED_DOUBLES doubles:
@@ -255,6 +269,15 @@ int pt_nccl_comm_destroy(pt_comm* comm);
 int pt_session_attach_comm(pt_session* s, pt_comm* comm);
 int pt_session_attach_comm_zslab(pt_session* s, pt_comm* comm, int32_t z_offset,
                                  int32_t z_total);
+/* Image-rows decomposition of a 2D problem: the session's plan is the row
+ * slab [row_offset, row_offset + height) of a rows_total-row image
+ * (pt_geometry_desc.row_offset / rows_total), its state the slab's rows.
+ * Every forward's partial line integrals are summed over the ranks in
+ * float64 (ncclAllReduce, 8 |S| B bytes); the gather, step and TV prox touch
+ * only the own rows (the prox exchanges 9 ghost rows with ranks -+ 1 per
+ * launch, ncclSend / ncclRecv).  Needs >= 9 rows per rank. */
+int pt_session_attach_comm_rows(pt_session* s, pt_comm* comm, int32_t row_offset,
+                                int32_t rows_total);
 int pt_session_attach_nccl(pt_session* s, const char* nccl_path, const uint8_t* host_id128,
                            int32_t rank, int32_t world);
 /* Test hook: run the angle-sector decomposition of `world` ranks on this one

@@ -31,7 +31,8 @@ class GeometryDesc(ctypes.Structure):
     _fields_ = [("height", c_i32), ("width", c_i32), ("n_slices", c_i32),
                 ("n_angles", c_i32), ("n_bins", c_i32),
                 ("bin_spacing", c_f64), ("pixel_size", c_f64),
-                ("host_angles", ctypes.POINTER(c_f64))]
+                ("host_angles", ctypes.POINTER(c_f64)),
+                ("row_offset", c_i32), ("rows_total", c_i32)]
 
 
 class StepEpilogue(ctypes.Structure):
@@ -63,6 +64,8 @@ _SIGS = {
     "pt_fgp_workspace_floats": (c_i64, [c_vp]),
     "pt_tv_prox": (ctypes.c_int, [c_vp, c_vp, c_f64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp,
                                   c_vp, c_vp, c_f32, c_i64, c_vp, c_vp, c_vp]),
+    "pt_tv_prox_emulate_rows": (ctypes.c_int, [c_vp, c_i32, c_vp, c_f64, c_i32, c_i32, c_vp, c_vp,
+                                               c_vp, c_vp]),
     "pt_dot": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "pt_tv_value": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "pt_diff_norms": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
@@ -100,6 +103,7 @@ _SIGS = {
     "pt_nccl_comm_destroy": (ctypes.c_int, [c_vp]),
     "pt_session_attach_comm": (ctypes.c_int, [c_vp, c_vp]),
     "pt_session_attach_comm_zslab": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32]),
+    "pt_session_attach_comm_rows": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -80,22 +80,27 @@ void workspace_free(Workspace* ws)
     ws->image = nullptr;
 }
 
-static AngleTab make_tab(double theta, int H, int W, int B, double ds, double h)
+// Row slab: the grid is rows [row0, row0 + H) of an Hg-row image; positions
+// are taken relative to the slab (row-stepping: step 0 is image row row0;
+// column-stepping: lane 0 is image row row0).
+static AngleTab make_tab(double theta, int Hg, int row0, int W, int B, double ds, double h)
 {
     AngleTab t;
     const double c = cos(theta), s = sin(theta);
-    const double cB = (B - 1) / 2.0, cH = (H - 1) / 2.0, cW = (W - 1) / 2.0;
+    const double cB = (B - 1) / 2.0, cH = (Hg - 1) / 2.0, cW = (W - 1) / 2.0;
     if (fabs(c) >= fabs(s)) {  // projector.py:32
         t.branch = 0;
         t.sigma = ds / (h * c);
         t.m = -(s / c);
         t.a0 = -cB * t.sigma + cH * (s / c) + cW;
+        if (row0) t.a0 += t.m * row0;
         t.step_len = (float)(h / fabs(c));
     } else {
         t.branch = 1;
         t.sigma = ds / (h * s);
         t.m = -(c / s);
         t.a0 = -cB * t.sigma + cW * (c / s) + cH;
+        if (row0) t.a0 -= row0;
         t.step_len = (float)(h / fabs(s));
     }
     t.isig = 1.0 / t.sigma;
@@ -173,15 +178,23 @@ int pt_plan_create(const pt_geometry_desc* d, pt_plan** out)
     }
     if (d->host_angles[0] < 0.0 || d->host_angles[d->n_angles - 1] >= M_PI) { set_error("angles must lie in [0, pi)"); return PT_EINVAL; }
 
+    if (d->rows_total != 0 && (d->row_offset < 0 || d->rows_total < d->row_offset + d->height)) {
+        set_error("row slab outside the image");
+        return PT_EINVAL;
+    }
+    if (d->rows_total != 0 && d->n_slices != 1) { set_error("row slabs are 2D"); return PT_EINVAL; }
+
     pt_plan* p = new pt_plan();
     p->H = d->height; p->W = d->width; p->Z = d->n_slices;
+    p->row0 = d->rows_total ? d->row_offset : 0;
+    p->Hg = d->rows_total ? d->rows_total : d->height;
     p->A = d->n_angles; p->B = d->n_bins;
     p->ds = d->bin_spacing; p->h = d->pixel_size;
     p->angles.assign(d->host_angles, d->host_angles + d->n_angles);
     p->h_tab.resize(p->A);
     double max_br = 0, max_bc = 0, min_abs_sigma = 1e300;
     for (int a = 0; a < p->A; ++a) {
-        const AngleTab t = make_tab(p->angles[a], p->H, p->W, p->B, p->ds, p->h);
+        const AngleTab t = make_tab(p->angles[a], p->Hg, p->row0, p->W, p->B, p->ds, p->h);
         p->h_tab[a] = t;
         const double ar = t.branch ? -1.0 : t.m, ac = t.branch ? t.m : -1.0;
         max_br = std::max(max_br, fabs(ar / t.sigma));
@@ -267,18 +280,22 @@ int64_t pt_selection_nnz(pt_plan* plan, const pt_selection* sel)
     if (sel->nnz >= 0) return sel->nnz;
     // exact count of kept COO entries (projector.py:55-60), float64 as the reference
     int64_t total = 0;
-    const int H = plan->H, W = plan->W, B = plan->B;
+    // image rows [r_lo, r_hi) are this plan's (a row slab counts its own taps)
+    const int H = plan->Hg, W = plan->W, B = plan->B;
+    const int r_lo = plan->row0, r_hi = plan->row0 + plan->H;
     for (int k = 0; k < sel->n; ++k) {
         const double th = plan->angles[sel->h_angle[k]];
         const double c = cos(th), s = sin(th), h = plan->h;
         const bool rows = fabs(c) >= fabs(s);
-        const int n_steps = rows ? H : W, n_lanes = rows ? W : H;
+        const int st_lo = rows ? r_lo : 0, st_hi = rows ? r_hi : W;
+        const int n_lanes = rows ? W : H;
+        const int ln_lo = rows ? 0 : r_lo, ln_hi = rows ? W : r_hi;
         const double step_len = rows ? h / fabs(c) : h / fabs(s);
         int64_t cnt = 0;
 #pragma omp parallel for reduction(+ : cnt)
         for (int b = 0; b < B; ++b) {
             const double sb = ((double)b - (B - 1) / 2.0) * plan->ds;
-            for (int st = 0; st < n_steps; ++st) {
+            for (int st = st_lo; st < st_hi; ++st) {
                 double cross;
                 if (rows) cross = (sb - (((double)st - (H - 1) / 2.0) * h) * s) / c;
                 else cross = (sb - (((double)st - (W - 1) / 2.0) * h) * c) / s;
@@ -286,8 +303,8 @@ int64_t pt_selection_nnz(pt_plan* plan, const pt_selection* sel)
                 const double fl = floor(pos);
                 const double fr = pos - fl;
                 const long long l0 = (long long)fl;
-                if (l0 >= 0 && l0 < n_lanes && (1.0 - fr) * step_len > 0.0) ++cnt;
-                if (l0 + 1 >= 0 && l0 + 1 < n_lanes && fr * step_len > 0.0) ++cnt;
+                if (l0 >= ln_lo && l0 < ln_hi && (1.0 - fr) * step_len > 0.0) ++cnt;
+                if (l0 + 1 >= ln_lo && l0 + 1 < ln_hi && fr * step_len > 0.0) ++cnt;
             }
         }
         total += cnt;
@@ -355,6 +372,38 @@ int pt_tv_prox(pt_plan* plan, const float* v, double lam, int32_t inner_iteratio
     if (h && !xhat) { set_error("h update needs x_hat"); return PT_EINVAL; }
     return launch_tv_prox(plan, v, lam, inner_iterations, nonneg, p, q, w, x_out, xhat, h,
                           p_over_gamma, iteration, bad_iter, work, (cudaStream_t)stream);
+}
+
+int pt_tv_prox_emulate_rows(pt_plan* plan, int32_t slabs, const float* v, double lam,
+                            int32_t inner_iterations, int32_t nonneg, float* p, float* q,
+                            float* x_out, void* stream)
+{
+    if (!plan || !v || !p || !q || !x_out) { set_error("null argument"); return PT_EINVAL; }
+    if (plan->Z != 1) { set_error("row slabs are a 2D decomposition"); return PT_EINVAL; }
+    if (!(lam > 0.0)) { set_error("tau must be positive"); return PT_EINVAL; }
+    if (slabs < 1 || slabs > plan->H) { set_error("bad slab count"); return PT_EINVAL; }
+    cudaStream_t st = (cudaStream_t)stream;
+    const int H = plan->H, W = plan->W;
+    std::vector<Fgp2Slab> sl(slabs);
+    size_t total = 0;
+    for (int g = 0; g < slabs; ++g) {
+        sl[g].r0 = (int)((long long)H * g / slabs);
+        sl[g].Hl = (int)((long long)H * (g + 1) / slabs) - sl[g].r0;
+        total += (size_t)fgp2d_slab_floats(sl[g].Hl, W);
+    }
+    float* work = nullptr;
+    PT_CHECK_CUDA(cudaMallocAsync(&work, total * 4, st));
+    float* w = work;
+    for (int g = 0; g < slabs; ++g) {
+        const size_t off = (size_t)sl[g].r0 * W;
+        sl[g].v = v + off; sl[g].p = p + off; sl[g].q = q + off; sl[g].x_out = x_out + off;
+        sl[g].work = w;
+        w += fgp2d_slab_floats(sl[g].Hl, W);
+    }
+    const int rc = fgp2d_rows_run(sl.data(), slabs, H, W, lam, inner_iterations, nonneg, 0.f, 0,
+                                  nullptr, nullptr, st);
+    cudaFreeAsync(work, st);
+    return rc;
 }
 
 int pt_dot(const float* a, const float* b, int64_t n, double* out, void* stream)

@@ -34,7 +34,11 @@
 namespace pt {
 
 struct FgpArgs {
-    int H, W;
+    int H, W;  // the image (H = global rows)
+    // the arrays hold rows [grow0, grow0 + Ha) of the image (row slab with
+    // ghost rows; the whole image: grow0 = 0, Ha = H); outputs are the array
+    // rows [row_lo, row_lo + rows_out) (final outputs indexed from row_lo)
+    int Ha, grow0, row_lo, rows_out;
     const float* v;
     const float *p_in, *q_in, *r_in, *s_in;  // r_in == nullptr: r = p, s = q (call start)
     float *p_out, *q_out, *r_out, *s_out;
@@ -52,6 +56,19 @@ struct FgpArgs {
     long long* bad_iter;
 };
 
+__device__ __forceinline__ float rsqrt_ftz(float x)
+{
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+// max that propagates NaN (max.NaN): the divergence check must see NaN duals
+__device__ __forceinline__ float max_nan(float a, float b)
+{
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
 // One FGP inner iteration on the register strips.  EDGE = the region touches
 // the image border (masks needed); interior regions skip every boundary test.
 template <int RW, int RH, int STRIP, bool EDGE, bool NONNEG>
@@ -83,8 +100,8 @@ __device__ __forceinline__ void fgp2d_iteration(
             o = o - s[k];
         }
         o += s_left;
-        float uu = v[k] - lam * o;
-        if (NONNEG) uu = (uu < 0.f) ? 0.f : uu;
+        float uu = fmaf(-lam, o, v[k]);
+        if (NONNEG) uu = max_nan(uu, 0.f);
         if (EDGE) uu = ((in_mask >> k) & 1u) ? uu : 0.f;
         u[k] = uu;
         S_u[row0 + k][tx + 1] = uu;
@@ -101,14 +118,16 @@ __device__ __forceinline__ void fgp2d_iteration(
             gv = (gi < H - 1) ? gv : 0.f;
             gh = not_last_col ? gh : 0.f;
         }
-        const float ph = r[k] + eta * gv;
-        const float qh = s[k] + eta * gh;
-        const float n2 = ph * ph + qh * qh;
-        const float inv = (n2 > 1.f) ? rsqrtf(n2) : 1.f;
+        // the packed path's operations exactly (fma order, rsqrt of max(n2, 1)),
+        // so an edge region and an interior one give the same bits
+        const float ph = fmaf(eta, gv, r[k]);
+        const float qh = fmaf(eta, gh, s[k]);
+        const float n2 = fmaf(ph, ph, qh * qh);
+        const float inv = rsqrt_ftz(max_nan(n2, 1.f));
         const float pn = ph * inv, qn = qh * inv;
         if (!EDGE || ((in_mask >> k) & 1u)) {
-            r[k] = pn + beta * (pn - p[k]);
-            s[k] = qn + beta * (qn - q[k]);
+            r[k] = fmaf(beta, pn - p[k], pn);
+            s[k] = fmaf(beta, qn - q[k], qn);
             p[k] = pn;
             q[k] = qn;
         }
@@ -121,19 +140,6 @@ __device__ __forceinline__ void fgp2d_iteration(
 // strip ends): the stencil needs no lane shuffling.  The left/right exchange
 // planes store the pairs as float2 (one 64-bit LDS/STS per pair, operands land
 // in aligned register pairs).
-__device__ __forceinline__ float rsqrt_ftz(float x)
-{
-    float r;
-    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-// max that propagates NaN (max.NaN): the divergence check must see NaN duals
-__device__ __forceinline__ float max_nan(float a, float b)
-{
-    float r;
-    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
-    return r;
-}
 __device__ __forceinline__ f2 ld2(const float2* p)
 {
     f2 r;
@@ -221,13 +227,16 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
     const int ty = tid / RW;
     const int IW = RW - 2 * P.halo, IH = RH - 2 * P.halo;
     const int j0 = blockIdx.x * IW - P.halo;
-    const int i0 = blockIdx.y * IH - P.halo;
+    const int i0 = P.row_lo + blockIdx.y * IH - P.halo;  // array row of the region
+    const int gi0 = i0 + P.grow0;                          // its image row
     const int gj = j0 + tx;
     const int row0 = ty * STRIP;
     const bool col_in = (gj >= 0 && gj < P.W);
     const bool not_last_col = (gj < P.W - 1);
     // the whole region, and one point beyond it, strictly inside the image
-    const bool edge = !(i0 >= 0 && j0 >= 0 && i0 + RH < P.H && j0 + RW < P.W);
+    // (and inside the arrays)
+    const bool edge = !(gi0 >= 0 && j0 >= 0 && gi0 + RH < P.H && j0 + RW < P.W && i0 >= 0 &&
+                        i0 + RH <= P.Ha);
 
     auto zero_pads = [&](bool packed) {
         // rows of the active layout: RH scalar rows or RH / 2 pair rows, 2 planes
@@ -294,10 +303,10 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int k = j + h * H2;
-                const int gi = i0 + row0 + k;
-                const bool in = col_in && gi >= 0 && gi < P.H;
+                const int ai = i0 + row0 + k, gi = ai + P.grow0;
+                const bool in = col_in && gi >= 0 && gi < P.H && ai >= 0 && ai < P.Ha;
                 if (in) in_mask |= 1u << k;
-                const size_t o = in ? (size_t)gi * P.W + gj : 0;
+                const size_t o = in ? (size_t)ai * P.W + gj : 0;
                 vv[h] = in ? P.v[o] : 0.f;
                 pv[h] = in ? P.p_in[o] : 0.f;
                 qv[h] = in ? P.q_in[o] : 0.f;
@@ -338,7 +347,7 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
                 upk(U[j], u[j], u[j + H2]);
             }
             fgp2d_iteration<RW, RH, STRIP, true, NONNEG>(v, p, q, r, s, u, S_s, S_u, S_r, S_ut, tx,
-                                                         ty, i0, P.H, not_last_col, in_mask, P.lam,
+                                                         ty, gi0, P.H, not_last_col, in_mask, P.lam,
                                                          P.eta, P.beta[it]);
 #pragma unroll
             for (int j = 0; j < H2; ++j) {
@@ -362,8 +371,11 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
     }
     // exact points: the region minus its halo, inside the image
     const bool col_inner = tx >= P.halo && tx < RW - P.halo && col_in;
-    const int k_lo = max(0, P.halo - row0), k_hi = min(STRIP, RH - P.halo - row0);
-    const size_t obase = (size_t)(i0 + row0) * P.W + gj;
+    // exact rows of the region that are output rows
+    const int k_lo = max(max(0, P.halo - row0), P.row_lo - (i0 + row0));
+    const int k_hi = min(min(STRIP, RH - P.halo - row0), P.row_lo + P.rows_out - (i0 + row0));
+    const size_t obase = (size_t)(i0 + row0) * P.W + gj;           // array index
+    const size_t fbase = obase - (size_t)P.row_lo * P.W;           // final outputs
     const float lam = P.lam;
     if (P.final_) {
         // x = max(v - lam D^T(p, q), 0), then the ProxSkip h update
@@ -375,7 +387,7 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < STRIP; ++k) {
-            const int gi = i0 + row0 + k;
+            const int gi = gi0 + row0 + k;
             if (!col_inner || k < k_lo || k >= k_hi || !((in_mask >> k) & 1u)) continue;
             const float p_up = k ? p[k - 1] : S_r[ty][tx];
             const float q_left = S_s[row0 + k][tx];
@@ -385,7 +397,7 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
             o += q_left;
             float x = v[k] - lam * o;
             if (NONNEG) x = (x < 0.f) ? 0.f : x;
-            const size_t idx = obase + (size_t)k * P.W;
+            const size_t idx = fbase + (size_t)k * P.W;
             P.x_out[idx] = x;
             P.p_out[idx] = p[k];
             P.q_out[idx] = q[k];
@@ -413,6 +425,16 @@ int64_t fgp_workspace_floats(const pt_plan* plan)
     // two ping-pong sets of (p, q, r, s) [2D] or (p, q, w, r, s, t) [3D]
     if (plan->Z > 1) return fgp3d_slab_floats(plan->Z, plan->H, plan->W);
     return 8 * (int64_t)plan->H * plan->W;
+}
+
+// inner iterations per launch of the 64 x 64 regions (PT_FGP_T, default 8)
+static int fgp2d_tmax()
+{
+    static const int tmax = [] {
+        const char* e = getenv("PT_FGP_T");
+        return e ? std::max(1, std::min(8, atoi(e))) : 8;
+    }();
+    return tmax;
 }
 
 template <int RW, int RH, int STRIP>
@@ -447,6 +469,7 @@ static int run_fgp2d(pt_plan* plan, const float* v, double lam, int inner, int n
         FgpArgs a;
         a.H = plan->H;
         a.W = plan->W;
+        a.Ha = plan->H; a.grow0 = 0; a.row_lo = 0; a.rows_out = plan->H;
         a.v = v;
         a.p_in = sp; a.q_in = sq; a.r_in = sr; a.s_in = ss;
         float** D = (L % 2 == 0) ? Y : X;
@@ -480,6 +503,152 @@ static int run_fgp2d(pt_plan* plan, const float* v, double lam, int inner, int n
         done += iters;
     }
     return PT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Row slabs of a 2D image (multi-GPU "rows" decomposition):
+// slab g owns image rows [r0, r0 + Hl).  Its FGP state lives in extended
+// arrays of Ha = Hl + 2 G rows (G = kRowGhost ghost rows above and below);
+// before every launch the ghost rows hold the neighbours' boundary rows, so
+// the launch's T <= G - 1 iterations on the slab's own rows see exactly the
+// values the whole-image launch sees: the result is bitwise the whole-image
+// result (edge and interior regions evaluate identical expressions).
+// Workspace per slab: v, (p, q, r, s) x 2, each Ha x W.
+// ---------------------------------------------------------------------------
+int64_t fgp2d_slab_floats(int Hl, int W) { return 9 * (int64_t)(Hl + 2 * kRowGhost) * W; }
+
+namespace {
+struct RowSets {
+    float* a[9];  // v, X[0..3], Y[0..3]
+};
+RowSets row_sets(const Fgp2Slab& s, int W)
+{
+    RowSets r;
+    const size_t n = (size_t)(s.Hl + 2 * kRowGhost) * W;
+    for (int i = 0; i < 9; ++i) r.a[i] = s.work + i * n;
+    return r;
+}
+}  // namespace
+
+// ghost rows of arrays `first .. first + n - 1` of every slab's sets
+static int fgp2d_rows_exchange(const Fgp2Slab* sl, int G, int W, int first, int n,
+                               const RowHalo* halo, cudaStream_t st)
+{
+    const int GR = kRowGhost;
+    const size_t band = (size_t)GR * W * 4;
+    for (int g = 0; g + 1 < G; ++g) {
+        const RowSets lo = row_sets(sl[g], W), hi = row_sets(sl[g + 1], W);
+        const int Hl = sl[g].Hl;
+        for (int i = first; i < first + n; ++i) {
+            // lower slab's bottom ghost rows <- upper slab's first own rows
+            PT_CHECK_CUDA(cudaMemcpyAsync(lo.a[i] + (size_t)(GR + Hl) * W, hi.a[i] + (size_t)GR * W,
+                                          band, cudaMemcpyDeviceToDevice, st));
+            // upper slab's top ghost rows <- lower slab's last own rows
+            PT_CHECK_CUDA(cudaMemcpyAsync(hi.a[i], lo.a[i] + (size_t)Hl * W, band,
+                                          cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    if (halo && halo->world > 1) {
+        const RowSets r = row_sets(sl[0], W);
+        return halo->exchange(halo->ctx, n, r.a + first, sl[0].Hl, W, GR, st);
+    }
+    return PT_OK;
+}
+
+template <int RW, int RH, int STRIP>
+static int fgp2d_rows_run_t(const Fgp2Slab* sl, int G, int H, int W, double lam, int inner,
+                            int nonneg, float pog, int64_t iteration, int64_t* bad_iter,
+                            const RowHalo* halo, int tmax, cudaStream_t st)
+{
+    const int GR = kRowGhost;
+    std::vector<double> betas(inner);
+    double t = 1.0;
+    for (int k = 0; k < inner; ++k) {
+        const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
+        betas[k] = (t - 1.0) / tn;
+        t = tn;
+    }
+    // own rows of v, p, q into the extended arrays, then their ghost rows
+    for (int g = 0; g < G; ++g) {
+        const RowSets r = row_sets(sl[g], W);
+        const size_t off = (size_t)GR * W, n = (size_t)sl[g].Hl * W * 4;
+        PT_CHECK_CUDA(cudaMemcpyAsync(r.a[0] + off, sl[g].v, n, cudaMemcpyDeviceToDevice, st));
+        PT_CHECK_CUDA(cudaMemcpyAsync(r.a[1] + off, sl[g].p, n, cudaMemcpyDeviceToDevice, st));
+        PT_CHECK_CUDA(cudaMemcpyAsync(r.a[2] + off, sl[g].q, n, cudaMemcpyDeviceToDevice, st));
+    }
+    int rc = fgp2d_rows_exchange(sl, G, W, 0, 3, halo, st);
+    if (rc) return rc;
+    const int n_launch = (inner + tmax - 1) / tmax;
+    int done = 0;
+    for (int L = 0; L < n_launch; ++L) {
+        const int iters = std::min(tmax, inner - done);
+        const bool fin = (L == n_launch - 1);
+        const int src = (L % 2 == 0) ? 1 : 5, dst = (L % 2 == 0) ? 5 : 1;  // X / Y sets
+        for (int g = 0; g < G; ++g) {
+            const RowSets r = row_sets(sl[g], W);
+            FgpArgs a;
+            a.H = H;
+            a.W = W;
+            a.Ha = sl[g].Hl + 2 * GR; a.grow0 = sl[g].r0 - GR; a.row_lo = GR; a.rows_out = sl[g].Hl;
+            a.v = r.a[0];
+            a.p_in = r.a[src]; a.q_in = r.a[src + 1];
+            a.r_in = L ? r.a[src + 2] : nullptr;
+            a.s_in = L ? r.a[src + 3] : nullptr;
+            if (fin) {
+                a.p_out = sl[g].p; a.q_out = sl[g].q; a.r_out = nullptr; a.s_out = nullptr;
+            } else {
+                a.p_out = r.a[dst]; a.q_out = r.a[dst + 1];
+                a.r_out = r.a[dst + 2]; a.s_out = r.a[dst + 3];
+            }
+            a.lam = (float)lam;
+            a.eta = (float)(1.0 / (8.0 * lam));
+            for (int k = 0; k < 8; ++k) a.beta[k] = (k < iters) ? (float)betas[done + k] : 0.f;
+            a.n_iter = iters;
+            a.halo = iters + 1;
+            a.nonneg = nonneg;
+            a.final_ = fin ? 1 : 0;
+            a.x_out = sl[g].x_out;
+            a.xhat = sl[g].xhat;
+            a.h = sl[g].h;
+            a.pog = pog;
+            a.iteration = (long long)iteration;
+            a.bad_iter = (long long*)bad_iter;
+            const int IW = RW - 2 * a.halo, IH = RH - 2 * a.halo;
+            dim3 grid((W + IW - 1) / IW, (sl[g].Hl + IH - 1) / IH);
+            PT_CHECK_CUDA(launch_pdl(nonneg ? fgp2d_kernel<RW, RH, STRIP, true>
+                                            : fgp2d_kernel<RW, RH, STRIP, false>,
+                                     grid, dim3(RW * (RH / STRIP)), 0, st, a));
+            PT_CHECK_LAUNCH();
+        }
+        if (!fin) {
+            rc = fgp2d_rows_exchange(sl, G, W, dst, 4, halo, st);
+            if (rc) return rc;
+        }
+        done += iters;
+    }
+    return PT_OK;
+}
+
+int fgp2d_rows_run(const Fgp2Slab* sl, int G, int H, int W, double lam, int inner, int nonneg,
+                   float pog, int64_t iteration, int64_t* bad_iter, const RowHalo* halo,
+                   cudaStream_t st)
+{
+    if (inner < 1) {
+        set_error("inner_iterations must be >= 1");
+        return PT_EINVAL;
+    }
+    for (int g = 0; g < G; ++g) {
+        if (sl[g].Hl < kRowGhost) {
+            set_error("a row slab needs at least %d rows", kRowGhost);
+            return PT_EINVAL;
+        }
+    }
+    // the whole-image tile choice (launch_tv_prox), so T and tiles match
+    if (std::min(H, W) >= 256)
+        return fgp2d_rows_run_t<64, 64, 8>(sl, G, H, W, lam, inner, nonneg, pog, iteration,
+                                           bad_iter, halo, fgp2d_tmax(), st);
+    return fgp2d_rows_run_t<32, 32, 8>(sl, G, H, W, lam, inner, nonneg, pog, iteration, bad_iter,
+                                       halo, 3, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -1459,14 +1628,8 @@ int launch_tv_prox(pt_plan* plan, const float* v, double lam, int inner, int non
                          iteration, bad_iter, nullptr, plan->sm_count, st);
     }
     if (std::min(plan->H, plan->W) >= 256)
-    {
-        static const int tmax = [] {
-            const char* e = getenv("PT_FGP_T");
-            return e ? std::max(1, std::min(8, atoi(e))) : 8;
-        }();
         return run_fgp2d<64, 64, 8>(plan, v, lam, inner, nonneg, p, q, x_out, xhat, h,
-                                    p_over_gamma, iteration, bad_iter, work, st, tmax);
-    }
+                                    p_over_gamma, iteration, bad_iter, work, st, fgp2d_tmax());
     return run_fgp2d<32, 32, 8>(plan, v, lam, inner, nonneg, p, q, x_out, xhat, h,
                                 p_over_gamma, iteration, bad_iter, work, st, 3);
 }

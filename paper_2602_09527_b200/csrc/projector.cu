@@ -419,6 +419,7 @@ struct RedArgs {
     const float* data2;
     float* y;
     double* block_sums;
+    double* y64;  // row-slab partial: s * step_len in float64, no data, no y
 };
 
 __global__ void __launch_bounds__(256) fwd_reduce_kernel(RedArgs P)
@@ -453,6 +454,11 @@ __global__ void __launch_bounds__(256) fwd_reduce_kernel(RedArgs P)
         for (; band < nb; ++band) s0 += __ldcs(pp + (size_t)band * stride);
         const double s = (s0 + s1) + (s2 + s3);
         double yd = s * (double)at.step_len;
+        if (P.y64) {  // partial line integrals of a row slab (summed over ranks later)
+            P.y64[((size_t)k * P.Z + z) * P.B + b] = yd;
+            pdl_trigger();
+            return;
+        }
         if (P.data) yd -= (double)P.data[((size_t)ang * P.Z + z) * P.B + b];
         if (P.data2) yd -= (double)P.data2[((size_t)ang * P.Z + z) * P.B + b];
         const float yv = (float)yd;
@@ -477,7 +483,7 @@ __global__ void __launch_bounds__(256) fwd_reduce_kernel(RedArgs P)
 template <int TY, int TX, int NT, int MINB>
 static int run_forward_cfg(pt_plan* plan, Workspace* ws, const pt_selection* sel,
                            const float* x, const float* x2, const float* data, float* y,
-                           double* sumsq, cudaStream_t st, const float* data2)
+                           double* sumsq, cudaStream_t st, const float* data2, double* y64)
 {
     using T = FwdTile<TY, TX>;
     {
@@ -576,6 +582,7 @@ static int run_forward_cfg(pt_plan* plan, Workspace* ws, const pt_selection* sel
         r.data2 = data2;
         r.y = y;
         r.block_sums = sumsq ? ws->red + red_off : nullptr;
+        r.y64 = y64;
         const size_t tot = (size_t)(ke - kb) * plan->Z * plan->B;
         if (tot >= (size_t)INT32_MAX) {
             set_error("forward chunk too large for the band reduction");
@@ -599,19 +606,57 @@ static int run_forward_cfg(pt_plan* plan, Workspace* ws, const pt_selection* sel
 
 int launch_forward(pt_plan* plan, Workspace* ws, const pt_selection* sel, const float* x,
                    const float* x2, const float* data, float* y, double* sumsq, cudaStream_t st,
-                   const float* data2)
+                   const float* data2, double* y64)
 {
     if (sel->n == 0) {
         if (sumsq) PT_CHECK_CUDA(cudaMemsetAsync(sumsq, 0, sizeof(double), st));
         return PT_OK;
     }
+    if (y64 && sumsq) { set_error("partial forward has no residual norm"); return PT_EINVAL; }
     switch (plan->fwd_cfg) {
 #define PT_FWD_CASE(id, TY, TX, NT, MB) \
-    case id: return run_forward_cfg<TY, TX, NT, MB>(plan, ws, sel, x, x2, data, y, sumsq, st, data2);
+    case id: return run_forward_cfg<TY, TX, NT, MB>(plan, ws, sel, x, x2, data, y, sumsq, st, data2, y64);
         PT_FWD_CONFIGS(PT_FWD_CASE)
 #undef PT_FWD_CASE
         default: set_error("bad forward config"); return PT_EINVAL;
     }
+}
+
+// Row slabs: the summed float64 partial line integrals -> residual rows, with
+// the reduction's own operation order (yd - data - data2, then float), so one
+// slab reproduces the whole-image forward bit for bit.
+__global__ void fwd_finish_kernel(const double* y64, const int32_t* sel_angle, int n_k, int Z,
+                                  int B, const float* data, const float* data2, float* y)
+{
+    pdl_wait();
+    const unsigned total = (unsigned)n_k * Z * B;
+    for (unsigned idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += gridDim.x * blockDim.x) {
+        const unsigned t = idx / (unsigned)B;
+        const int b = (int)(idx - t * B);
+        const int k = (int)(t / (unsigned)Z);
+        const int z = (int)(t - k * Z);
+        const int ang = sel_angle[k];
+        double yd = y64[idx];
+        if (data) yd -= (double)data[((size_t)ang * Z + z) * B + b];
+        if (data2) yd -= (double)data2[((size_t)ang * Z + z) * B + b];
+        y[idx] = (float)yd;
+    }
+    pdl_trigger();
+}
+
+int launch_forward_finish(pt_plan* plan, const pt_selection* sel, const double* y64,
+                          const float* data, const float* data2, float* y, cudaStream_t st)
+{
+    if (sel->n == 0) return PT_OK;
+    const size_t tot = (size_t)sel->n * plan->Z * plan->B;
+    if (tot >= (size_t)INT32_MAX) { set_error("selection too large"); return PT_EINVAL; }
+    const int blocks = (int)std::min<size_t>((tot + 255) / 256, (size_t)plan->sm_count * 8);
+    PT_CHECK_CUDA(launch_pdl(fwd_finish_kernel, dim3(blocks), dim3(256), 0, st, y64,
+                             (const int32_t*)sel->d_angle, sel->n, plan->Z, plan->B, data, data2,
+                             y));
+    PT_CHECK_LAUNCH();
+    return PT_OK;
 }
 
 // ---------------------------------------------------------------------------

@@ -152,6 +152,7 @@ void workspace_free(Workspace* ws);
 
 struct pt_plan {
     int32_t H = 0, W = 0, Z = 1, A = 0, B = 0;
+    int32_t row0 = 0, Hg = 0;  // row slab: rows [row0, row0 + H) of an Hg-row image
     double ds = 1.0, h = 1.0;
     std::vector<double> angles;
     std::vector<pt::AngleTab> h_tab;
@@ -178,7 +179,10 @@ void forward_config(int cfg, int32_t* ty, int32_t* tx);
 // y = A_S (x - x2) - data_S - data2_S; data / data2 are full sinograms indexed by angle
 int launch_forward(pt_plan* plan, Workspace* ws, const pt_selection* sel, const float* x,
                    const float* x2, const float* data, float* y, double* sumsq, cudaStream_t st,
-                   const float* data2 = nullptr);
+                   const float* data2 = nullptr, double* y64 = nullptr);
+// y (float residual rows) = y64 (summed float64 partial line integrals) - data - data2
+int launch_forward_finish(pt_plan* plan, const pt_selection* sel, const double* y64,
+                          const float* data, const float* data2, float* y, cudaStream_t st);
 int launch_adjoint(pt_plan* plan, const pt_selection* sel, const float* y, float* x_out,
                    float alpha, int accumulate, const pt_step_epilogue* ep, cudaStream_t st,
                    Workspace* ws = nullptr, int cat = PT_PROF_GATHER);
@@ -210,6 +214,29 @@ struct ZHalo {
                     float* recv_hi, size_t count, cudaStream_t st) = nullptr;
 };
 int64_t fgp3d_slab_floats(int Zl, int H, int W);
+// 2D row slabs (rows decomposition): slab owns image rows [r0, r0 + Hl)
+constexpr int kRowGhost = 9;  // ghost rows per side: the largest FGP T (8) + 1
+struct Fgp2Slab {
+    int Hl = 0, r0 = 0;
+    const float* v = nullptr;  // own rows, Hl x W (as p, q, x_out, xhat, h)
+    float *p = nullptr, *q = nullptr;
+    float* x_out = nullptr;
+    const float* xhat = nullptr;
+    float* h = nullptr;
+    float* work = nullptr;  // fgp2d_slab_floats(Hl, W)
+};
+// exchange of the kRowGhost-row boundary bands of n extended arrays (Hl own
+// rows between `ghost` ghost rows each side) with the rank -+ 1 slabs
+struct RowHalo {
+    int rank = 0, world = 1;
+    void* ctx = nullptr;
+    int (*exchange)(void* ctx, int n, float* const* arrays, int Hl, int W, int ghost,
+                    cudaStream_t st) = nullptr;
+};
+int64_t fgp2d_slab_floats(int Hl, int W);
+int fgp2d_rows_run(const Fgp2Slab* slabs, int G, int H, int W, double lam, int inner,
+                   int nonneg, float pog, int64_t iteration, int64_t* bad_iter,
+                   const RowHalo* halo, cudaStream_t st);
 int fgp3d_run(const Fgp3Slab* slabs, int G, int H, int W, int Zg, double lam, int inner,
               int nonneg, float pog, int64_t iteration, int64_t* bad_iter, const ZHalo* halo,
               int sm_count, cudaStream_t st);

@@ -9,10 +9,19 @@
 // The subset / theta / refresh sequences are drawn on the host with the
 // reference's own PCG64 streams (solvers.py:164,174-176) and passed in.
 //
-// Multi-GPU (angle sectors): rank g owns angles [g A/G, (g+1) A/G); its
-// forward/gather cover only those rows of subset i; the partial A_i^T r is
-// summed with ncclAllReduce on the session stream; every rank then applies the
-// identical epilogue and prox, so the replicas stay bitwise equal.
+// Multi-GPU, three decompositions:
+//  * angle sectors (2D): rank g owns angles [g A/G, (g+1) A/G); its
+//    forward/gather cover only those rows of subset i; the partial A_i^T r
+//    (4 n_px bytes) is summed with ncclAllReduce on the session stream; every
+//    rank then applies the identical epilogue and prox (bitwise replicas);
+//  * image rows (2D): rank g owns image rows [r0, r0 + Hl) (a row-slab plan);
+//    its forward gives partial line integrals of subset i, summed in float64
+//    with ncclAllReduce (8 |S_i| B bytes: 0.7 MB at config 2 instead of
+//    16 MB), then every rank forms the full residual and gathers, steps and
+//    proxes only its own rows (the TV prox exchanges ghost rows with ranks
+//    g -+ 1 every launch);
+//  * z-slabs (slice-stacked 3D): the projector is slab-local, the 3D prox
+//    exchanges ghost planes.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <math.h>
@@ -38,6 +47,7 @@ typedef const char* (*fn_errstr)(int);
 typedef int (*fn_p2p)(const void*, size_t, int, int, nccl_comm, cudaStream_t);
 typedef int (*fn_group)(void);
 constexpr int kNcclFloat32 = 7;
+constexpr int kNcclFloat64 = 8;
 constexpr int kNcclSum = 0;
 
 struct NcclApi {
@@ -175,6 +185,11 @@ struct pt_session {
     // test hook: G virtual z-slabs of this volume on one device
     int emu_z = 1;
     float* emu_z_work = nullptr;
+    // image-rows mode (2D): the plan is rows [plan->row0, + H) of plan->Hg
+    bool rows = false;
+    double* y64 = nullptr;       // partial line integrals (A rows x B), float64
+    float* rows_work = nullptr;  // extended-row FGP state (fgp2d_slab_floats)
+    pt::RowHalo rhalo;
 };
 
 namespace {
@@ -227,7 +242,8 @@ int build_selections(pt_session* s)
 {
     pt_plan* P = s->plan;
     const int A = P->A;
-    const int world = s->zslab ? 1 : s->world, rank = s->zslab ? 0 : s->rank;
+    const bool all = s->zslab || s->rows;  // slab modes own every angle
+    const int world = all ? 1 : s->world, rank = all ? 0 : s->rank;
     const int lo = (int)((long long)A * rank / world);
     const int hi = (int)((long long)A * (rank + 1) / world);
     const int n = (s->d.estimator != PT_EST_FULL) ? s->d.n_subsets : 0;
@@ -236,13 +252,34 @@ int build_selections(pt_session* s)
 
 int allreduce(pt_session* s, float* buf, cudaStream_t st)
 {
-    if (!s->comm || s->zslab) return PT_OK;
+    if (!s->comm || s->zslab || s->rows) return PT_OK;
     int e = s->nccl.allreduce(buf, buf, s->n, kNcclFloat32, kNcclSum, s->comm, st);
     if (e != 0) {
         pt::set_error("ncclAllReduce: %s", s->nccl.errstr ? s->nccl.errstr(e) : "error");
         return PT_ENCCL;
     }
     return PT_OK;
+}
+
+// Rows mode: residual rows of `sel` = (sum over ranks of the slabs' partial
+// line integrals) - data - data2; the float64 sum is one ncclAllReduce.
+int rows_forward(pt_session* s, const pt_selection* sel, const float* x, const float* data2,
+                 float* out, cudaStream_t st)
+{
+    pt_plan* P = s->plan;
+    int rc = pt::launch_forward(P, &s->ws, sel, x, nullptr, nullptr, nullptr, nullptr, st,
+                                nullptr, s->y64);
+    if (rc || sel->n == 0) return rc;
+    {
+        pt::ProfScope ps(&s->ws, PT_PROF_OTHER, st);
+        const int e = s->nccl.allreduce(s->y64, s->y64, (size_t)sel->n * P->Z * P->B,
+                                        kNcclFloat64, kNcclSum, s->comm, st);
+        if (e != 0) {
+            pt::set_error("ncclAllReduce: %s", s->nccl.errstr ? s->nccl.errstr(e) : "error");
+            return PT_ENCCL;
+        }
+    }
+    return pt::launch_forward_finish(P, sel, s->y64, s->data, data2, out, st);
 }
 
 // G = A^T (A x - b) over the owned angles, summed over ranks (estimators.py:40-48).
@@ -253,7 +290,9 @@ int full_gradient(pt_session* s, const float* x, float* out, float* res, cudaStr
 {
     pt::ProfScope ps(&s->ws, PT_PROF_SNAPSHOT, st);
     pt_plan* P = s->plan;
-    int rc = pt::launch_forward(P, &s->ws, s->own_all, x, nullptr, s->data, res, nullptr, st);
+    int rc = s->rows ? rows_forward(s, s->own_all, x, nullptr, res, st)
+                     : pt::launch_forward(P, &s->ws, s->own_all, x, nullptr, s->data, res,
+                                          nullptr, st);
     if (rc) return rc;
     if (s->emu > 1) {
         // virtual sectors: each sector's A_S^T over the shared residual, summed
@@ -304,6 +343,44 @@ int nccl_halo(void* ctx, const float* send_lo, float* recv_lo, const float* send
         return PT_ENCCL;
     }
     return PT_OK;
+}
+
+// Ghost-row exchange of a rows rank with ranks -+ 1 (one NCCL group for all
+// n arrays; arrays hold `ghost` rows, Hl own rows, `ghost` rows).
+int nccl_rows_halo(void* ctx, int n, float* const* arrays, int Hl, int W, int ghost,
+                   cudaStream_t st)
+{
+    pt_session* s = (pt_session*)ctx;
+    const NcclApi& api = s->nccl;
+    const bool lo = s->rank > 0, hi = s->rank + 1 < s->world;
+    const size_t cnt = (size_t)ghost * W;
+    int e = api.group_start();
+    for (int i = 0; i < n && !e; ++i) {
+        float* a = arrays[i];
+        if (lo && !e) e = api.send(a + cnt, cnt, kNcclFloat32, s->rank - 1, s->comm, st);
+        if (lo && !e) e = api.recv(a, cnt, kNcclFloat32, s->rank - 1, s->comm, st);
+        if (hi && !e) e = api.send(a + (size_t)Hl * W, cnt, kNcclFloat32, s->rank + 1, s->comm, st);
+        if (hi && !e) e = api.recv(a + (size_t)(ghost + Hl) * W, cnt, kNcclFloat32, s->rank + 1,
+                                   s->comm, st);
+    }
+    const int e2 = api.group_end();
+    if (e || e2) {
+        pt::set_error("NCCL row halo exchange: %s", api.errstr ? api.errstr(e ? e : e2) : "error");
+        return PT_ENCCL;
+    }
+    return PT_OK;
+}
+
+// The 2D TV prox of a rows rank: its own rows, ghost rows over NCCL.
+int rows_tv_prox(pt_session* s, double lam, float pog, float* xn, int64_t k, cudaStream_t st)
+{
+    pt_plan* P = s->plan;
+    pt::Fgp2Slab a;
+    a.Hl = P->H; a.r0 = P->row0;
+    a.v = s->v; a.p = s->dp; a.q = s->dq;
+    a.x_out = xn; a.xhat = s->xhat; a.h = s->h; a.work = s->rows_work;
+    return pt::fgp2d_rows_run(&a, 1, P->Hg, P->W, lam, s->d.tv_inner, s->d.tv_nonneg, pog, k,
+                              s->bad, &s->rhalo, st);
 }
 
 // The 3D TV prox of a z-slab rank (halos over NCCL), or of G virtual slabs of
@@ -492,6 +569,8 @@ int pt_session_destroy(pt_session* s)
     if (s->fgp3_work) cudaFree(s->fgp3_work);
     if (s->dw_slab) cudaFree(s->dw_slab);
     if (s->emu_z_work) cudaFree(s->emu_z_work);
+    if (s->y64) cudaFree(s->y64);
+    if (s->rows_work) cudaFree(s->rows_work);
     delete s;
     return PT_OK;
 }
@@ -549,6 +628,8 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
         // forward: residual rows of the (own part of the) selection
         if (refreshed || s->emu > 1)
             ;  // none / per virtual sector below
+        else if (s->rows)
+            rc = rows_forward(s, sel, xc, vr ? rsnap_by_angle(s) : nullptr, s->r, st);
         else if (vr)  // A_i (x - x_snap) = (A_i x - b_i) - (A_i x_snap - b_i)
             rc = pt::launch_forward(P, &s->ws, sel, xc, nullptr, s->data, s->r, nullptr, st,
                                     rsnap_by_angle(s));
@@ -596,7 +677,7 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
                 if (!rc) rc = pt::launch_adjoint(P, sg, s->r, s->g, 1.f, g > 0, nullptr, st, &s->ws);
             }
             if (!rc) rc = pt::launch_epilogue(P, s->g, &ep, st);
-        } else if (!s->comm || s->zslab) {
+        } else if (!s->comm || s->zslab || s->rows) {
             rc = pt::launch_adjoint(P, sel, s->r, nullptr, 1.f, 0, &ep, st, &s->ws);
         } else {
             if (sel->n == 0) {
@@ -626,6 +707,8 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
                 }
                 if (s->zslab || s->emu_z > 1)
                     rc = slab_tv_prox(s, lam, pog, xn, k, st);
+                else if (s->rows)
+                    rc = rows_tv_prox(s, lam, pog, xn, k, st);
                 else
                     rc = pt::launch_tv_prox(P, s->v, lam, d.tv_inner, d.tv_nonneg, s->dp, s->dq,
                                             s->dw, xn, s->xhat, s->h, pog, k, s->bad,
@@ -804,7 +887,47 @@ int attach_zslab(pt_session* s, const NcclApi& api, nccl_comm comm, int rank, in
     return build_selections(s);
 }
 
+int attach_rows(pt_session* s, const NcclApi& api, nccl_comm comm, int rank, int world,
+                int32_t row_offset, int32_t rows_total)
+{
+    pt_plan* P = s->plan;
+    if (P->Z != 1 || P->row0 != row_offset || P->Hg != rows_total) {
+        pt::set_error("the session's plan is not the row slab [%d, %d) of %d rows", row_offset,
+                      row_offset + P->H, rows_total);
+        return PT_EINVAL;
+    }
+    if (!api.send || !api.recv || !api.group_start || !api.group_end) {
+        pt::set_error("libnccl lacks ncclSend/ncclRecv");
+        return PT_ENCCL;
+    }
+    if (s->d.prox_kind == 1 && world > 1 && P->H < pt::kRowGhost) {
+        pt::set_error("a row slab needs at least %d rows for the TV prox", pt::kRowGhost);
+        return PT_EINVAL;
+    }
+    PT_CHECK_CUDA(cudaMalloc(&s->y64, (size_t)P->A * P->Z * P->B * sizeof(double)));
+    if (s->d.prox_kind == 1)
+        PT_CHECK_CUDA(cudaMalloc(&s->rows_work,
+                                 (size_t)pt::fgp2d_slab_floats(P->H, P->W) * sizeof(float)));
+    s->nccl = api;
+    s->comm = comm;
+    s->rank = rank;
+    s->world = world;
+    s->rows = true;
+    s->rhalo.rank = rank;
+    s->rhalo.world = world;
+    s->rhalo.ctx = s;
+    s->rhalo.exchange = nccl_rows_halo;
+    return build_selections(s);
+}
+
 }  // namespace
+
+int pt_session_attach_comm_rows(pt_session* s, pt_comm* c, int32_t row_offset, int32_t rows_total)
+{
+    if (!s || !c) { pt::set_error("null argument"); return PT_EINVAL; }
+    if (s->comm) { pt::set_error("session already attached"); return PT_EINVAL; }
+    return attach_rows(s, c->api, c->comm, c->rank, c->world, row_offset, rows_total);
+}
 
 int pt_session_attach_comm(pt_session* s, pt_comm* c)
 {

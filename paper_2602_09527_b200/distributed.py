@@ -1,5 +1,12 @@
-"""Multi-GPU data parallelism (one process per GPU): angle sectors (2D) and
-z-slabs (slice-stacked 3D).
+"""Multi-GPU data parallelism (one process per GPU): image rows or angle
+sectors (2D), z-slabs (slice-stacked 3D).
+
+Image rows (the 2D default): rank g owns image rows [g*H/G, (g+1)*H/G) with a
+row-slab plan; each forward's partial line integrals are summed in float64 by
+ncclAllReduce (8 |S_i| B bytes per step: 0.7 MB at config 2), the gather,
+ProxSkip step and TV prox touch only the own rows (ghost rows exchanged with
+ranks g -+ 1 per FGP launch).  The per-step exchange is 23x smaller than the
+sector layout's image-sized allreduce and the prox is sharded too.
 
 Rank g of G owns the contiguous sinogram rows of angles
 [g*A/G, (g+1)*A/G) (geometry.angle_sector).  Staggered subsets therefore
@@ -169,5 +176,62 @@ def gather_zslabs(x_slab: torch.Tensor, n_slices: int, group=None) -> torch.Tens
     out = torch.empty((n_slices, H, W), device=x_slab.device, dtype=x_slab.dtype)
     for g in range(world):
         a, b = zslab_bounds(n_slices, g, world)
+        out[a:b] = parts[g][:b - a]
+    return out
+
+
+# ---------------------------------------------------------------------------
+# image-row decomposition of 2D problems
+# ---------------------------------------------------------------------------
+
+ROW_GHOST = 9  # ghost rows per side of a slab's TV prox (csrc kRowGhost)
+
+
+def rowslab_bounds(n_rows: int, rank: int, world: int) -> tuple[int, int]:
+    """Rank g of G owns image rows [g H / G, (g + 1) H / G) (contiguous, rank order)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank / world")
+    if n_rows < world:
+        raise ValueError(f"{n_rows} rows cannot be split over {world} ranks")
+    return n_rows * rank // world, n_rows * (rank + 1) // world
+
+
+def rowslab_problem(problem, r0: int, r1: int):
+    """Rows [r0, r1) of a 2D TomoProblem: a row-slab projector (partial line
+    integrals; the sinogram stays whole), same data and regulariser."""
+    from .projector import Projector
+    from .solvers import TomoProblem
+    proj = problem.projector
+    if getattr(proj, "n_slices", 1) != 1:
+        raise ValueError("row slabs are a 2D decomposition")
+    if problem.tv is not None and r1 - r0 < ROW_GHOST and (r0 > 0 or r1 < proj.height):
+        raise ValueError(f"a row slab needs at least {ROW_GHOST} rows for the TV prox")
+    sub = Projector(proj.geometry, proj.width, r1 - r0, row_slab=(r0, proj.height))
+    return TomoProblem(sub, problem.data, tv=problem.tv, denoiser=problem.denoiser)
+
+
+def attach_rows(session, r0: int, rows_total: int, rank: int | None = None,
+                world: int | None = None, group=None) -> None:
+    """Attach a row-slab session to the process group's communicator."""
+    N.check(N.lib().pt_session_attach_comm_rows(session.handle,
+                                                communicator(rank, world, group), int(r0),
+                                                int(rows_total)), "attach_rows")
+
+
+def gather_rowslabs(x_slab: torch.Tensor, n_rows: int, group=None) -> torch.Tensor:
+    """The full (H, W) image on every rank from each rank's rows (log rows and
+    the final image only; padded all_gather over the process group)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    W = x_slab.shape[-1]
+    spans = [rowslab_bounds(n_rows, g, world) for g in range(world)]
+    hmax = max(b - a for a, b in spans)
+    buf = torch.zeros((hmax, W), device=x_slab.device, dtype=x_slab.dtype)
+    r0, r1 = spans[rank]
+    buf[:r1 - r0] = x_slab.reshape(r1 - r0, W)
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    out = torch.empty((n_rows, W), device=x_slab.device, dtype=x_slab.dtype)
+    for g, (a, b) in enumerate(spans):
         out[a:b] = parts[g][:b - a]
     return out

@@ -37,15 +37,20 @@ def as_device(a, dtype=torch.float32) -> torch.Tensor:
 class Plan:
     """Native plan: geometry + grid (+ slice count) and cached selections."""
 
-    def __init__(self, geometry: ParallelGeometry, width: int, height: int, n_slices: int = 1):
+    def __init__(self, geometry: ParallelGeometry, width: int, height: int, n_slices: int = 1,
+                 row_slab: tuple | None = None):
         lib = N.lib()
         self.geometry = geometry
         self.width, self.height, self.n_slices = int(width), int(height), int(n_slices)
+        # (row_offset, rows_total): the grid is rows [row_offset, row_offset + height)
+        # of a rows_total-row image (multi-GPU rows decomposition)
+        self.row_slab = None if row_slab is None else (int(row_slab[0]), int(row_slab[1]))
+        r0, rt = self.row_slab if self.row_slab else (0, 0)
         self._angles = (ctypes.c_double * geometry.n_angles)(*geometry.angles)
         desc = N.GeometryDesc(self.height, self.width, self.n_slices, geometry.n_angles,
                               geometry.n_bins, float(geometry.bin_spacing),
                               float(geometry.pixel_size),
-                              ctypes.cast(self._angles, ctypes.POINTER(ctypes.c_double)))
+                              ctypes.cast(self._angles, ctypes.POINTER(ctypes.c_double)), r0, rt)
         handle = ctypes.c_void_p()
         N.check(lib.pt_plan_create(ctypes.byref(desc), ctypes.byref(handle)), "plan")
         self.handle = handle
@@ -112,17 +117,19 @@ _plans: "OrderedDict[tuple, Plan]" = OrderedDict()
 _plans_lock = threading.Lock()
 
 
-def get_plan(geometry: ParallelGeometry, width: int, height: int, n_slices: int = 1) -> Plan:
+def get_plan(geometry: ParallelGeometry, width: int, height: int, n_slices: int = 1,
+             row_slab: tuple | None = None) -> Plan:
     """lru_cache(maxsize=8) over (geometry, grid), like projector.py:100-102;
     plans hold device tables, so the current CUDA device is part of the key."""
     device = torch.cuda.current_device() if torch.cuda.is_available() else -1
-    key = (geometry, int(width), int(height), int(n_slices), device)
+    row_slab = None if row_slab is None else (int(row_slab[0]), int(row_slab[1]))
+    key = (geometry, int(width), int(height), int(n_slices), row_slab, device)
     with _plans_lock:
         plan = _plans.get(key)
         if plan is not None:
             _plans.move_to_end(key)
             return plan
-    plan = Plan(geometry, width, height, n_slices)
+    plan = Plan(geometry, width, height, n_slices, row_slab)
     with _plans_lock:
         _plans[key] = plan
         while len(_plans) > 8:
@@ -179,11 +186,21 @@ class Projector:
     (projector.py:143-167).  ``n_slices > 1`` = slice-stacked 3D volume
     (rotation about z), images (Z, H, W), sinograms (A, Z, B)."""
 
-    def __init__(self, geometry: ParallelGeometry, width: int, height: int, n_slices: int = 1):
+    def __init__(self, geometry: ParallelGeometry, width: int, height: int, n_slices: int = 1,
+                 row_slab: tuple | None = None):
         self.geometry = geometry
         self.width = int(width)
         self.height = int(height)
         self.n_slices = int(n_slices)
+        # (row_offset, rows_total): this grid is rows [row_offset, row_offset +
+        # height) of a rows_total-row image; forward gives the slab's partial
+        # line integrals (they add up over the slabs), adjoint the slab's rows
+        self.row_slab = None
+        if row_slab is not None:
+            r0, rt = int(row_slab[0]), int(row_slab[1])
+            if self.n_slices != 1 or r0 < 0 or r0 + self.height > rt:
+                raise ValueError("row slab outside the image (or not 2D)")
+            self.row_slab = (r0, rt)
 
     @property
     def shape(self) -> tuple:
@@ -193,23 +210,40 @@ class Projector:
 
     @property
     def plan(self) -> Plan:
-        return get_plan(self.geometry, self.width, self.height, self.n_slices)
+        return get_plan(self.geometry, self.width, self.height, self.n_slices, self.row_slab)
 
     def forward(self, image, subset=None) -> torch.Tensor:
         x = as_device(image)
         if tuple(x.shape) != self.shape:
             raise ValueError(f"image shape {tuple(x.shape)} does not match grid {self.shape}")
-        return forward_project(x, self.geometry, subset)
+        if self.row_slab is None:
+            return forward_project(x, self.geometry, subset)
+        subset = _check_subset(subset, self.geometry.n_angles)
+        plan = self.plan
+        n_rows = self.geometry.n_angles if subset is None else len(subset)
+        y = torch.empty(plan.sino_shape(n_rows), device="cuda", dtype=torch.float32)
+        plan.forward_into(x, y, subset)
+        return y
 
     def adjoint(self, sino, subset=None) -> torch.Tensor:
-        return back_project(sino, self.geometry, self.shape, subset)
+        if self.row_slab is None:
+            return back_project(sino, self.geometry, self.shape, subset)
+        y = as_device(sino)
+        subset = _check_subset(subset, self.geometry.n_angles)
+        n_rows = self.geometry.n_angles if subset is None else len(subset)
+        if tuple(y.shape) != (n_rows, self.geometry.n_bins):
+            raise ValueError(f"sinogram shape {tuple(y.shape)} does not match "
+                             f"{(n_rows, self.geometry.n_bins)}")
+        out = torch.empty(self.shape, device="cuda", dtype=torch.float32)
+        self.plan.adjoint_into(y, out, subset)
+        return out
 
     def norm_sq(self, iterations: int = 100, seed: int = 0) -> float:
         return operator_norm_sq(self.geometry, self.width, self.height,
                                 iterations=iterations, seed=seed, n_slices=self.n_slices)
 
     def __reduce__(self):
-        return (Projector, (self.geometry, self.width, self.height, self.n_slices))
+        return (Projector, (self.geometry, self.width, self.height, self.n_slices, self.row_slab))
 
 
 def operator_norm_sq(geometry: ParallelGeometry, width: int, height: int,

@@ -213,17 +213,20 @@ class IterateState:
     denoiser_calls: int = 0
     work_seconds: float = 0.0
     zslab: tuple | None = None  # (z0, z1, Z) when this rank holds a z-slab
+    rowslab: tuple | None = None  # (r0, r1, H) when this rank holds image rows
 
     @property
     def x(self) -> torch.Tensor:
         return self.session.x
 
     def full_x(self) -> torch.Tensor:
-        """The whole iterate (a z-slab rank gathers the other slabs)."""
-        if self.zslab is None:
-            return self.session.x
+        """The whole iterate (a z-slab / row-slab rank gathers the other slabs)."""
         from . import distributed as _dist
-        return _dist.gather_zslabs(self.session.x, self.zslab[2])
+        if self.zslab is not None:
+            return _dist.gather_zslabs(self.session.x, self.zslab[2])
+        if self.rowslab is not None:
+            return _dist.gather_rowslabs(self.session.x, self.rowslab[2])
+        return self.session.x
 
     @property
     def h(self) -> torch.Tensor:
@@ -284,13 +287,15 @@ class RunRecord:
 
 
 def _init_state(config: SolverConfig, problem: TomoProblem, x0, stream=None,
-                data_parallel: bool = False, zslab: tuple | None = None) -> IterateState:
+                data_parallel: bool = False, zslab: tuple | None = None,
+                rowslab: tuple | None = None) -> IterateState:
     """solvers.py:159-186: x0 (or zeros), h = 0, three PCG64 streams, the
     staggered partition, SAGA zeros, SVRG initial snapshot (+1 pass).
 
     data_parallel: shard the angles over the torch.distributed ranks (one GPU
     each; the library's own NCCL communicator, see distributed.py); with
-    `zslab` = (z0, z1, Z) the problem is this rank's z-slab instead."""
+    `zslab` = (z0, z1, Z) / `rowslab` = (r0, r1, H) the problem is this
+    rank's z-slab / image rows instead."""
     shape = problem.projector.shape
     if x0 is not None and tuple(x0.shape) != tuple(shape):
         raise ValueError(f"x0 shape {tuple(x0.shape)} does not match grid {shape}")
@@ -304,13 +309,17 @@ def _init_state(config: SolverConfig, problem: TomoProblem, x0, stream=None,
     if zslab is not None:
         from . import distributed as _dist
         _dist.attach_zslab(session, zslab[0], zslab[2])
+    elif rowslab is not None:
+        from . import distributed as _dist
+        _dist.attach_rows(session, rowslab[0], rowslab[2])
     elif data_parallel:
         from . import distributed as _dist
         _dist.attach(session)
     state = IterateState(session=session, partition=partition,
                          rng_subset=np.random.default_rng(streams[0]),
                          rng_theta=np.random.default_rng(streams[1]),
-                         rng_refresh=np.random.default_rng(streams[2]), zslab=zslab)
+                         rng_refresh=np.random.default_rng(streams[2]), zslab=zslab,
+                         rowslab=rowslab)
     if config.estimator in ("svrg", "lsvrg"):
         if config.estimator == "svrg":
             state.svrg_period = config.n_subsets
@@ -452,18 +461,30 @@ def _metrics_row(passes, wall, x, reference, ground_truth, prox_calls, problem,
 
 def run(config: SolverConfig, problem: TomoProblem, x0=None, reference=None,
         ground_truth=None, record_objective: bool = False, stream=None,
-        data_parallel: bool = False) -> RunRecord:
+        data_parallel: bool = False, decomposition: str = "rows") -> RunRecord:
     """Run the skip-capable loop until tolerance or budget exhaustion (:327-336).
 
     Rows are logged at every data-pass boundary exactly as :280-324; the
     iterations between two rows are one native segment.  The host syncs only
     at rows that need a metric (or for a time budget) and at the end.
     data_parallel=True shards the work over the torch.distributed ranks (every
-    rank calls run with the same arguments): the projection angles of a 2D
-    problem, the z-slabs of a slice-stacked 3D one (the returned image is the
-    gathered volume on every rank)."""
+    rank calls run with the same arguments): the image rows (decomposition
+    "rows", default) or the projection angles ("sectors") of a 2D problem, the
+    z-slabs of a slice-stacked 3D one (the returned image is the gathered
+    image / volume on every rank)."""
+    if decomposition not in ("rows", "sectors"):
+        raise ValueError("decomposition must be 'rows' or 'sectors'")
     stream = stream if stream is not None else torch.cuda.current_stream()
-    work, zs = problem, None
+    work, zs, rs = problem, None, None
+    if (data_parallel and decomposition == "rows"
+            and getattr(problem.projector, "n_slices", 1) == 1):
+        import torch.distributed as dist
+        from . import distributed as _dist
+        H = problem.projector.height
+        r0, r1 = _dist.rowslab_bounds(H, dist.get_rank(), dist.get_world_size())
+        work, rs = _dist.rowslab_problem(problem, r0, r1), (r0, r1, H)
+        if x0 is not None:
+            x0 = as_device(x0)[r0:r1].contiguous()
     if data_parallel and getattr(problem.projector, "n_slices", 1) > 1:
         import torch.distributed as dist
         from . import distributed as _dist
@@ -473,7 +494,8 @@ def run(config: SolverConfig, problem: TomoProblem, x0=None, reference=None,
         if x0 is not None:
             x0 = as_device(x0)[z0:z1].contiguous().reshape(work.projector.shape)
     with torch.cuda.stream(stream):
-        state = _init_state(config, work, x0, stream, data_parallel=data_parallel, zslab=zs)
+        state = _init_state(config, work, x0, stream, data_parallel=data_parallel, zslab=zs,
+                            rowslab=rs)
         return _run_loop(state, config, problem, reference, ground_truth, record_objective,
                          stream)
 
@@ -557,7 +579,7 @@ def _bad_iteration(state: IterateState) -> int | None:
     """First non-finite iteration (z-slab ranks: the minimum over ranks, so
     every rank raises together)."""
     bad = state.session.bad_iteration()
-    if state.zslab is None:
+    if state.zslab is None and state.rowslab is None:
         return bad
     import torch.distributed as dist
     t = torch.tensor([INT64_MAX if bad is None else bad], device="cuda", dtype=torch.int64)
