@@ -231,3 +231,150 @@ def test_zslab_logic_and_halo_protocol_over_gloo(world):
         res = results[r]
         assert res["tiles"] and res["slab_ok"] and res["gather_ok"], res
         assert res["fgp_err_0"] <= 1e-12 and res["fgp_err_1"] <= 1e-12, res
+
+
+# ---------------------------------------------------------------------------
+# image-row decomposition (2D): host logic and the protocols of the native
+# rows mode, restated in numpy over a gloo world
+# ---------------------------------------------------------------------------
+
+def _exchange_rows(own, lo_g, hi_g, rank, world):
+    """Own rows -> extended array with lo_g / hi_g ghost rows from the ranks
+    -+ 1 (the native rows halo: first / last own rows sent, ghosts received)."""
+    import torch
+    hl, W = own.shape
+    ext = np.zeros((lo_g + hl + hi_g, W))
+    ext[lo_g:lo_g + hl] = own
+    reqs, bufs = [], []
+    if rank > 0:
+        reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(own[:lo_g])), rank - 1))
+        bufs.append(("lo", torch.empty((lo_g, W), dtype=torch.float64)))
+        reqs.append(dist.irecv(bufs[-1][1], rank - 1))
+    if rank < world - 1:
+        reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(own[hl - hi_g:])), rank + 1))
+        bufs.append(("hi", torch.empty((hi_g, W), dtype=torch.float64)))
+        reqs.append(dist.irecv(bufs[-1][1], rank + 1))
+    for r in reqs:
+        r.wait()
+    for side, t in bufs:
+        if side == "lo":
+            ext[:lo_g] = t.numpy()
+        else:
+            ext[lo_g + hl:] = t.numpy()
+    return ext
+
+
+def _row_fgp(v_own, r0, H, lam, inner, nonneg, rank, world, T=4):
+    """Row-slab FGP: T iterations per launch on own rows + T+1 ghost rows a
+    side (fewer at the image edge), ghosts refreshed before every launch."""
+    G = T + 1
+    hl, W = v_own.shape
+    lo_g = G if rank > 0 else 0
+    hi_g = G if rank < world - 1 else 0
+    gi = (r0 - lo_g + np.arange(lo_g + hl + hi_g))[:, None]  # image rows of the extended array
+    jj = np.arange(W)[None, :]
+
+    def dt(a, b):
+        up = np.zeros_like(a); up[1:] = a[:-1]
+        left = np.zeros_like(b); left[:, 1:] = b[:, :-1]
+        return (-a * (gi < H - 1) + up * (gi > 0)) - b * (jj < W - 1) + left * (jj > 0)
+
+    def grad(u):
+        gv = np.zeros_like(u); gv[:-1] = u[1:] - u[:-1]
+        gh = np.zeros_like(u); gh[:, :-1] = u[:, 1:] - u[:, :-1]
+        return gv * (gi < H - 1), gh * (jj < W - 1)
+
+    own = slice(lo_g, lo_g + hl)
+    v = _exchange_rows(v_own, lo_g, hi_g, rank, world)
+    p_own = np.zeros((hl, W)); q_own = np.zeros((hl, W))
+    r_own, s_own = p_own, q_own
+    eta, t, done = 1.0 / (8.0 * lam), 1.0, 0
+    while done < inner:
+        p, q, r, s = (_exchange_rows(a, lo_g, hi_g, rank, world)
+                      for a in (p_own, q_own, r_own, s_own))
+        for _ in range(min(T, inner - done)):
+            u = v - lam * dt(r, s)
+            if nonneg:
+                u = np.maximum(u, 0.0)
+            gv, gh = grad(u)
+            ph, qh = r + eta * gv, s + eta * gh
+            nrm = np.maximum(1.0, np.sqrt(ph * ph + qh * qh))
+            pn, qn = ph / nrm, qh / nrm
+            tn = (1.0 + np.sqrt(1.0 + 4.0 * t * t)) / 2.0
+            beta = (t - 1.0) / tn
+            t = tn
+            r, s = pn + beta * (pn - p), qn + beta * (qn - q)
+            p, q = pn, qn
+            done += 1
+        p_own, q_own, r_own, s_own = p[own], q[own], r[own], s[own]
+    p, q = (_exchange_rows(a, lo_g, hi_g, rank, world) for a in (p_own, q_own))
+    x = v - lam * dt(p, q)
+    return (np.maximum(x, 0.0) if nonneg else x)[own]
+
+
+def _rworker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch
+        import oracle as O
+        from paper_2602_09527_b200 import Projector, TomoProblem, TvProxConfig
+        from paper_2602_09527_b200.distributed import (gather_rowslabs, rowslab_bounds,
+                                                       rowslab_problem)
+        out = {}
+        H, W = 29, 17
+        r0, r1 = rowslab_bounds(H, rank, world)
+        spans = [rowslab_bounds(H, g, world) for g in range(world)]
+        out["tiles"] = spans[0][0] == 0 and spans[-1][1] == H and all(
+            spans[g][1] == spans[g + 1][0] for g in range(world - 1))
+        # the slab problem: a row-slab projector over the whole sinogram
+        g = ParallelGeometry.uniform(12, 25)
+        data = np.arange(12 * 25, dtype=np.float64).reshape(12, 25)
+        sp = rowslab_problem(TomoProblem(Projector(g, W, H), data, tv=TvProxConfig(alpha=0.1)),
+                             r0, r1)
+        out["slab_ok"] = (sp.projector.shape == (r1 - r0, W)
+                          and sp.projector.row_slab == (r0, H) and sp.data is data)
+        img = torch.arange(H * W, dtype=torch.float32).reshape(H, W)
+        out["gather_ok"] = bool(torch.equal(gather_rowslabs(img[r0:r1].clone(), H), img))
+        # forward protocol: own-row partial line integrals summed over ranks
+        rng = np.random.default_rng(4)
+        x = rng.random((H, W))
+        mask = np.zeros((H, W)); mask[r0:r1] = 1.0
+        part = torch.from_numpy(O.forward_project(x * mask, g, None))
+        dist.all_reduce(part)
+        full = O.forward_project(x, g, None)
+        out["fwd_err"] = float(np.abs(part.numpy() - full).max() / np.abs(full).max())
+        # adjoint protocol: each rank's rows of the whole adjoint of the full residual
+        res = rng.standard_normal((12, 25))
+        adj = O.back_project(res, g, (H, W), None)
+        out["adj_rows"] = adj[r0:r1].shape == (r1 - r0, W)
+        # TV prox: the ghost-row protocol = the whole-image FGP
+        v = rng.standard_normal((H, W))
+        for nn in (False, True):
+            xs = _row_fgp(v[r0:r1], r0, H, 0.3, 13, nn, rank, world)
+            xt = gather_rowslabs(torch.from_numpy(xs), H).numpy()
+            xo, _ = O.tv_prox(v, 1.0, 0.3, 13, nn)
+            out[f"fgp_err_{int(nn)}"] = float(np.abs(xt - xo).max())
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_rows_logic_and_protocols_over_gloo(world):
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rworker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        res = results[r]
+        assert res["tiles"] and res["slab_ok"] and res["gather_ok"] and res["adj_rows"], res
+        assert res["fwd_err"] <= 1e-13, res
+        assert res["fgp_err_0"] <= 1e-12 and res["fgp_err_1"] <= 1e-12, res
