@@ -443,7 +443,17 @@ __global__ void __launch_bounds__(256) fwd_reduce_kernel(RedArgs P)
         const float* pp = P.partial + idx;
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
         int band = 0;
-#pragma unroll 4
+        // 16 loads in flight before the first add (the partials sit in L2);
+        // the same accumulator assignment and order as the 4-band loop below
+        for (; band + 16 <= nb; band += 16) {
+            float v[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = __ldcs(pp + (size_t)(band + i) * stride);
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) {
+                s0 += v[i]; s1 += v[i + 1]; s2 += v[i + 2]; s3 += v[i + 3];
+            }
+        }
         for (; band + 4 <= nb; band += 4) {
             const float a = __ldcs(pp + (size_t)band * stride);
             const float b2 = __ldcs(pp + (size_t)(band + 1) * stride);
