@@ -427,14 +427,31 @@ int64_t fgp_workspace_floats(const pt_plan* plan)
     return 8 * (int64_t)plan->H * plan->W;
 }
 
-// inner iterations per launch of the 64 x 64 regions (PT_FGP_T, default 8)
-static int fgp2d_tmax()
+// 64 x 64 regions (T up to 8) unless the image is tiny, then 32 x 32 (T = 3)
+// (PT_FGP_BIG_MIN: the smallest min(H, W) that uses 64 x 64 regions).
+// FGP-100 measured: 128^2 153 vs 170 us, 256^2 157 us with 64 x 64 regions.
+static bool fgp2d_big(int H, int W)
 {
-    static const int tmax = [] {
-        const char* e = getenv("PT_FGP_T");
-        return e ? std::max(1, std::min(8, atoi(e))) : 8;
+    static const int big_min = [] {
+        const char* e = getenv("PT_FGP_BIG_MIN");
+        return e ? atoi(e) : 64;
     }();
-    return tmax;
+    return std::min(H, W) >= big_min;
+}
+
+// inner iterations per launch of the 64 x 64 regions (PT_FGP_T overrides).
+// The result does not depend on T (exact points only), the time does, through
+// launches x ragged last regions x waves; measured FGP-100: 512^2 T = 6/7/8:
+// 175/162/200 us; 1024^2: 412/390/376 us; 2048^2: 1.19/1.065/1.056 ms.
+static int fgp2d_tmax(int H, int W)
+{
+    static const int env = [] {
+        const char* e = getenv("PT_FGP_T");
+        return e ? std::max(1, std::min(8, atoi(e))) : 0;
+    }();
+    if (env) return env;
+    const int m = std::min(H, W);
+    return (m >= 384 && m < 768) ? 7 : 8;
 }
 
 template <int RW, int RH, int STRIP>
@@ -644,9 +661,9 @@ int fgp2d_rows_run(const Fgp2Slab* sl, int G, int H, int W, double lam, int inne
         }
     }
     // the whole-image tile choice (launch_tv_prox), so T and tiles match
-    if (std::min(H, W) >= 256)
+    if (fgp2d_big(H, W))
         return fgp2d_rows_run_t<64, 64, 8>(sl, G, H, W, lam, inner, nonneg, pog, iteration,
-                                           bad_iter, halo, fgp2d_tmax(), st);
+                                           bad_iter, halo, fgp2d_tmax(H, W), st);
     return fgp2d_rows_run_t<32, 32, 8>(sl, G, H, W, lam, inner, nonneg, pog, iteration, bad_iter,
                                        halo, 3, st);
 }
@@ -1627,9 +1644,10 @@ int launch_tv_prox(pt_plan* plan, const float* v, double lam, int inner, int non
         return fgp3d_run(&sl, 1, plan->H, plan->W, plan->Z, lam, inner, nonneg, p_over_gamma,
                          iteration, bad_iter, nullptr, plan->sm_count, st);
     }
-    if (std::min(plan->H, plan->W) >= 256)
+    if (fgp2d_big(plan->H, plan->W))
         return run_fgp2d<64, 64, 8>(plan, v, lam, inner, nonneg, p, q, x_out, xhat, h,
-                                    p_over_gamma, iteration, bad_iter, work, st, fgp2d_tmax());
+                                    p_over_gamma, iteration, bad_iter, work, st,
+                                    fgp2d_tmax(plan->H, plan->W));
     return run_fgp2d<32, 32, 8>(plan, v, lam, inner, nonneg, p, q, x_out, xhat, h,
                                 p_over_gamma, iteration, bad_iter, work, st, 3);
 }
