@@ -729,6 +729,41 @@ __device__ __forceinline__ void step_epilogue_vals(const pt_step_epilogue& ep, s
     }
 }
 
+// Gather epilogue kinds (compile-time): 0 plain adjoint, 1 full/sgd, 2 saga,
+// 3 svrg/lsvrg; the number of operand planes prefetched for each
+__host__ __device__ constexpr int epi_planes(int epi)
+{
+    return epi == 0 ? 0 : epi == 1 ? 2 : epi == 2 ? 4 : 3;
+}
+
+// step_epilogue_vals with the estimator class fixed at compile time (the
+// per-pixel epilogue of the gather; same expressions, same operation order)
+template <int EPI>
+__device__ __forceinline__ void step_epilogue_k(const pt_step_epilogue& ep, size_t p, float g,
+                                                float xv, float hv, float a0v, float a1v)
+{
+    float est;
+    if (EPI == 1) {
+        est = ep.estimator == PT_EST_FULL ? g : ep.n_scale * g;
+    } else if (EPI == 2) {
+        est = ep.n_scale * g + (a1v - ep.n_scale * a0v);
+        ep.aux1[p] = (a1v - a0v) + g;
+        ep.aux0[p] = g;
+    } else {
+        est = ep.n_scale * g + a0v;
+    }
+    const float base = xv - ep.gamma * est;
+    const float xh = base + ep.gamma * hv;
+    if (ep.theta) {
+        ep.v_out[p] = base + ep.hcoef * hv;
+        ep.xhat_out[p] = xh;
+    } else {
+        ep.x_out[p] = xh;
+        if (!isfinite(xh) && ep.bad_iter)
+            atomicMin((long long*)ep.bad_iter, (long long)ep.iteration);
+    }
+}
+
 __device__ __forceinline__ void step_epilogue(const pt_step_epilogue& ep, size_t p, float g)
 {
     const bool saga = ep.estimator == PT_EST_SAGA;
@@ -737,10 +772,11 @@ __device__ __forceinline__ void step_epilogue(const pt_step_epilogue& ep, size_t
                        saga ? ep.aux1[p] : 0.f);
 }
 
-template <int TR, int TC, int NT, int NA, bool TWO_TAP>
+template <int TR, int TC, int NT, int NA, bool TWO_TAP, int EPI>
 __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_kernel(AdjArgs P)
 {
     constexpr int PIX = TR * TC / NT;  // pixels per thread
+    constexpr int NEPI = epi_planes(EPI);
     constexpr int ROWSTEP = NT / TC;
     constexpr int NW = NT / 32;
     extern __shared__ float smem[];
@@ -762,14 +798,31 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
     const uint32_t epi_u32 = stage_u32 + (uint32_t)(P.nbuf * NA * P.slot) * 4u;
 
     // --- epilogue operands: prefetched with cp.async, consumed at the end ---
-    if (P.n_epi) {
+    if (NEPI) {
         const bool vec = (P.W % 4) == 0;  // 16-byte rows (c0 is a multiple of TC)
-        for (int e = 0; e < P.n_epi; ++e) {
+        constexpr int Q = TC / 4;          // 16-byte quads per tile row
+        static_assert(NT % Q == 0 && (TR * Q) % NT == 0, "epilogue prefetch shape");
+        if (vec && r0 + TR <= P.H && c0 + TC <= P.W) {
+            // whole tile inside the image: one 64-bit base per plane, 32-bit
+            // offsets stepping NT / Q rows per copy
+            const int rl0 = tid / Q, q = tid % Q;
+            const uint32_t off0 = (uint32_t)((r0 + rl0) * P.W + c0 + 4 * q);
+            const uint32_t dst0 = epi_u32 + (uint32_t)(rl0 * TC + 4 * q) * 4u;
+            const uint32_t dstep = (uint32_t)(NT / Q) * P.W;
+#pragma unroll
+            for (int e = 0; e < NEPI; ++e) {
+                const float* srcp = e == 0 ? P.ep.x : e == 1 ? P.ep.h : e == 2 ? P.ep.aux0 : P.ep.aux1;
+                const float* base = srcp + (size_t)z * plane;
+#pragma unroll
+                for (int k = 0; k < TR * Q / NT; ++k)
+                    cp_async16(dst0 + (uint32_t)(e * TR * TC + k * (NT / Q) * TC) * 4u,
+                               base + (off0 + (uint32_t)k * dstep), 16);
+            }
+        } else for (int e = 0; e < NEPI; ++e) {
             const float* srcp = e == 0 ? P.ep.x : e == 1 ? P.ep.h : e == 2 ? P.ep.aux0 : P.ep.aux1;
             const float* base = srcp + (size_t)z * plane;
             const uint32_t dst = epi_u32 + (uint32_t)(e * TR * TC) * 4u;
             if (vec) {
-                constexpr int Q = TC / 4;  // 16-byte quads per tile row
                 for (int idx = tid; idx < TR * Q; idx += NT) {
                     const int rl = idx / Q, q = idx - rl * Q;
                     const int r = r0 + rl, c = c0 + 4 * q;
@@ -902,8 +955,7 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
             f2 acc2[PIX / 2];
 #pragma unroll
             for (int jj = 0; jj < PIX / 2; ++jj) acc2[jj] = pk(0.f, 0.f);
-#pragma unroll 8
-            for (int a = 0; a < nc; ++a) {
+            auto angle = [&](int a) {
                 const float4 q4 = s_p4[buf][a];
                 const float2 q2 = s_p2[buf][a];
                 const float br = q4.x, S1 = q4.w;
@@ -929,7 +981,19 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
                     lds_pair(mad4(__float_as_uint(tb), yb), y0b, y1b);
                     acc2[jj] = fma2(w0, pk(y0a, y0b), fma2(w1, pk(y1a, y1b), acc2[jj]));
                 }
+            };
+            // 8 angles per trip (their shared-memory latencies overlap), then
+            // pairs: a subset chunk (30 angles at config 2) has no 1-angle tail loop
+            int a = 0;
+            for (; a + 8 <= nc; a += 8) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) angle(a + u);
             }
+            for (; a + 2 <= nc; a += 2) {
+                angle(a);
+                angle(a + 1);
+            }
+            if (a < nc) angle(a);
 #pragma unroll
             for (int jj = 0; jj < PIX / 2; ++jj) {
                 float a0, a1;
@@ -965,7 +1029,7 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
         }
         if (ci + 1 < n_chunks) __syncthreads();  // buffers are restaged next
     }
-    if (n_chunks == 0 && P.n_epi) {
+    if (n_chunks == 0 && NEPI) {
         cp_async_wait_all();
         __syncthreads();
     }
@@ -976,21 +1040,21 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
         return;
     }
     const float* epi = smem + P.nbuf * NA * P.slot;
+    const size_t p0 = (size_t)z * plane + (size_t)(r0 + rg) * P.W + c;
 #pragma unroll
     for (int j = 0; j < PIX; ++j) {
         const int rl = rg + j * ROWSTEP;
-        const int r = r0 + rl;
-        if (r >= P.H) continue;
-        const size_t p = (size_t)z * plane + (size_t)r * P.W + c;
-        if (P.mode == 0) {
+        if (r0 + rl >= P.H) continue;
+        const size_t p = p0 + (uint32_t)(j * ROWSTEP * P.W);
+        if (EPI == 0) {
             float v = P.alpha * acc_o[j];
             if (P.accumulate) v += P.out[p];
             P.out[p] = v;
         } else {
             const int e = rl * TC + cl;
-            step_epilogue_vals(P.ep, p, acc_o[j], epi[e], epi[TR * TC + e],
-                               P.n_epi > 2 ? epi[2 * TR * TC + e] : 0.f,
-                               P.n_epi > 3 ? epi[3 * TR * TC + e] : 0.f);
+            step_epilogue_k<EPI>(P.ep, p, acc_o[j], epi[e], epi[TR * TC + e],
+                                 NEPI > 2 ? epi[2 * TR * TC + e] : 0.f,
+                                 NEPI > 3 ? epi[3 * TR * TC + e] : 0.f);
         }
     }
     pdl_trigger();
@@ -1007,19 +1071,30 @@ __global__ void epilogue_kernel(const float* g, size_t n, pt_step_epilogue ep)
 
 static constexpr int kNT = 256, kNA = 32;
 
-template <int TR, int TC, bool TWO>
-static int run_gather_t(pt_plan* plan, const AdjArgs& a, cudaStream_t st)
+template <int TR, int TC, bool TWO, int EPI>
+static int run_gather_e(pt_plan* plan, const AdjArgs& a, cudaStream_t st)
 {
-    const size_t smem = (size_t)(a.nbuf * kNA * a.slot + a.n_epi * TR * TC) * sizeof(float);
+    const size_t smem = (size_t)(a.nbuf * kNA * a.slot + epi_planes(EPI) * TR * TC) * sizeof(float);
     {
-        const int rc = ensure_smem((const void*)adj_gather_kernel<TR, TC, kNT, kNA, TWO>, smem);
+        const int rc = ensure_smem((const void*)adj_gather_kernel<TR, TC, kNT, kNA, TWO, EPI>, smem);
         if (rc) return rc;
     }
     dim3 grid((plan->W + TC - 1) / TC, (plan->H + TR - 1) / TR, plan->Z);
-    PT_CHECK_CUDA(launch_pdl(adj_gather_kernel<TR, TC, kNT, kNA, TWO>, grid, dim3(kNT), smem, st,
-                             a));
+    PT_CHECK_CUDA(launch_pdl(adj_gather_kernel<TR, TC, kNT, kNA, TWO, EPI>, grid, dim3(kNT), smem,
+                             st, a));
     PT_CHECK_LAUNCH();
     return PT_OK;
+}
+
+template <int TR, int TC, bool TWO>
+static int run_gather_t(pt_plan* plan, const AdjArgs& a, cudaStream_t st)
+{
+    switch (a.mode == 0 ? 0 : a.n_epi == 2 ? 1 : a.n_epi == 4 ? 2 : 3) {
+        case 0: return run_gather_e<TR, TC, TWO, 0>(plan, a, st);
+        case 1: return run_gather_e<TR, TC, TWO, 1>(plan, a, st);
+        case 2: return run_gather_e<TR, TC, TWO, 2>(plan, a, st);
+        default: return run_gather_e<TR, TC, TWO, 3>(plan, a, st);
+    }
 }
 
 template <bool TWO>
