@@ -175,6 +175,40 @@ __device__ __forceinline__ void stage_tile(const FwdArgs& P, const FwdItem& it, 
     const int s0 = it.band * TY;
     const int lane_org = it.tile * TX - T::HL;
     const float* img = P.x + (size_t)it.z * P.H * P.W;
+    const int n_steps = it.branch ? P.W : P.H;
+    const int n_lanes = it.branch ? P.H : P.W;
+    if (s0 + TY <= n_steps && lane_org >= 0 && lane_org + T::NL <= n_lanes &&
+        (it.branch == 1 || (P.W & 3) == 0)) {
+        // interior tile (the common case): no bounds tests, one 64-bit base,
+        // 32-bit offsets, a warp per staged row
+        if (it.branch == 0) {
+            // [st][ll] = img[s0 + st][lane_org + ll], 16-byte copies
+            constexpr int NQ = T::NL / 4;
+            const float* src0 = img + ((size_t)s0 * P.W + lane_org);
+            for (int st = warp; st < TY; st += NW) {
+                const uint32_t so = (uint32_t)(st * P.W);
+                const uint32_t dst = buf + (uint32_t)(st * T::PITCH_R) * 4u;
+#pragma unroll
+                for (int u = 0; u < (NQ + 31) / 32; ++u) {
+                    const int q = lane + 32 * u;
+                    if (NQ % 32 == 0 || q < NQ) cp_async16(dst + 16u * q, src0 + (so + 4u * q), 16);
+                }
+            }
+        } else {
+            // [ll][st] = img[lane_org + ll][s0 + st], 4-byte copies into the odd pitch
+            const float* src0 = img + ((size_t)lane_org * P.W + s0);
+            for (int ll = warp; ll < T::NL; ll += NW) {
+                const uint32_t so = (uint32_t)(ll * P.W) + lane;
+                const uint32_t dst = buf + (uint32_t)(ll * T::PITCH_C + lane) * 4u;
+#pragma unroll
+                for (int u = 0; u < (TY + 31) / 32; ++u) {
+                    if (TY % 32 != 0 && lane + 32 * u >= TY) break;
+                    cp_async4(dst + 128u * u, src0 + (so + 32u * u), true);
+                }
+            }
+        }
+        return;
+    }
     if (it.branch == 0 && (P.W & 3) == 0) {
         // [st][ll] = img[s0 + st][lane_org + ll]: 16-byte copies (lane_org and
         // W are multiples of 4), zero-filled outside the image
@@ -233,30 +267,34 @@ __device__ __forceinline__ float ray_band_sum(uint32_t tile_u32, int st_a, int s
     // magic offset folded in (mod 2^32)
     uint32_t sbase = tile_u32 + (uint32_t)(st_a * SS) - (uint32_t)kMagicBits * (uint32_t)LS;
     const f2 pl2 = pk(pl, pl), m2 = pk(mf, mf), mg2 = pk(kMagic, kMagic);
-    const f2 two2 = pk(2.f, 2.f);
-    f2 st2 = pk((float)st_a, (float)st_a + 1.f);
+    const f2 eight2 = pk(8.f, 8.f);
+    // a trip = 8 samples as 4 packed pairs (s + u, s + u + 4), u = 0..3: the
+    // pair's positions are u*m + (pos(s), pos(s + 4)), so one FFMA2 per pair
+    // with a broadcast immediate and no per-pair step counter
+    f2 st2 = pk((float)st_a, (float)st_a + 4.f);
     f2 acc2 = pk(0.f, 0.f);
     const int n = st_b - st_a;
     int i = 0;
-    for (; i + 8 <= n; i += 8) {  // 8 samples per trip: 4 packed pairs
+    for (; i + 8 <= n; i += 8) {
         const uint32_t sb = opaque(sbase);
+        const f2 base2 = fma2(st2, m2, pl2);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const f2 pos = fma2(st2, m2, pl2);
+            const f2 pos = u == 0 ? base2 : fma2(pk((float)u, (float)u), m2, base2);
             const f2 t = add2_rm(pos, mg2);
             const f2 fr = sub2(pos, sub2(t, mg2));
             float ta, tb, a0, a1, b0, b1;
             upk(t, ta, tb);
-            const uint32_t aa = __float_as_uint(ta) * (uint32_t)LS + sb + (2 * u) * SS;
-            const uint32_t ab = __float_as_uint(tb) * (uint32_t)LS + sb + (2 * u + 1) * SS;
+            const uint32_t aa = __float_as_uint(ta) * (uint32_t)LS + sb + u * SS;
+            const uint32_t ab = __float_as_uint(tb) * (uint32_t)LS + sb + (u + 4) * SS;
             asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+%3];"
                          : "=f"(a0), "=f"(a1) : "r"(aa), "n"(LS));
             asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+%3];"
                          : "=f"(b0), "=f"(b1) : "r"(ab), "n"(LS));
             const f2 x0 = pk(a0, b0), x1 = pk(a1, b1);
             acc2 = add2(acc2, fma2(fr, sub2(x1, x0), x0));
-            st2 = add2(st2, two2);
         }
+        st2 = add2(st2, eight2);
         sbase += 8 * SS;
     }
     float acc0, acc1;
