@@ -943,7 +943,7 @@ __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
             const float ph = rv(st, o) + a.eta * gv;
             const float qh = rv(st, ARR + o) + a.eta * gh;
             const float wh = rv(st, 2 * ARR + o) + a.eta * gz;
-            const float n2 = ph * ph + qh * qh + wh * wh;
+            const float n2 = fmaf(wh, wh, fmaf(qh, qh, __fmul_rn(ph, ph)));  // pinned order (all 3D paths)
             const float inv = (n2 > 1.f) ? rsqrt_ftz(n2) : 1.f;
             const float p0 = ph * inv, p1 = qh * inv, p2 = wh * inv;
             const int g = gi * W + gj;
@@ -980,6 +980,10 @@ __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
 // ---------------------------------------------------------------------------
 template <int TX, int TY, int NT_>
 struct Fgp3Pair {
+    // X2 path: x-adjacent point pairs (even columns) per thread, f32x2 math
+    static constexpr int CP_AB = TX / 2 + 2, CP_C = TX / 2 + 1, CP_D = TX / 2;
+    static constexpr int NPA = (TY + 3) * CP_AB, NPB = (TY + 2) * CP_AB;
+    static constexpr int NPC = (TY + 1) * CP_C, NPD = TY * CP_D;
     static constexpr int NT = NT_;
     static constexpr int NS = 3;
     static constexpr int SW = TX + 8, SR = TY + 4, SA = SR * SW;  // window (all arrays)
@@ -995,12 +999,44 @@ struct Fgp3Pair {
     static constexpr int SMEM_FLOATS = UK1O + 2 * SA;
     static constexpr int KA = (NA + NT - 1) / NT, KB = (NB + NT - 1) / NT, KC = (NC + NT - 1) / NT;
     static constexpr int KD = TX * TY / NT;
+    static constexpr int KA2 = (NPA + NT - 1) / NT, KB2 = (NPB + NT - 1) / NT;
+    static constexpr int KC2 = (NPC + NT - 1) / NT, KD2 = (NPD + NT - 1) / NT;
     static constexpr uint32_t TMA_BYTES = 7u * SA * 4u;
 };
 
+__device__ __forceinline__ f2 ld2s(const float* p)
+{
+    const float2 v = *reinterpret_cast<const float2*>(p);
+    return pk(v.x, v.y);
+}
+__device__ __forceinline__ void st2s(float* p, f2 v)
+{
+    float2 w;
+    upk(v, w.x, w.y);
+    *reinterpret_cast<float2*>(p) = w;
+}
+// the one-point kernels' clamp (nonneg: u < 0 -> 0, NaN kept) per lane
+__device__ __forceinline__ f2 clamp2(f2 u, bool nonneg, bool in)
+{
+    float a, b;
+    upk(u, a, b);
+    if (nonneg) {
+        a = (a < 0.f) ? 0.f : a;
+        b = (b < 0.f) ? 0.f : b;
+    }
+    return in ? pk(a, b) : pk(0.f, 0.f);
+}
+// (n2 > 1 ? rsqrt(n2) : 1) per lane
+__device__ __forceinline__ f2 inv_norm2(f2 n2)
+{
+    float a, b;
+    upk(n2, a, b);
+    return pk((a > 1.f) ? rsqrt_ftz(a) : 1.f, (b > 1.f) ? rsqrt_ftz(b) : 1.f);
+}
+
 // Fgp3Args use: R = P_k set, P = P_{k-1} set, Pn = P_{k+1} set, Rn = P_{k+2}
 // set; beta_r = beta_{k-1} (forms R_k), beta = beta_k (forms R_{k+1}).
-template <int TX, int TY, int NT_>
+template <int TX, int TY, int NT_, bool X2>
 __global__ void __launch_bounds__(NT_, 2)
     fgp3d_pair_kernel(Fgp3Args a, const __grid_constant__ Fgp3Maps m)
 {
@@ -1082,9 +1118,62 @@ __global__ void __launch_bounds__(NT_, 2)
         const int idx = tid + k * NT;
         ptC[k] = idx < T::NC ? pack(idx / (TX + 1), idx % (TX + 1)) : -1;
     }
+    // X2: pair descriptors (offset of the even point | 16: i < H-1 | 17: i > 0 |
+    // 20: inside the image | 21: the odd point is column W-1); -1 = none.  W is
+    // even (TMA), so a pair never straddles the image's x edges.
+    auto pack2 = [&](int r, int c) -> int {
+        const int gi = i0 + r, gj = j0 + c;
+        const bool in = gi >= 0 && gi < H && gj >= 0 && gj < W;
+        return ((r + 2) * SW + (c + 4)) | ((int)(gi < H - 1) << 16) | ((int)(gi > 0) << 17) |
+               ((int)in << 20) | ((int)(gj == W - 2) << 21);
+    };
+    int qA[T::KA2], qB[T::KB2], qC[T::KC2], qD[T::KD2], hB[T::KB2], hD[T::KD2];
+    if constexpr (X2) {
+#pragma unroll
+        for (int k = 0; k < T::KA2; ++k) {
+            const int idx = tid + k * NT;
+            qA[k] = idx < T::NPA ? pack2(idx / T::CP_AB - 1, 2 * (idx % T::CP_AB) - 2) : -1;
+        }
+#pragma unroll
+        for (int k = 0; k < T::KB2; ++k) {
+            const int idx = tid + k * NT;
+            const int r = idx / T::CP_AB - 1, c = 2 * (idx % T::CP_AB) - 2;
+            qB[k] = idx < T::NPB ? pack2(r, c) : -1;
+            const bool centre = idx < T::NPB && r >= 0 && r < TY && c >= 0 && c < TX &&
+                                i0 + r < H && j0 + c < W;
+            hB[k] = centre ? (i0 + r) * W + (j0 + c) : -1;
+        }
+#pragma unroll
+        for (int k = 0; k < T::KC2; ++k) {
+            const int idx = tid + k * NT;
+            qC[k] = idx < T::NPC ? pack2(idx / T::CP_C, 2 * (idx % T::CP_C)) : -1;
+        }
+#pragma unroll
+        for (int k = 0; k < T::KD2; ++k) {
+            const int idx = tid + k * NT;
+            const int r = idx / T::CP_D, c = 2 * (idx % T::CP_D);
+            const bool ok = idx < T::NPD && i0 + r < H && j0 + c < W;
+            qD[k] = ok ? pack2(r, c) : -1;
+            hD[k] = ok ? (i0 + r) * W + (j0 + c) : -1;
+        }
+    }
     const int tx = tid % TX, ty = tid / TX;
     const float lam = a.lam, eta = a.eta, br = a.beta_r, bk = a.beta;
     const bool nonneg = a.nonneg != 0;
+    const f2 br2 = pk(br, br), bk2 = pk(bk, bk), eta2 = pk(eta, eta), nlam2 = pk(-lam, -lam);
+    const f2 z2 = pk(0.f, 0.f), nz2 = pk(-0.f, -0.f);
+    // D^T of a pair in the one-point order: x = -a0 [i < H-1]; + a1 [i > 0];
+    // - a2 [j < W-1, the odd point of the last pair skips it: x + (-0) a2];
+    // + a3 (j > 0: at j = 0 a3 is the zero-filled column -1); - a4 [z]; + a5 [z]
+    auto divT2 = [&](int q, f2 a0, f2 a1, f2 a2, f2 a3, f2 a4, f2 a5, bool zhi, bool zlo) -> f2 {
+        f2 x = (q & (1 << 16)) ? sub2(nz2, a0) : z2;
+        if (q & (1 << 17)) x = add2(x, a1);
+        x = fma2(a2, (q & (1 << 21)) ? pk(-1.f, -0.f) : pk(-1.f, -1.f), x);
+        x = add2(x, a3);
+        if (zhi) x = sub2(x, a4);
+        if (zlo) x = add2(x, a5);
+        return x;
+    };
     const float* sUK = fsm + T::UKO;
     const float* sRK = fsm + T::RKO;
     const float* sUK1 = fsm + T::UK1O;
@@ -1131,6 +1220,25 @@ __global__ void __launch_bounds__(NT_, 2)
             const float* st = fsm + c2 * T::STAGE;
             const float* st1 = fsm + c1 * T::STAGE;
             float* U = fsm + T::UKO + (pA & 1) * SA;
+            if constexpr (X2) {
+                auto rk2 = [&](const float* sp, int o) -> f2 {
+                    const f2 pv = ld2s(sp + o);
+                    return fma2(sub2(pv, ld2s(sp + T::QOFF + o)), br2, pv);
+                };
+#pragma unroll
+                for (int k = 0; k < T::KA2; ++k) {
+                    const int q = qA[k];
+                    if (q < 0) continue;
+                    const int o = q & 0xffff;
+                    const f2 a2 = rk2(st, SA + o);
+                    const float pm = st[SA + o - 1];
+                    const float rm = fmaf(pm - st[T::QOFF + SA + o - 1], br, pm);
+                    const f2 x = divT2(q, rk2(st, o), rk2(st, o - SW), a2, pk(rm, lo_of(a2)),
+                                       rk2(st, 2 * SA + o), rk2(st1, 2 * SA + o), zhi, zlo);
+                    st2s(U + o, clamp2(fma2(x, nlam2, ld2s(st + T::VOFF + o)), nonneg,
+                                       (q & (1 << 20)) != 0));
+                }
+            } else
 #pragma unroll
             for (int k = 0; k < T::KA; ++k) {
                 const int pt = ptA[k];
@@ -1154,6 +1262,35 @@ __global__ void __launch_bounds__(NT_, 2)
                 const float* U1 = sUK + ((pB + 1) & 1) * SA;
                 float* R1 = fsm + T::RKO + (pB & 1) * 3 * SA;
                 float* __restrict__ pn = a.Pn + ((size_t)(pB + 1) * 3) * HW;
+                if constexpr (X2) {
+#pragma unroll
+                    for (int k = 0; k < T::KB2; ++k) {
+                        const int q = qB[k];
+                        if (q < 0) continue;
+                        const int o = q & 0xffff;
+                        const f2 uo = ld2s(U0 + o);
+                        const f2 gv = (q & (1 << 16)) ? sub2(ld2s(U0 + o + SW), uo) : z2;
+                        const f2 gh = sub2(pk(hi_of(uo), U0[o + 2]), uo);
+                        const f2 gz = top ? sub2(ld2s(U1 + o), uo) : z2;
+                        const f2 k0 = ld2s(st + o), k1 = ld2s(st + SA + o), k2 = ld2s(st + 2 * SA + o);
+                        const f2 ph = fma2(gv, eta2, fma2(sub2(k0, ld2s(st + T::QOFF + o)), br2, k0));
+                        const f2 qh = fma2(gh, (q & (1 << 21)) ? pk(eta, 0.f) : eta2,
+                                           fma2(sub2(k1, ld2s(st + T::QOFF + SA + o)), br2, k1));
+                        const f2 wh = fma2(gz, eta2,
+                                           fma2(sub2(k2, ld2s(st + T::QOFF + 2 * SA + o)), br2, k2));
+                        const f2 inv = inv_norm2(fma2(wh, wh, fma2(qh, qh, mul2(ph, ph))));
+                        const f2 p0 = mul2(ph, inv), p1 = mul2(qh, inv), p2 = mul2(wh, inv);
+                        const bool in = (q & (1 << 20)) != 0;
+                        st2s(R1 + o, in ? fma2(sub2(p0, k0), bk2, p0) : z2);
+                        st2s(R1 + SA + o, in ? fma2(sub2(p1, k1), bk2, p1) : z2);
+                        st2s(R1 + 2 * SA + o, in ? fma2(sub2(p2, k2), bk2, p2) : z2);
+                        if (own && hB[k] >= 0) {
+                            st2s(pn + hB[k], p0);
+                            st2s(pn + HW + hB[k], p1);
+                            st2s(pn + 2 * HW + hB[k], p2);
+                        }
+                    }
+                } else
 #pragma unroll
                 for (int k = 0; k < T::KB; ++k) {
                     const int pt = ptB[k];
@@ -1167,7 +1304,7 @@ __global__ void __launch_bounds__(NT_, 2)
                     const float ph = (k0 + br * (k0 - st[T::QOFF + o])) + eta * gv;
                     const float qh = (k1 + br * (k1 - st[T::QOFF + SA + o])) + eta * gh;
                     const float wh = (k2 + br * (k2 - st[T::QOFF + 2 * SA + o])) + eta * gz;
-                    const float n2 = ph * ph + qh * qh + wh * wh;
+                    const float n2 = fmaf(wh, wh, fmaf(qh, qh, __fmul_rn(ph, ph)));  // pinned order (all 3D paths)
                     const float inv = (n2 > 1.f) ? rsqrt_ftz(n2) : 1.f;
                     const float p0 = ph * inv, p1 = qh * inv, p2 = wh * inv;
                     const bool in = pt & (1 << 20);
@@ -1189,6 +1326,20 @@ __global__ void __launch_bounds__(NT_, 2)
                 const float* R0 = sRK + (pB & 1) * 3 * SA;
                 const float* Rm = sRK + ((pB - 1) & 1) * 3 * SA;
                 float* U = fsm + T::UK1O + (pB & 1) * SA;
+                if constexpr (X2) {
+#pragma unroll
+                    for (int k = 0; k < T::KC2; ++k) {
+                        const int q = qC[k];
+                        if (q < 0) continue;
+                        const int o = q & 0xffff;
+                        const f2 a2 = ld2s(R0 + SA + o);
+                        const f2 x = divT2(q, ld2s(R0 + o), ld2s(R0 + o - SW), a2,
+                                           pk(R0[SA + o - 1], lo_of(a2)), ld2s(R0 + 2 * SA + o),
+                                           ld2s(Rm + 2 * SA + o), zhi, zlo);
+                        st2s(U + o, clamp2(fma2(x, nlam2, ld2s(st + T::VOFF + o)), nonneg,
+                                           (q & (1 << 20)) != 0));
+                    }
+                } else
 #pragma unroll
                 for (int k = 0; k < T::KC; ++k) {
                     const int pt = ptC[k];
@@ -1208,6 +1359,25 @@ __global__ void __launch_bounds__(NT_, 2)
                 const float* U1 = sUK1 + ((pD + 1) & 1) * SA;
                 const float* R0 = sRK + (pD & 1) * 3 * SA;
                 float* __restrict__ pn2 = a.Rn + ((size_t)(pD + 1) * 3) * HW;
+                if constexpr (X2) {
+#pragma unroll
+                    for (int k = 0; k < T::KD2; ++k) {
+                        const int q = qD[k];
+                        if (q < 0) continue;
+                        const int o = q & 0xffff;
+                        const f2 uo = ld2s(U0 + o);
+                        const f2 gv = (q & (1 << 16)) ? sub2(ld2s(U0 + o + SW), uo) : z2;
+                        const f2 gh = sub2(pk(hi_of(uo), U0[o + 2]), uo);
+                        const f2 gz = top ? sub2(ld2s(U1 + o), uo) : z2;
+                        const f2 ph = fma2(gv, eta2, ld2s(R0 + o));
+                        const f2 qh = fma2(gh, (q & (1 << 21)) ? pk(eta, 0.f) : eta2, ld2s(R0 + SA + o));
+                        const f2 wh = fma2(gz, eta2, ld2s(R0 + 2 * SA + o));
+                        const f2 inv = inv_norm2(fma2(wh, wh, fma2(qh, qh, mul2(ph, ph))));
+                        st2s(pn2 + hD[k], mul2(ph, inv));
+                        st2s(pn2 + HW + hD[k], mul2(qh, inv));
+                        st2s(pn2 + 2 * HW + hD[k], mul2(wh, inv));
+                    }
+                } else
 #pragma unroll
                 for (int rr = 0; rr < T::KD; ++rr) {
                     const int r = ty + rr * (NT / TX), gi = i0 + r, gj = j0 + tx;
@@ -1220,7 +1390,7 @@ __global__ void __launch_bounds__(NT_, 2)
                     const float ph = R0[o] + eta * gv;
                     const float qh = R0[SA + o] + eta * gh;
                     const float wh = R0[2 * SA + o] + eta * gz;
-                    const float n2 = ph * ph + qh * qh + wh * wh;
+                    const float n2 = fmaf(wh, wh, fmaf(qh, qh, __fmul_rn(ph, ph)));  // pinned order (all 3D paths)
                     const float inv = (n2 > 1.f) ? rsqrt_ftz(n2) : 1.f;
                     const int g = gi * W + gj;
                     pn2[g] = ph * inv;
@@ -1421,13 +1591,13 @@ static int fgp3d_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
     return PT_OK;
 }
 
-template <int TX, int TY, int NT>
+template <int TX, int TY, int NT, bool X2>
 static int fgp3d_pair_launch(Fgp3Args& a, cudaStream_t st)
 {
     using T = Fgp3Pair<TX, TY, NT>;
     const size_t smem = (size_t)T::SMEM_FLOATS * 4;
     {
-        const int rc = ensure_smem((const void*)fgp3d_pair_kernel<TX, TY, NT>, smem);
+        const int rc = ensure_smem((const void*)fgp3d_pair_kernel<TX, TY, NT, X2>, smem);
         if (rc) return rc;
     }
     Fgp3Maps m;
@@ -1449,7 +1619,7 @@ static int fgp3d_pair_launch(Fgp3Args& a, cudaStream_t st)
     // 12.8 / 12.6 / 12.2 / 13.1 ms for runs of 16 / 24 / 32 / 64
     a.zchunk = zc_env ? zc_env : 32;
     const dim3 grid((a.W + TX - 1) / TX, (a.H + TY - 1) / TY, (a.Zl + a.zchunk - 1) / a.zchunk);
-    PT_CHECK_CUDA(launch_pdl(fgp3d_pair_kernel<TX, TY, NT>, grid, dim3(T::NT), smem, st, a, m));
+    PT_CHECK_CUDA(launch_pdl(fgp3d_pair_kernel<TX, TY, NT, X2>, grid, dim3(T::NT), smem, st, a, m));
     PT_CHECK_LAUNCH();
     return PT_OK;
 }
@@ -1522,8 +1692,13 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
             a.nonneg = nonneg;
             // 256^3 FGP-100: 12.2 ms (64 x 8 tiles, 256 threads, 32-plane runs);
             // 13.8 ms with 512 threads; 14.0 ms one iteration per pass
-            rc = pair_env == 2 ? fgp3d_pair_launch<64, 8, 512>(a, st)
-                               : fgp3d_pair_launch<64, 8, 256>(a, st);
+            // point pairs with f32x2 math (X2, PT_FGP3_PAIR=1): 12.3 -> 11.7 ms;
+            // 2 / 3 / 4 select one point per lane with 512 threads, X2 with
+            // 384 threads (11.7 ms), one point per lane with 256 threads
+            rc = pair_env == 2 ? fgp3d_pair_launch<64, 8, 512, false>(a, st)
+               : pair_env == 3 ? fgp3d_pair_launch<64, 8, 384, true>(a, st)
+               : pair_env == 4 ? fgp3d_pair_launch<64, 8, 256, false>(a, st)
+                               : fgp3d_pair_launch<64, 8, 256, true>(a, st);
             if (rc) return rc;
             sp = o1;
             sk = o1 + 1;

@@ -140,18 +140,19 @@ np.save(sys.argv[1], np.concatenate(out))
 
 
 def test_fgp_3d_pair_pass_bitwise(tmp_path):
-    """Two iterations per HBM pass (PT_FGP3_PAIR=1, the default for one slab)
-    give the same bits as one iteration per pass; odd counts, ragged tiles and
-    z-runs included."""
+    """Two iterations per HBM pass (PT_FGP3_PAIR=1 / 3: point pairs with f32x2
+    math, 2 / 4: one point per lane) give the same values as one iteration per
+    pass (0); odd counts, ragged tiles and z-runs included."""
     import os
     import subprocess
     import sys
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
-    for flag, zc in (("1", ""), ("0", ""), ("2", "16")):
+    for flag, zc in (("1", ""), ("0", ""), ("2", "16"), ("3", ""), ("4", ""), ("1", "16")):
         path = tmp_path / f"pair{flag}.npy"
         env = dict(os.environ, PT_FGP3_PAIR=flag, PT_FGP3_ZCHUNK=zc)
         subprocess.run([sys.executable, "-c", _PAIR_SNIPPET.format(repo=repo), str(path)],
                        check=True, env=env, timeout=300)
         outs.append(np.load(path))
-    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    for o in outs[1:]:
+        assert np.array_equal(outs[0], o)
