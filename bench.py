@@ -274,6 +274,10 @@ def gpu_arm(args, cfg, rank, world, local):
     torch.cuda.set_device(local)
     dp = world > 1 or args.dp_one_rank  # the multi-GPU data path
     if dp:
+        if "RANK" not in os.environ:  # --dp-one-rank without torchrun: a one-rank group
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0")
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2602_09527_b200 import SolverConfig, TomoProblem, run
     from paper_2602_09527_b200 import _native as N
