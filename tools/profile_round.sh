@@ -7,6 +7,8 @@ O=gpurun_out
 timeout 900 python bench.py > $O/bench_c2.json 2> $O/bench_c2.err
 timeout 900 python bench.py --impl reference > $O/bench_ref.json 2> $O/bench_ref.err
 timeout 600 python bench.py --config c3 --no-cpu-baseline > $O/bench_c3.json 2> $O/bench_c3.err
+timeout 600 python bench.py --config c1 --no-cpu-baseline > $O/bench_c1.json 2> $O/bench_c1.err
+timeout 600 python bench.py --config c0 --no-cpu-baseline > $O/bench_c0.json 2> $O/bench_c0.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
     --log-file $O/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e \
     > $O/ncu_launch.log 2>&1
