@@ -207,6 +207,17 @@ class ClockSampler:
                 if len(parts) >= 9:
                     rows.append(parts)
         if not rows:
+            # timed region shorter than nvidia-smi's start-up (configs 0 / 1):
+            # one query right after it, the clocks still at their loaded state
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=10).stdout
+                rows = [[p.strip() for p in ln.split(",")] for ln in out.splitlines()
+                        if len(ln.split(",")) >= 9]
+            except Exception:
+                rows = []
+        if not rows:
             return None
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
