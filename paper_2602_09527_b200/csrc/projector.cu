@@ -848,7 +848,8 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
     if (NEPI) {
         const bool vec = (P.W % 4) == 0;  // 16-byte rows (c0 is a multiple of TC)
         constexpr int Q = TC / 4;          // 16-byte quads per tile row
-        static_assert(NT % Q == 0 && (TR * Q) % NT == 0, "epilogue prefetch shape");
+        static_assert(NT % Q == 0, "epilogue prefetch shape");
+        constexpr int KQ = (TR * Q + NT - 1) / NT;  // copies per thread and plane
         if (vec && r0 + TR <= P.H && c0 + TC <= P.W) {
             // whole tile inside the image: one 64-bit base per plane, 32-bit
             // offsets stepping NT / Q rows per copy
@@ -861,9 +862,11 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
                 const float* srcp = e == 0 ? P.ep.x : e == 1 ? P.ep.h : e == 2 ? P.ep.aux0 : P.ep.aux1;
                 const float* base = srcp + (size_t)z * plane;
 #pragma unroll
-                for (int k = 0; k < TR * Q / NT; ++k)
+                for (int k = 0; k < KQ; ++k) {
+                    if ((TR * Q) % NT != 0 && rl0 + k * (NT / Q) >= TR) continue;
                     cp_async16(dst0 + (uint32_t)(e * TR * TC + k * (NT / Q) * TC) * 4u,
                                base + (off0 + (uint32_t)k * dstep), 16);
+                }
             }
         } else for (int e = 0; e < NEPI; ++e) {
             const float* srcp = e == 0 ? P.ep.x : e == 1 ? P.ep.h : e == 2 ? P.ep.aux0 : P.ep.aux1;
@@ -1149,10 +1152,12 @@ static int run_gather(pt_plan* plan, const AdjArgs& a, cudaStream_t st)
 {
     static_assert(kGatherTiles[0][0] == 32 && kGatherTiles[0][1] == 128 &&
                   kGatherTiles[1][0] == 32 && kGatherTiles[1][1] == 64 &&
-                  kGatherTiles[2][0] == 16 && kGatherTiles[2][1] == 64, "gather tiles");
+                  kGatherTiles[2][0] == 16 && kGatherTiles[2][1] == 64 &&
+                  kGatherTiles[3][0] == 8 && kGatherTiles[3][1] == 64, "gather tiles");
     switch (plan->gather_tile) {
         case 0: return run_gather_t<32, 128, TWO>(plan, a, st);
         case 1: return run_gather_t<32, 64, TWO>(plan, a, st);
+        case 3: return run_gather_t<8, 64, TWO>(plan, a, st);
         default: return run_gather_t<16, 64, TWO>(plan, a, st);
     }
 }

@@ -104,7 +104,7 @@ namespace pt {
 // pixels per thread, large images), 1 = 32 x 64 (8), 2 = 16 x 64 (4, small
 // images: enough CTAs).  The plan picks one and sizes its staged-bin slot per
 // angle for that tile (capi.cu).
-constexpr int kGatherTiles[3][2] = {{32, 128}, {32, 64}, {16, 64}};
+constexpr int kGatherTiles[4][2] = {{32, 128}, {32, 64}, {16, 64}, {8, 64}};
 
 // Per-caller scratch for the forward band partials and reductions.  The plan
 // owns one (used by the standalone C-ABI calls, which must therefore be

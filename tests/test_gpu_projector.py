@@ -217,7 +217,7 @@ print(float(np.linalg.norm(got - ref) / np.linalg.norm(ref)))
 """
 
 
-@pytest.mark.parametrize("tile", [0, 1, 2])
+@pytest.mark.parametrize("tile", [0, 1, 2, 3])
 def test_every_gather_tile_matches_oracle(tile):
     """Each gather tile shape (the plan picks one by image size) against the oracle."""
     import os
