@@ -475,7 +475,9 @@ __global__ void __launch_bounds__(256) fwd_reduce_kernel(RedArgs P)
         const int k = kk + P.k_begin;
         const int ang = P.sel_angle[k];
         const AngleTab at = P.tab[ang];
-        const int nb = at.branch ? P.nb_col : P.nb_row;
+        // square images: the band count does not depend on the branch, so the
+        // partial loads need not wait for the angle-table load (latency chain)
+        const int nb = (P.nb_row == P.nb_col) ? P.nb_row : at.branch ? P.nb_col : P.nb_row;
         const size_t stride = (size_t)P.n_k * P.Z * P.B;
         // four independent float64 partial sums (latency), combined pairwise
         const float* pp = P.partial + idx;
