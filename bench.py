@@ -28,7 +28,6 @@ from __future__ import annotations
 import argparse
 import glob
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -39,6 +38,9 @@ import numpy as np
 
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
+
+from paper_2602_09527_b200._native import PROF_NAMES  # noqa: E402  (no device needed)
+from paper_2602_09527_b200.problems import POWER_L  # noqa: E402
 
 
 def parse():
@@ -52,8 +54,12 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
-    ap.add_argument("--decomposition", default="rows", choices=["rows", "sectors"],
-                    help="2D multi-GPU layout: image rows (default) or angle sectors")
+    ap.add_argument("--decomposition", default="sectors", choices=["sectors", "rows"],
+                    help="2D multi-GPU layout: angle sectors with a replicated image and prox "
+                         "(north_star's layout, default) or image rows")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="test hook: form the N-rank process group (gloo, no GPU work) and "
+                         "print its size; used by tests/test_bench_cli.py")
     ap.add_argument("--dp-one-rank", action="store_true",
                     help="test hook: run the multi-GPU data path (NCCL process group, sharded "
                          "session) with a single rank")
@@ -91,6 +97,20 @@ def l2_note(cfg):
         return f"working set ~{ws / 1e6:.0f} MB > L2 (126 MB); no flush"
     return (f"working set ~{ws / 1e6:.0f} MB < L2 (126 MB); no flush: the solver state stays "
             f"L2-resident across steps in any run of this size")
+
+
+def bench_config(cfg):
+    """The `config` object both arms print (identical, so the driver can
+    compare them): the workload, the unit of the metric and the problem
+    constants' provenance.  Per-arm details (what one timed step is, the
+    parallelism) are top-level keys."""
+    return {"workload": workload_name(cfg),
+            "epoch": "1 SVRG snapshot full gradient + N ProxSkip iterations (SURVEY.md 8d)"
+                     if cfg.estimator in ("svrg", "lsvrg") else "N ProxSkip iterations",
+            "L": f"{cfg.power_iterations} power iterations, seed {cfg.power_seed} "
+                 f"(problems.POWER_L['{cfg.name}'] = {POWER_L[cfg.name]!r})",
+            "alpha": "0.01 max|A^T b| / n_pixels",
+            "l2": l2_note(cfg)}
 
 
 def workload_name(cfg):
@@ -147,15 +167,17 @@ def cpu_epochs_per_second(cfg, seconds, gamma, alpha, b):
 
 
 def reference_arm(args, cfg, rank, world):
+    """The reference's algorithm on the host (float64 oracle port, all host
+    threads; the reference itself is Python/scipy and cannot run config 2:
+    SURVEY.md 0).  Same problem, gamma and draws as the GPU arm; one
+    continuing trajectory of which each timed step is a bounded slice of N/6
+    iterations (snapshot refreshes and prox calls included as they fall);
+    epochs/s = timed iterations / N / timed seconds."""
     if rank != 0:
         return 0
-    from paper_2602_09527_b200 import problems  # noqa: F401
     from oracle import solver as S
-    prob = cpu_problem(cfg)
-    O, proj, b, alpha = prob
-    gamma = 1.0 / O.operator_norm_sq(proj.geometry, cfg.size, cfg.size, 5, cfg.power_seed)
-    # one "step" = a bounded slice of the solve: N/6 iterations (snapshot
-    # refreshes and prox calls included as they fall), one continuing trajectory
+    O, proj, b, alpha = cpu_problem(cfg)
+    gamma = default_gamma_for(cfg)
     per_step = max(1, cfg.n_subsets // 6)
     total_iters = (args.warmup + args.steps) * per_step
     rw = S.run_proxskip(proj, b, gamma=gamma, p=cfg.p, estimator=cfg.estimator,
@@ -172,16 +194,26 @@ def reference_arm(args, cfg, rank, world):
         "unit": "epochs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * timed_s / max(1, args.steps), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(cfg), "step": f"{per_step} ProxSkip iterations",
-                   "parallelism": "host threads"},
+        "config": bench_config(cfg),
+        "step": f"{per_step} ProxSkip iterations of one continuing trajectory",
+        "parallelism": f"{O.nthreads()} host threads (OpenMP)",
         "cpu_baseline": {"value": value, "unit": "epochs/s", "cores": O.nthreads(), "kind": "port",
                          "sample": f"{timed_iters} iterations ({timed_iters / cfg.n_subsets:.3f} "
-                                   f"epochs) of the float64 oracle restatement"},
+                                   f"epochs, {rw.prox_calls} prox calls in the whole run) of "
+                                   f"the float64 oracle restatement"},
         "e2e": {"value": value, "unit": "epochs/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "problem": {"gamma": gamma, "alpha": alpha},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def default_gamma_for(cfg):
+    """gamma from the pinned L (problems.POWER_L) by the reference's rule
+    (solvers.py:468-479)."""
+    from paper_2602_09527_b200.solvers import default_gamma
+    return default_gamma(cfg.estimator, POWER_L[cfg.name])
 
 
 # --------------------------------------------------------------------------
@@ -246,9 +278,9 @@ class ClockSampler:
 
 def build_gpu_problem(cfg, torch):
     """Synthetic BASELINE problem on the device: phantom (host law), b = A x
-    (device) + host noise, alpha from A^T b, L by 50 power iterations."""
+    (device) + host noise, alpha from A^T b; gamma from the pinned L."""
     from paper_2602_09527_b200 import (ParallelGeometry, Projector, TomoProblem, TvProxConfig,
-                                       default_gamma, problems)
+                                       problems)
     g = ParallelGeometry.uniform(cfg.n_angles, cfg.n_bins)
     proj = Projector(g, cfg.size, cfg.size, cfg.depth)
     x_true = problems.phantom_for(cfg)
@@ -258,42 +290,172 @@ def build_gpu_problem(cfg, torch):
     b_dev = b_host.to("cuda")
     alpha = problems.alpha_from_backprojection(float(proj.adjoint(b_dev).abs().max()),
                                                cfg.n_pixels)
-    lip = proj.norm_sq(cfg.power_iterations, cfg.power_seed)
-    gamma = default_gamma(cfg.estimator, lip)
+    gamma = default_gamma_for(cfg)
     tv = TvProxConfig(alpha=alpha, inner_iterations=cfg.fgp_inner)
-    return proj, b_host, b_dev, TomoProblem(proj, b_dev, tv=tv), gamma, alpha, lip
+    return proj, b_host, b_dev, TomoProblem(proj, b_dev, tv=tv), gamma, alpha
 
 
-def algorithmic_bytes(cfg, proj, state):
-    """SURVEY.md 8d per-launch algorithmic bytes of each launch category."""
-    depth = getattr(proj, "n_slices", 1)  # this rank's planes (z-slab) or the volume
-    n_px = proj.width * proj.height * depth  # this rank's pixels (row / z slab or all)
-    plan = proj.plan
-    part = state.partition
-    sub0 = part.subsets[0] if part else None
-    nnz = plan.nnz(sub0) if sub0 else plan.nnz(None)
-    rays = (len(sub0) if sub0 else cfg.n_angles) * cfg.n_bins * depth
+# --------------------------------------------------------------------------
+# roofline of the timed region (SURVEY.md 8d algorithmic bytes)
+# --------------------------------------------------------------------------
+
+# launch category -> (kernel, ncu kernel-name key) as in profiles/ncu_roofline_*.json
+KERNEL_OF = {"fwd_band": "fwd_band_kernel", "gather": "adj_gather_kernel",
+             "fgp": "fgp2d_kernel", "fgp3": "fgp3d_pair_kernel"}
+
+
+def owned_angles(cfg, rank, world, sectors):
+    if not sectors:
+        return None
+    return (cfg.n_angles * rank // world, cfg.n_angles * (rank + 1) // world)
+
+
+def epoch_algorithmic_bytes(cfg, plan, subs, refr, n_prox, n_px, depth, own):
+    """Total algorithmic bytes of the timed steps per kernel family:
+    forward 4 nnz_i + 4 R_i per subset launch (+ the snapshot's all-angle
+    launch per refresh), gather 4 nnz_i + 4 n_px e (SVRG step e = 4: x, h,
+    grad f(x~), x-hat / x+; snapshot gather e = 1), FGP 28 (2D) / 40 (3D)
+    bytes per pixel per inner iteration + 28 for the epilogue."""
+    n = cfg.n_subsets
+
+    def sel(k):
+        angles = list(range(k, cfg.n_angles, n))
+        if own:
+            angles = [a for a in angles if own[0] <= a < own[1]]
+        return angles
+
+    nnz_sub, rays_sub = {}, {}
+    for k in range(n):
+        a = sel(k)
+        nnz_sub[k] = plan.nnz(tuple(a)) if a else 0
+        rays_sub[k] = len(a) * cfg.n_bins * depth
+    all_angles = (list(range(own[0], own[1])) if own else None)
+    nnz_all = plan.nnz(tuple(all_angles) if own else None)
+    rays_all = (len(all_angles) if own else cfg.n_angles) * cfg.n_bins * depth
     e = 4 if cfg.estimator in ("svrg", "lsvrg") else (7 if cfg.estimator == "saga" else 3)
-    return {
-        "fwd_band": 4 * nnz + 4 * rays,
-        "gather_step": 4 * nnz + 4 * n_px * e,
-        "fgp_call": (40 if cfg.depth > 1 else 28) * n_px * cfg.fgp_inner + 28 * n_px,
-        "fwd_reduce": None, "snapshot": None, "other": None,
-    }, nnz
+    fwd = gat = 0
+    n_fwd = 0
+    for i, rf in zip(subs, refr):
+        if rf:
+            fwd += 4 * nnz_all + 4 * rays_all
+            gat += 4 * nnz_all + 4 * n_px
+            continue  # the post-refresh step runs no projection (DESIGN.md 4)
+        fwd += 4 * nnz_sub[int(i)] + 4 * rays_sub[int(i)]
+        gat += 4 * nnz_sub[int(i)] + 4 * n_px * e
+        n_fwd += 1
+    fgp_b = ((40 if depth > 1 else 28) * n_px * cfg.fgp_inner + 28 * n_px) * n_prox
+    return {"fwd_band": fwd, "gather": gat, "fgp": fgp_b}, nnz_sub[0], n_fwd
 
 
-def ncu_traffic(kernel_key):
-    """dram bytes per launch of the top kernel from the committed ncu capture."""
-    best = None
-    for path in sorted(glob.glob(os.path.join(REPO, "profiles", "*ncu_traffic*.json"))):
+def ncu_binding(config_name, kernel):
+    """Per-launch ncu figures of `kernel` captured on THIS config (the
+    newest profiles/ncu_roofline_r*.json that has the pair), else None."""
+    found = None
+    for path in sorted(glob.glob(os.path.join(REPO, "profiles", "ncu_roofline_r*.json"))):
         try:
             with open(path) as fh:
                 d = json.load(fh)
-            if kernel_key in d:
-                best = d[kernel_key]
         except Exception:
-            pass
-    return best
+            continue
+        rec = d.get(config_name, {}).get(kernel)
+        if rec:
+            found = dict(rec, source=os.path.relpath(path, REPO))
+    return found
+
+
+def roofline_record(cfg, msa, cnt, alg, peak, peak_kind):
+    """Dominant kernel of the timed region (subset + snapshot launches) and its
+    achieved algorithmic GB/s; binding fractions from the same config's ncu
+    capture decide `bound`."""
+    idx = {name: i for i, name in enumerate(PROF_NAMES)}
+    ms = {"fwd_band": msa[idx["fwd_band"]] + msa[idx["snap_fwd_band"]],
+          "gather": msa[idx["gather_step"]] + msa[idx["snap_gather"]],
+          "fgp": msa[idx["fgp_call"]]}
+    launches = {"fwd_band": cnt[idx["fwd_band"]] + cnt[idx["snap_fwd_band"]],
+                "gather": cnt[idx["gather_step"]] + cnt[idx["snap_gather"]],
+                "fgp": cnt[idx["fgp_call"]]}
+    cands = [k for k in ms if ms[k] > 0 and alg[k]]
+    if not cands:
+        return None
+    top = max(cands, key=lambda k: ms[k])
+    achieved = alg[top] / (ms[top] / 1e3) / 1e9
+    kernel = KERNEL_OF["fgp3" if (top == "fgp" and cfg.depth > 1) else top]
+    rec = {"kernel": kernel, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+           "frac": round(achieved / peak, 4), "peak_source": peak_kind,
+           "algorithmic_bytes_timed": int(alg[top]), "ms_timed": round(ms[top], 3),
+           "calls": int(launches[top]),
+           "avg_call_us": round(1e3 * ms[top] / max(1, launches[top]), 2),
+           "share_of_profiled_step": None, "traffic": None, "bound": None,
+           "note": "achieved = SURVEY.md 8d algorithmic bytes (one 4-byte operand per Joseph "
+                   "nonzero + the arrays each kernel must touch) / CUDA-event time, summed over "
+                   "the subset and snapshot launches of the profiled epochs; > 1 of HBM peak is "
+                   "on-chip operand reuse, so `bound` comes from ncu's binding unit"}
+    tot = sum(msa[idx[k]] for k in ("fwd_band", "fwd_reduce", "gather_step", "fgp_call",
+                                     "snapshot", "other"))
+    rec["share_of_profiled_step"] = round(ms[top] / tot, 4) if tot else None
+    b = ncu_binding(cfg.name, kernel)
+    if b:
+        fr = {"issue": b.get("issue_frac"), "lsu": b.get("lsu_shared_frac"),
+              "hbm": b.get("dram_frac")}
+        fr = {k: v for k, v in fr.items() if v is not None}
+        rec["bound"] = max(fr, key=fr.get) if fr else None
+        rec["binding"] = {"issue_frac": b.get("issue_frac"),
+                          "lsu_shared_frac": b.get("lsu_shared_frac"),
+                          "dram_frac": b.get("dram_frac"), "l2_hit": b.get("l2_hit"),
+                          "bank_conflict_share": b.get("bank_conflict_share"),
+                          "ncu_us": b.get("us"), "source": b.get("source")}
+        # ncu bytes of one launch; per call for the FGP (launches per call)
+        per = b.get("dram_bytes")
+        if per is not None:
+            rec["traffic"] = per * b.get("launches_per_call", 1)
+            rec["traffic_unit"] = "bytes per call (ncu dram__bytes_read+write, same config)"
+    return rec
+
+
+# --------------------------------------------------------------------------
+# process group: --gpus N spawns N ranks itself
+# --------------------------------------------------------------------------
+
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn(args):
+    """`python bench.py --gpus N` without torchrun: re-exec under
+    torch.distributed.run with N ranks on this node (127.0.0.1 rendezvous),
+    refusing to run with fewer than N visible GPUs."""
+    if not args.dry_run and args.impl != "reference":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but only {have} GPU(s) visible", file=sys.stderr)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def dry_run(args, rank, world):
+    """Form the process group exactly as the GPU arm does (gloo instead of
+    NCCL, no device work) and report its size."""
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo")
+    t = torch.ones(1)
+    dist.all_reduce(t)
+    if world != args.gpus:
+        raise SystemExit(f"process group has {world} ranks, --gpus {args.gpus}")
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": args.gpus, "world": dist.get_world_size(),
+                          "allreduce_sum": float(t.item())}), flush=True)
+    dist.destroy_process_group()
+    return 0
 
 
 def gpu_arm(args, cfg, rank, world, local):
@@ -305,18 +467,20 @@ def gpu_arm(args, cfg, rank, world, local):
         if "RANK" not in os.environ:  # --dp-one-rank without torchrun: a one-rank group
             os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0")
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("MASTER_PORT", str(free_port()))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if world != max(1, args.gpus) and not args.dp_one_rank:
+            raise SystemExit(f"NCCL group has {world} ranks, --gpus {args.gpus}")
     from paper_2602_09527_b200 import SolverConfig, TomoProblem, run
     from paper_2602_09527_b200 import _native as N
     from paper_2602_09527_b200 import distributed as D
     from paper_2602_09527_b200.solvers import _init_state, _plan_segment
 
-    proj, b_host, b_dev, problem, gamma, alpha, lip = build_gpu_problem(cfg, torch)
+    proj, b_host, b_dev, problem, gamma, alpha = build_gpu_problem(cfg, torch)
     scfg = SolverConfig(gamma=gamma, skip_probability=cfg.p, n_subsets=cfg.n_subsets,
                         estimator=cfg.estimator, max_data_passes=1e18, seed=cfg.solver_seed)
     stream = torch.cuda.Stream()
-    # multi-GPU: image rows or angle sectors (2D), z-slabs (slice-stacked 3D);
+    # multi-GPU: angle sectors or image rows (2D), z-slabs (slice-stacked 3D);
     # SURVEY.md 8e, DESIGN.md "Multi-GPU"
     zs, rs, work = None, None, problem
     if dp and cfg.depth > 1:
@@ -345,7 +509,7 @@ def gpu_arm(args, cfg, rank, world, local):
         state.k += len(subs)
         state.data_passes = passes
         state.prox_calls += int(np.count_nonzero(thetas))
-        return len(subs), int(np.count_nonzero(thetas))
+        return subs, thetas, refr
 
     def barrier():
         if dp:
@@ -363,12 +527,13 @@ def gpu_arm(args, cfg, rank, world, local):
     torch.cuda.synchronize()
     barrier()
     t_start.record(stream)
-    n_iter, n_prox = run_epochs(args.steps)
+    subs, thetas, refr = run_epochs(args.steps)
     t_end.record(stream)
     torch.cuda.synchronize()
     barrier()
     launches = N.launch_count() - launches0
     clock_info = clocks.stop()
+    n_iter, n_prox = len(subs), int(np.count_nonzero(thetas))
     ms = t_start.elapsed_time(t_end)
     if dp:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
@@ -377,39 +542,39 @@ def gpu_arm(args, cfg, rank, world, local):
     bad = sess.bad_iteration()
     value = args.steps / (ms / 1e3)
 
-    # replica check across ranks
     # replicas exist only in the angle-sector layout (slab layouts own disjoint parts)
     replicas_ok = D.replicas_identical(sess.x) if (dp and zs is None and rs is None) else None
 
-    # live per-kernel timing: a second timed pass with CUDA events per launch
+    # live per-kernel timing: the same number of epochs again (the trajectory
+    # continues) with CUDA events around every launch category
     roofline = None
     kernel_times = None
     if not args.no_profile:
-        N.check(N.lib().pt_session_set_profiling(sess.handle, 1))
-        run_epochs(max(1, min(args.steps, 3)))
         import ctypes
-        msa = (ctypes.c_double * 6)()
-        cnt = (ctypes.c_int64 * 6)()
+        N.check(N.lib().pt_session_set_profiling(sess.handle, 1))
+        psubs, pthetas, prefr = run_epochs(args.steps)
+        nc = len(N.PROF_NAMES)
+        msa = (ctypes.c_double * nc)()
+        cnt = (ctypes.c_int64 * nc)()
         N.check(N.lib().pt_session_profile(sess.handle, msa, cnt))
         N.check(N.lib().pt_session_set_profiling(sess.handle, 0))
-        tot = sum(msa)
+        top_level = ("fwd_band", "fwd_reduce", "gather_step", "fgp_call", "snapshot", "other")
+        tot = sum(msa[N.PROF_NAMES.index(k)] for k in top_level)
         kernel_times = {name: {"ms": round(msa[i], 3), "calls": int(cnt[i]),
                                "share": round(msa[i] / tot, 4) if tot else None}
                         for i, name in enumerate(N.PROF_NAMES)}
-        alg, nnz = algorithmic_bytes(cfg, work.projector, state)  # per rank
-        cands = [k for k in ("gather_step", "fwd_band", "fgp_call") if alg[k] and cnt[N.PROF_NAMES.index(k)]]
-        top = max(cands, key=lambda k: msa[N.PROF_NAMES.index(k)])
-        i = N.PROF_NAMES.index(top)
-        per_launch_s = msa[i] / cnt[i] / 1e3
-        achieved = alg[top] / per_launch_s / 1e9
+        kernel_times["_note"] = ("top-level categories partition the profiled epochs; snap_* "
+                                 "are the snapshot's own launches (inside 'snapshot')")
+        wp = work.projector
+        depth = getattr(wp, "n_slices", 1)
+        n_px = wp.width * wp.height * depth
+        own = owned_angles(cfg, rank, world, dp and zs is None and rs is None)
+        alg, nnz0, _ = epoch_algorithmic_bytes(cfg, wp.plan, psubs, prefr,
+                                               int(np.count_nonzero(pthetas)), n_px, depth, own)
         peak, peak_kind = peaks()
-        roofline = {"bound": "hbm", "kernel": top, "achieved": round(achieved, 1), "peak": peak,
-                    "unit": "GB/s", "frac": round(achieved / peak, 4),
-                    "traffic": ncu_traffic(top), "peak_source": peak_kind,
-                    "bytes_per_launch": alg[top], "avg_launch_us": round(per_launch_s * 1e6, 2),
-                    "nnz_subset0": nnz,
-                    "note": "algorithmic bytes (SURVEY.md 8d: 4 B per Joseph nonzero + epilogue "
-                            "arrays); > 1 means on-chip operand reuse"}
+        roofline = roofline_record(cfg, msa, cnt, alg, peak, peak_kind)
+        if roofline:
+            roofline["nnz_subset0"] = nnz0
 
     # end-to-end through the public API, host buffers
     e2e = None
@@ -472,18 +637,19 @@ def gpu_arm(args, cfg, rank, world, local):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": workload_name(cfg), "step": "1 epoch = snapshot + N iterations",
-                       "epochs_timed": args.steps, "iterations_timed": n_iter,
-                       "prox_calls_timed": n_prox,
-                       "parallelism": ("1 GPU" if not dp else
-                                       f"z-slab dp{world}" if zs else
-                                       f"image-row dp{world}" if rs else
-                                       f"angle-sector dp{world}"),
-                       "l2": l2_note(cfg),
-                       "L": lip, "gamma": gamma, "alpha": alpha},
+            "config": bench_config(cfg),
+            "step": "1 epoch (snapshot + N iterations) of one continuing trajectory",
+            "parallelism": ("1 GPU" if not dp else
+                            f"z-slab dp{world}" if zs else
+                            f"image-row dp{world}" if rs else
+                            f"angle-sector dp{world} (replicated image and prox)"),
+            "timed": {"epochs": args.steps, "iterations": n_iter, "prox_calls": n_prox,
+                      "snapshots": int(np.count_nonzero(refr))},
             "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clock_info, "kernel_times": kernel_times,
+            "problem": {"L": POWER_L[cfg.name], "gamma": gamma, "alpha": alpha},
             "finite": bad is None, "replicas_identical": replicas_ok,
+            "nccl_ranks": world if dp else None,
         }
         print(json.dumps(line), flush=True)
     if dp:
@@ -500,6 +666,10 @@ def main():
     # is dropped, any other debug level is the user's choice and kept
     if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
         os.environ.pop("NCCL_DEBUG")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args)
+    if args.dry_run:
+        return dry_run(args, rank, world)
     from paper_2602_09527_b200 import problems
     cfg = problems.CONFIGS[args.config]
     if args.impl == "reference":

@@ -64,6 +64,10 @@ const char* pt_version(void);
 /* Process-wide number of kernels this library has launched (evidence that
  * the native path, not a fallback, ran). */
 int64_t pt_launch_count(void);
+/* sizeof(pt_geometry_desc): a binding built from its own copy of the struct
+ * (ctypes, cffi, cgo) asserts this at load time so a layout change cannot
+ * make pt_plan_create read past the caller's struct. */
+int64_t pt_geometry_desc_size(void);
 
 /* Plan lifecycle: uploads the per-angle Joseph tables (computed on the host
  * in float64 from the reference's expressions, projector.py:26-61). */
@@ -101,6 +105,13 @@ int pt_adjoint(pt_plan* plan, const pt_selection* sel, const float* y, float* x_
 #define PT_EST_SAGA 2
 #define PT_EST_SVRG 3
 #define PT_EST_LSVRG 4
+/* Session-only kinds (not an estimator of the reference, a solver of it):
+ * FISTA (solvers.py:367-392) -- per step the full gradient at the momentum
+ * point y, x+ = prox_gamma(y - gamma grad f(y)), y = x+ + beta_k (x+ - x) with
+ * t_{k+1} = (1 + sqrt(1 + 4 t_k^2)) / 2, beta_k = (t_k - 1) / t_{k+1}, t_1 = 1
+ * (the t sequence is kept in float64 on the host side of the session).
+ * ISTA (:339-364) is PT_EST_FULL with skip_probability 1 (hcoef = 0). */
+#define PT_EST_FISTA 5
 
 /* Fused adjoint + estimator + ProxSkip gradient half-step, one pass:
  *   g    = A_S^T r                              (estimators.py:32)
@@ -244,7 +255,11 @@ int64_t* pt_session_bad_iter(pt_session* s);            /* device int64, INT64_M
 #define PT_PROF_FGP 3        /* one TV prox call (all its launches)           */
 #define PT_PROF_SNAPSHOT 4   /* SVRG snapshot full gradient (fwd + adj)       */
 #define PT_PROF_OTHER 5      /* copies, identity prox, allreduce              */
-#define PT_PROF_N 6
+/* the snapshot's own launches (also inside PT_PROF_SNAPSHOT's time) */
+#define PT_PROF_SNAP_FWD_BAND 6
+#define PT_PROF_SNAP_FWD_REDUCE 7
+#define PT_PROF_SNAP_GATHER 8
+#define PT_PROF_N 9
 int pt_session_set_profiling(pt_session* s, int32_t on);
 /* Syncs the session stream; returns accumulated ms and call counts per
  * category since the last collection, then resets them. */
@@ -280,6 +295,12 @@ int pt_session_attach_comm_rows(pt_session* s, pt_comm* comm, int32_t row_offset
                                 int32_t rows_total);
 int pt_session_attach_nccl(pt_session* s, const char* nccl_path, const uint8_t* host_id128,
                            int32_t rank, int32_t world);
+/* Test hook: make an attached session believe it is rank `rank` of `world`
+ * while its communicator keeps its real size (a one-rank communicator then
+ * exercises the per-rank offsets of the slab layouts, e.g. the snapshot
+ * residual's angle indexing in rows mode, on one GPU).  Only for runs that
+ * exchange no halos (no TV prox).  Call before pt_session_init. */
+int pt_session_override_rank(pt_session* s, int32_t rank, int32_t world);
 /* Test hook: run the angle-sector decomposition of `world` ranks on this one
  * device (each sector's partial A_i^T r computed separately and summed, which
  * is exactly what ncclAllReduce sums across real ranks).  Call before run. */

@@ -162,6 +162,63 @@ def run_proxskip(projector: OracleProjector, data, *, gamma, p, estimator, n_sub
     return res
 
 
+def run_fista(projector, data, *, gamma, max_data_passes, tv_alpha=None, tv_inner=10,
+              warm_start=True, nonneg=True, accelerate=True, record_objective=False) -> Result:
+    """run_fista / run_ista (solvers.py:339-392): full gradient at y, prox every
+    iteration, t_{k+1} = (1 + sqrt(1 + 4 t_k^2)) / 2, y = x+ + ((t_k - 1) / t_{k+1})
+    (x+ - x); one data pass per iteration, rows as _run_loop (:280-324)."""
+    data = np.asarray(data, dtype=np.float64)
+    x = np.zeros(projector.shape)
+    y = x.copy()
+    t = 1.0
+    warm = None
+    passes = 0.0
+    res = Result(image=x)
+
+    def log(k):
+        obj = objective(projector, data, x, tv_alpha) if record_objective else None
+        res.rows.append((passes, res.work_seconds, res.prox_calls, obj))
+        res.iterations.append(k)
+
+    log(0)
+    last_floor = math.floor(passes + 1e-12)
+    k = 0
+    while True:
+        t0 = time.perf_counter()
+        grad = projector.adjoint(projector.forward(y) - data)
+        target = y - gamma * grad
+        if tv_alpha:
+            x_next, warm = tv_prox(target, gamma, tv_alpha, tv_inner, nonneg,
+                                   warm if warm_start else None)
+        else:
+            x_next = target
+        res.prox_calls += 1
+        if not np.all(np.isfinite(x_next)):
+            res.diverged_at = k
+            res.image = None
+            return res
+        if accelerate:
+            t_next = (1.0 + math.sqrt(1.0 + 4.0 * t * t)) / 2.0
+            y = x_next + ((t - 1.0) / t_next) * (x_next - x)
+            t = t_next
+        else:
+            y = x_next
+        x = x_next
+        k += 1
+        passes += 1.0
+        res.work_seconds += time.perf_counter() - t0
+        exhausted = passes >= max_data_passes - 1e-9
+        crossed = math.floor(passes + 1e-12) > last_floor
+        if crossed or exhausted:
+            last_floor = math.floor(passes + 1e-12)
+            log(k)
+            if exhausted:
+                break
+    res.image = x
+    res.k = k
+    return res
+
+
 def _forward_diff(x):
     """regularizers.py:62-68: forward differences, 0 on the last row / column."""
     gv = np.zeros_like(x)

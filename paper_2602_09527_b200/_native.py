@@ -18,7 +18,9 @@ from . import build as _build
 PT_OK, PT_EINVAL, PT_ECUDA, PT_EUNSUPPORTED, PT_ENCCL = 0, -1, -2, -3, -4
 PT_RED_DOUBLES = 1025
 EST_CODES = {"full": 0, "sgd": 1, "saga": 2, "svrg": 3, "lsvrg": 4}
-PROF_NAMES = ("fwd_band", "fwd_reduce", "gather_step", "fgp_call", "snapshot", "other")
+SESSION_KINDS = {"fista": 5}  # include/proxtomo_b200.h PT_EST_FISTA
+PROF_NAMES = ("fwd_band", "fwd_reduce", "gather_step", "fgp_call", "snapshot", "other",
+              "snap_fwd_band", "snap_fwd_reduce", "snap_gather")
 
 _lock = threading.Lock()
 _lib = None
@@ -52,6 +54,7 @@ _SIGS = {
     "pt_last_error": (ctypes.c_char_p, []),
     "pt_version": (ctypes.c_char_p, []),
     "pt_launch_count": (c_i64, []),
+    "pt_geometry_desc_size": (c_i64, []),
     "pt_plan_create": (ctypes.c_int, [ctypes.POINTER(GeometryDesc), ctypes.POINTER(c_vp)]),
     "pt_plan_destroy": (ctypes.c_int, [c_vp]),
     "pt_selection_create": (ctypes.c_int, [c_vp, ctypes.POINTER(c_i32), c_i32, ctypes.POINTER(c_vp)]),
@@ -104,6 +107,7 @@ _SIGS = {
     "pt_session_attach_comm": (ctypes.c_int, [c_vp, c_vp]),
     "pt_session_attach_comm_zslab": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32]),
     "pt_session_attach_comm_rows": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32]),
+    "pt_session_override_rank": (ctypes.c_int, [c_vp, c_i32, c_i32]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)
@@ -129,6 +133,9 @@ def load(build_if_missing: bool = True):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        if lib.pt_geometry_desc_size() != ctypes.sizeof(GeometryDesc):
+            raise RuntimeError("pt_geometry_desc layout mismatch between include/proxtomo_b200.h "
+                               "and this binding")
         _lib = lib
         return lib
 

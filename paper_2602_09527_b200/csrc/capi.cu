@@ -162,6 +162,7 @@ extern "C" {
 const char* pt_last_error(void) { return g_err; }
 const char* pt_version(void) { return "proxtomo_b200 0.1.0 sm_100a"; }
 int64_t pt_launch_count(void) { return g_launches.load(); }
+int64_t pt_geometry_desc_size(void) { return (int64_t)sizeof(pt_geometry_desc); }
 
 int pt_plan_create(const pt_geometry_desc* d, pt_plan** out)
 {

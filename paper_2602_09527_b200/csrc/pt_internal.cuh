@@ -117,7 +117,11 @@ struct Profiler {
     size_t used = 0;
     struct Rec { int cat; size_t ev0; };
     std::vector<Rec> recs;
-    int depth = 0;  // nested scopes: only the outermost one records
+    // open scopes: index into recs, or -1 for a nested scope that does not
+    // record (only the outermost scope records, except that the kernel
+    // scopes inside a snapshot record as the PT_PROF_SNAP_* categories)
+    std::vector<long> open;
+    int outer = -1;  // category of the outermost open scope
     double ms[PT_PROF_N] = {0};
     long long calls[PT_PROF_N] = {0};
     cudaEvent_t ev();
@@ -249,6 +253,9 @@ int launch_identity_prox(const float* v, const float* xhat, float* x_out, float*
                          float p_over_gamma, int64_t n, int64_t iteration, int64_t* bad_iter,
                          cudaStream_t st);
 int launch_scale_by_rsqrt(float* v, const float* u, const double* sumsq, int64_t n,
+                          cudaStream_t st);
+int launch_fista_momentum(const float* src, const float* x_prev, float* x_out, float* y,
+                          float beta, int64_t n, int64_t iteration, int64_t* bad_iter,
                           cudaStream_t st);
 int launch_fill_i64(int64_t* p, int64_t value, cudaStream_t st);
 }  // namespace pt

@@ -176,6 +176,33 @@ int launch_scale_by_rsqrt(float* v, const float* u, const double* sumsq, int64_t
     return PT_OK;
 }
 
+// FISTA momentum (solvers.py:384-386): x+ = src (the prox output, or the
+// prox input when there is no regulariser), y = x+ + beta (x+ - x); a
+// non-finite x+ lowers *bad_iter (solvers.py:380-381).
+__global__ void fista_momentum_kernel(const float* src, const float* x_prev, float* x_out,
+                                      float* y, float beta, int64_t n, long long iteration,
+                                      long long* bad_iter)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float xn = src[i];
+        if (x_out != src) x_out[i] = xn;
+        y[i] = xn + beta * (xn - x_prev[i]);
+        if (!isfinite(xn)) atomicMin(bad_iter, iteration);
+    }
+}
+
+int launch_fista_momentum(const float* src, const float* x_prev, float* x_out, float* y,
+                          float beta, int64_t n, int64_t iteration, int64_t* bad_iter,
+                          cudaStream_t st)
+{
+    const int g = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    fista_momentum_kernel<<<g, 256, 0, st>>>(src, x_prev, x_out, y, beta, n,
+                                             (long long)iteration, (long long*)bad_iter);
+    PT_CHECK_LAUNCH();
+    return PT_OK;
+}
+
 __global__ void fill_i64_kernel(int64_t* p, int64_t value) { *p = value; }
 
 int launch_fill_i64(int64_t* p, int64_t value, cudaStream_t st)

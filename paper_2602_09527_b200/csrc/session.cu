@@ -108,17 +108,32 @@ cudaEvent_t Profiler::ev()
 
 void Profiler::begin(int cat, cudaStream_t st)
 {
-    if (depth++ > 0) return;
-    Rec r{cat, used};
+    int rec_cat = -1;
+    if (open.empty()) {
+        rec_cat = cat;
+        outer = cat;
+    } else if (outer == PT_PROF_SNAPSHOT && open.size() == 1) {
+        if (cat == PT_PROF_FWD_BAND) rec_cat = PT_PROF_SNAP_FWD_BAND;
+        else if (cat == PT_PROF_FWD_REDUCE) rec_cat = PT_PROF_SNAP_FWD_REDUCE;
+        else if (cat == PT_PROF_GATHER) rec_cat = PT_PROF_SNAP_GATHER;
+    }
+    if (rec_cat < 0) {
+        open.push_back(-1);
+        return;
+    }
+    Rec r{rec_cat, used};
     cudaEventRecord(ev(), st);
     ev();  // reserve the end event
+    open.push_back((long)recs.size());
     recs.push_back(r);
 }
 
 void Profiler::end(cudaStream_t st)
 {
-    if (--depth > 0) return;
-    cudaEventRecord(pool[recs.back().ev0 + 1], st);
+    const long i = open.back();
+    open.pop_back();
+    if (i >= 0) cudaEventRecord(pool[recs[i].ev0 + 1], st);
+    if (open.empty()) outer = -1;
 }
 
 int Profiler::collect()
@@ -164,6 +179,7 @@ struct pt_session {
     pt::Profiler prof;
     bool have_duals = false;
     double dual_weight = 0.0;
+    double fista_t = 1.0;  // FISTA momentum sequence t_k (solvers.py:384)
     std::vector<pt_selection*> subsets;  // (own rows of) subset i
     pt_selection* own_all = nullptr;     // all (own) angles
     // test hook: G virtual angle sectors on one device (sums what the ranks' allreduce sums)
@@ -238,15 +254,26 @@ int sector_selections(pt_plan* P, int n_subsets, int lo, int hi, pt_selection** 
     return PT_OK;
 }
 
+// Estimators whose step uses every (owned) angle: the full gradient and FISTA.
+bool full_kind(int est) { return est == PT_EST_FULL || est == PT_EST_FISTA; }
+
+// First owned angle: the sector start in the angle-sector layout; 0 in the
+// slab layouts (rows / z-slabs own every angle, build_selections).
+int owned_angle_lo(const pt_session* s)
+{
+    if (s->zslab || s->rows) return 0;
+    return (int)((long long)s->plan->A * s->rank / s->world);
+}
+
 int build_selections(pt_session* s)
 {
     pt_plan* P = s->plan;
     const int A = P->A;
     const bool all = s->zslab || s->rows;  // slab modes own every angle
     const int world = all ? 1 : s->world, rank = all ? 0 : s->rank;
-    const int lo = (int)((long long)A * rank / world);
+    const int lo = owned_angle_lo(s);
     const int hi = (int)((long long)A * (rank + 1) / world);
-    const int n = (s->d.estimator != PT_EST_FULL) ? s->d.n_subsets : 0;
+    const int n = !full_kind(s->d.estimator) ? s->d.n_subsets : 0;
     return sector_selections(P, n, lo, hi, &s->own_all, &s->subsets);
 }
 
@@ -321,8 +348,7 @@ int full_gradient(pt_session* s, const float* x, float* out, float* res, cudaStr
 // The snapshot residual indexed by geometry angle (rows [lo, hi) are owned).
 const float* rsnap_by_angle(const pt_session* s)
 {
-    const int lo = s->zslab ? 0 : (int)((long long)s->plan->A * s->rank / s->world);
-    return s->rsnap - (ptrdiff_t)lo * s->plan->Z * s->plan->B;
+    return s->rsnap - (ptrdiff_t)owned_angle_lo(s) * s->plan->Z * s->plan->B;
 }
 
 // Halo exchange with the z-neighbours (ncclSend / ncclRecv in one group).
@@ -430,8 +456,12 @@ int check_desc(const pt_plan* plan, const pt_solver_desc* desc)
         pt::set_error("skip_probability must be in (0, 1]");
         return PT_EINVAL;
     }
-    if (desc->estimator < PT_EST_FULL || desc->estimator > PT_EST_LSVRG) { pt::set_error("unknown estimator"); return PT_EINVAL; }
-    if (desc->estimator != PT_EST_FULL && (desc->n_subsets < 1 || desc->n_subsets > plan->A)) {
+    if (desc->estimator < PT_EST_FULL || desc->estimator > PT_EST_FISTA) { pt::set_error("unknown estimator"); return PT_EINVAL; }
+    if (desc->estimator == PT_EST_FISTA && desc->skip_probability != 1.0) {
+        pt::set_error("FISTA applies the prox every iteration (skip_probability 1)");
+        return PT_EINVAL;
+    }
+    if (!full_kind(desc->estimator) && (desc->n_subsets < 1 || desc->n_subsets > plan->A)) {
         pt::set_error("n_subsets must be in [1, n_angles], got %d for %d angles", desc->n_subsets, plan->A);
         return PT_EINVAL;
     }
@@ -463,6 +493,7 @@ size_t session_layout(const pt_plan* plan, const pt_solver_desc* desc, pt_sessio
     F(s ? &s->x[0] : nullptr, n); F(s ? &s->x[1] : nullptr, n);
     F(s ? &s->h : nullptr, n); F(s ? &s->v : nullptr, n); F(s ? &s->xhat : nullptr, n);
     if (vr) { F(s ? &s->snap : nullptr, n); F(s ? &s->fg : nullptr, n); F(s ? &s->rsnap : nullptr, sino); }
+    if (desc->estimator == PT_EST_FISTA) F(s ? &s->snap : nullptr, n);  // momentum point y
     if (desc->estimator == PT_EST_SAGA) {
         F(s ? &s->saga_table : nullptr, n * desc->n_subsets);
         F(s ? &s->saga_sum : nullptr, n);
@@ -578,8 +609,14 @@ int pt_session_destroy(pt_session* s)
 int pt_session_init(pt_session* s, void* stream)
 {
     if (!s) { pt::set_error("null session"); return PT_EINVAL; }
-    if (s->d.estimator != PT_EST_SVRG && s->d.estimator != PT_EST_LSVRG) return PT_OK;
     cudaStream_t st = (cudaStream_t)stream;
+    if (s->d.estimator == PT_EST_FISTA) {
+        // run_fista (solvers.py:378): y = x0, t = 1
+        s->fista_t = 1.0;
+        PT_CHECK_CUDA(cudaMemcpyAsync(s->snap, s->x[s->cur], s->n * 4, cudaMemcpyDeviceToDevice, st));
+        return PT_OK;
+    }
+    if (s->d.estimator != PT_EST_SVRG && s->d.estimator != PT_EST_LSVRG) return PT_OK;
     // init_svrg_state (estimators.py:117-123): snapshot = x0, G = full gradient
     PT_CHECK_CUDA(cudaMemcpyAsync(s->snap, s->x[s->cur], s->n * 4, cudaMemcpyDeviceToDevice, st));
     return full_gradient(s, s->snap, s->fg, s->rsnap, st);
@@ -593,6 +630,11 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
     pt_plan* P = s->plan;
     const pt_solver_desc& d = s->d;
     const bool vr = (d.estimator == PT_EST_SVRG || d.estimator == PT_EST_LSVRG);
+    const bool fista = d.estimator == PT_EST_FISTA;
+    if (fista && (s->zslab || s->rows)) {
+        pt::set_error("FISTA runs on one device or angle sectors");
+        return PT_EINVAL;
+    }
     const double gamma = d.gamma, p = d.skip_probability;
     for (int j = 0; j < n_steps; ++j) {
         const int64_t k = k0 + j;
@@ -609,7 +651,7 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
         }
         const pt_selection* sel = s->own_all;
         int i = 0;
-        if (d.estimator != PT_EST_FULL) {
+        if (!full_kind(d.estimator)) {
             i = host_subset ? host_subset[j] : 0;
             if (i < 0 || i >= d.n_subsets) {
                 pt::set_error("subset index %d out of range [0, %d)", i, d.n_subsets);
@@ -619,6 +661,8 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
         }
         const float* xc = s->x[s->cur];
         float* xn = s->x[1 - s->cur];
+        // the point the gradient is taken at: x, or FISTA's momentum point y
+        const float* xg = fista ? s->snap : xc;
         const int theta = (p >= 1.0) ? 1 : (host_theta ? host_theta[j] : 0);
 
         // Right after a refresh x == x_snap bitwise, so the reference's
@@ -634,18 +678,18 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
             rc = pt::launch_forward(P, &s->ws, sel, xc, nullptr, s->data, s->r, nullptr, st,
                                     rsnap_by_angle(s));
         else
-            rc = pt::launch_forward(P, &s->ws, sel, xc, nullptr, s->data, s->r, nullptr, st);
+            rc = pt::launch_forward(P, &s->ws, sel, xg, nullptr, s->data, s->r, nullptr, st);
         if (rc) return rc;
 
         pt_step_epilogue ep;
         memset(&ep, 0, sizeof(ep));
-        ep.estimator = d.estimator;
+        ep.estimator = fista ? PT_EST_FULL : d.estimator;
         ep.theta = theta;
         ep.n_scale = (float)d.n_subsets;
         ep.gamma = (float)gamma;
         ep.hcoef = (float)(gamma - gamma / p);  // solvers.py:242, exactly 0 at p = 1
         ep.iteration = k;
-        ep.x = xc;
+        ep.x = xg;
         ep.h = s->h;
         if (d.estimator == PT_EST_SAGA) {
             ep.aux0 = s->saga_table + (size_t)i * s->n;
@@ -663,8 +707,8 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
         } else if (s->emu > 1) {
             // virtual ranks: partial A_i^T r per sector, summed in g, then the epilogue
             for (int g = 0; g < s->emu && !rc; ++g) {
-                const pt_selection* sg = (d.estimator == PT_EST_FULL) ? s->emu_all[g]
-                                                                      : s->emu_subsets[g][i];
+                const pt_selection* sg = full_kind(d.estimator) ? s->emu_all[g]
+                                                                : s->emu_subsets[g][i];
                 if (sg->n == 0) {
                     if (g == 0) PT_CHECK_CUDA(cudaMemsetAsync(s->g, 0, s->n * 4, st));
                     continue;
@@ -673,7 +717,7 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
                     rc = pt::launch_forward(P, &s->ws, sg, xc, nullptr, s->data, s->r, nullptr, st,
                                             rsnap_by_angle(s));
                 else
-                    rc = pt::launch_forward(P, &s->ws, sg, xc, nullptr, s->data, s->r, nullptr, st);
+                    rc = pt::launch_forward(P, &s->ws, sg, xg, nullptr, s->data, s->r, nullptr, st);
                 if (!rc) rc = pt::launch_adjoint(P, sg, s->r, s->g, 1.f, g > 0, nullptr, st, &s->ws);
             }
             if (!rc) rc = pt::launch_epilogue(P, s->g, &ep, st);
@@ -705,7 +749,11 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
                     PT_CHECK_CUDA(cudaMemsetAsync(s->dq, 0, s->n * 4, st));
                     if (dw) PT_CHECK_CUDA(cudaMemsetAsync(dw, 0, s->n * 4, st));
                 }
-                if (s->zslab || s->emu_z > 1)
+                if (fista)  // x+ = prox(v); no control variate (the momentum kernel checks x+)
+                    rc = pt::launch_tv_prox(P, s->v, lam, d.tv_inner, d.tv_nonneg, s->dp, s->dq,
+                                            s->dw, xn, nullptr, nullptr, 0.f, k, nullptr,
+                                            s->fgp_work, st);
+                else if (s->zslab || s->emu_z > 1)
                     rc = slab_tv_prox(s, lam, pog, xn, k, st);
                 else if (s->rows)
                     rc = rows_tv_prox(s, lam, pog, xn, k, st);
@@ -715,11 +763,22 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
                                             s->fgp_work, st);
                 s->have_duals = true;
                 s->dual_weight = lam;
-            } else {
+            } else if (!fista) {
                 pt::ProfScope ps(&s->ws, PT_PROF_OTHER, st);
                 rc = pt::launch_identity_prox(s->v, s->xhat, xn, s->h, pog, (int64_t)s->n, k,
                                               s->bad, st);
             }
+            if (rc) return rc;
+        }
+        if (fista) {
+            // solvers.py:384-386: t_next, y = x+ + ((t - 1) / t_next)(x+ - x)
+            const double t = s->fista_t;
+            const double t_next = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
+            s->fista_t = t_next;
+            pt::ProfScope ps(&s->ws, PT_PROF_OTHER, st);
+            rc = pt::launch_fista_momentum(d.prox_kind == 1 ? xn : s->v, xc, xn, s->snap,
+                                           (float)((t - 1.0) / t_next), (int64_t)s->n, k, s->bad,
+                                           st);
             if (rc) return rc;
         }
         s->cur = 1 - s->cur;
@@ -786,7 +845,7 @@ int pt_session_emulate_sectors(pt_session* s, int32_t world)
     const int A = P->A;
     s->emu_subsets.assign(world, {});
     s->emu_all.assign(world, nullptr);
-    const int n = (s->d.estimator != PT_EST_FULL) ? s->d.n_subsets : 0;
+    const int n = !full_kind(s->d.estimator) ? s->d.n_subsets : 0;
     for (int g = 0; g < world; ++g) {
         const int lo = (int)((long long)A * g / world), hi = (int)((long long)A * (g + 1) / world);
         int rc = sector_selections(P, n, lo, hi, &s->emu_all[g], &s->emu_subsets[g]);
@@ -921,6 +980,15 @@ int attach_rows(pt_session* s, const NcclApi& api, nccl_comm comm, int rank, int
 }
 
 }  // namespace
+
+int pt_session_override_rank(pt_session* s, int32_t rank, int32_t world)
+{
+    if (!s || world < 1 || rank < 0 || rank >= world) { pt::set_error("bad argument"); return PT_EINVAL; }
+    if (!s->comm) { pt::set_error("session is not attached"); return PT_EINVAL; }
+    s->rank = rank;
+    s->world = world;
+    return build_selections(s);
+}
 
 int pt_session_attach_comm_rows(pt_session* s, pt_comm* c, int32_t row_offset, int32_t rows_total)
 {

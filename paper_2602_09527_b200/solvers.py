@@ -22,7 +22,6 @@ from __future__ import annotations
 
 import ctypes
 import math
-import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -35,7 +34,7 @@ from .metrics import psnr as _psnr
 from .metrics import relative_error_sq as _relative_error_sq
 from .metrics import ssim as _ssim
 from .projector import Projector, as_device
-from .regularizers import TvDualState, TvProxConfig, tv_prox, tv_value
+from .regularizers import TvDualState, TvProxConfig, tv_value
 
 RUN_COLUMNS = ("data_passes", "wall_seconds", "rel_err", "psnr", "ssim",
                "prox_calls", "objective")
@@ -119,7 +118,8 @@ class TomoProblem:
 class _Session:
     """Owner of a native pt_session (device-resident solver state)."""
 
-    def __init__(self, config: SolverConfig, problem: TomoProblem, x0, stream):
+    def __init__(self, config: SolverConfig, problem: TomoProblem, x0, stream,
+                 kind: str | None = None):
         if problem.denoiser is not None:
             raise NotImplementedError("plug-and-play denoisers are out of scope (DESIGN.md)")
         lib = N.lib()
@@ -127,7 +127,9 @@ class _Session:
         self.data = problem.device_data()
         self.stream = stream
         tv = problem.tv
-        desc = N.SolverDesc(N.EST_CODES[config.estimator], int(config.n_subsets),
+        # kind: the session's step ("fista" for run_fista; default the estimator)
+        code = N.SESSION_KINDS[kind] if kind else N.EST_CODES[config.estimator]
+        desc = N.SolverDesc(code, int(config.n_subsets),
                             float(config.gamma), float(config.skip_probability),
                             1 if tv is not None else 0, float(tv.alpha) if tv else 0.0,
                             int(tv.inner_iterations) if tv else 0,
@@ -288,7 +290,7 @@ class RunRecord:
 
 def _init_state(config: SolverConfig, problem: TomoProblem, x0, stream=None,
                 data_parallel: bool = False, zslab: tuple | None = None,
-                rowslab: tuple | None = None) -> IterateState:
+                rowslab: tuple | None = None, kind: str | None = None) -> IterateState:
     """solvers.py:159-186: x0 (or zeros), h = 0, three PCG64 streams, the
     staggered partition, SAGA zeros, SVRG initial snapshot (+1 pass).
 
@@ -305,7 +307,7 @@ def _init_state(config: SolverConfig, problem: TomoProblem, x0, stream=None,
         partition = build_staggered_partition(problem.projector.geometry.n_angles,
                                               config.n_subsets)
     stream = stream if stream is not None else torch.cuda.current_stream()
-    session = _Session(config, problem, x0, stream)
+    session = _Session(config, problem, x0, stream, kind)
     if zslab is not None:
         from . import distributed as _dist
         _dist.attach_zslab(session, zslab[0], zslab[2])
@@ -320,6 +322,8 @@ def _init_state(config: SolverConfig, problem: TomoProblem, x0, stream=None,
                          rng_theta=np.random.default_rng(streams[1]),
                          rng_refresh=np.random.default_rng(streams[2]), zslab=zslab,
                          rowslab=rowslab)
+    if kind == "fista":
+        session.init()  # y = x0, t = 1 (solvers.py:378)
     if config.estimator in ("svrg", "lsvrg"):
         if config.estimator == "svrg":
             state.svrg_period = config.n_subsets
@@ -461,19 +465,28 @@ def _metrics_row(passes, wall, x, reference, ground_truth, prox_calls, problem,
 
 def run(config: SolverConfig, problem: TomoProblem, x0=None, reference=None,
         ground_truth=None, record_objective: bool = False, stream=None,
-        data_parallel: bool = False, decomposition: str = "rows") -> RunRecord:
+        data_parallel: bool = False, decomposition: str = "sectors") -> RunRecord:
     """Run the skip-capable loop until tolerance or budget exhaustion (:327-336).
 
     Rows are logged at every data-pass boundary exactly as :280-324; the
     iterations between two rows are one native segment.  The host syncs only
     at rows that need a metric (or for a time budget) and at the end.
     data_parallel=True shards the work over the torch.distributed ranks (every
-    rank calls run with the same arguments): the image rows (decomposition
-    "rows", default) or the projection angles ("sectors") of a 2D problem, the
+    rank calls run with the same arguments): the projection angles
+    (decomposition "sectors", default: image and prox replicated) or the image
+    rows ("rows") of a 2D problem, the
     z-slabs of a slice-stacked 3D one (the returned image is the gathered
     image / volume on every rank)."""
+    return _run(config, problem, x0, reference, ground_truth, record_objective, stream,
+                data_parallel, decomposition)
+
+
+def _run(config, problem, x0, reference, ground_truth, record_objective, stream,
+         data_parallel, decomposition, kind: str | None = None) -> RunRecord:
     if decomposition not in ("rows", "sectors"):
         raise ValueError("decomposition must be 'rows' or 'sectors'")
+    if kind == "fista" and data_parallel and decomposition == "rows":
+        raise ValueError("FISTA shards over angle sectors only")
     stream = stream if stream is not None else torch.cuda.current_stream()
     work, zs, rs = problem, None, None
     if (data_parallel and decomposition == "rows"
@@ -495,7 +508,7 @@ def run(config: SolverConfig, problem: TomoProblem, x0=None, reference=None,
             x0 = as_device(x0)[z0:z1].contiguous().reshape(work.projector.shape)
     with torch.cuda.stream(stream):
         state = _init_state(config, work, x0, stream, data_parallel=data_parallel, zslab=zs,
-                            rowslab=rs)
+                            rowslab=rs, kind=kind)
         return _run_loop(state, config, problem, reference, ground_truth, record_objective,
                          stream)
 
@@ -601,97 +614,35 @@ def _diverged(bad: int, config: SolverConfig, record: RunRecord) -> DivergenceEr
 # native operators.  They keep the reference's loop and logging semantics.
 # ----------------------------------------------------------------------------
 
-def _apply_prox_simple(target, tau, problem, warm):
-    if problem.tv is not None:
-        w = warm if problem.tv.warm_start else None
-        return tv_prox(target, tau, problem.tv, w)
-    if problem.denoiser is not None:
-        raise NotImplementedError("plug-and-play denoisers are out of scope (DESIGN.md)")
-    return target, warm
-
-
-def _full_loop(config, problem, x0, reference, ground_truth, record_objective, step_fn):
-    """_run_loop semantics (:280-324) for the full-gradient solvers (1 pass/iteration)."""
-    record = RunRecord()
-    shape = problem.projector.shape
-    x = torch.zeros(shape, device="cuda") if x0 is None else as_device(x0).clone()
-    ctx = {"x": x, "warm": None, "k": 0, "passes": 0.0, "prox": 0, "work": 0.0}
-
-    def log_row():
-        row = _metrics_row(ctx["passes"], ctx["work"], ctx["x"], reference, ground_truth,
-                           ctx["prox"], problem, record_objective)
-        record.rows.append(row)
-        record.iterations.append(ctx["k"])
-        return row
-
-    def satisfied(row):
-        rel = row[2]
-        return config.tolerance is not None and rel is not None and rel < config.tolerance
-
-    row = log_row()
-    if satisfied(row):
-        record.image = ctx["x"].clone()
-        return record
-    last_floor = math.floor(ctx["passes"] + 1e-12)
-    while True:
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        step_fn(ctx)
-        torch.cuda.synchronize()
-        ctx["work"] += time.perf_counter() - t0
-        if not bool(torch.isfinite(ctx["x"]).all()):
-            record.image = None
-            raise DivergenceError(ctx["k"] - 1, config.gamma, record)
-        exhausted = ctx["passes"] >= config.max_data_passes - 1e-9
-        if config.time_budget is not None:
-            exhausted = exhausted or ctx["work"] >= config.time_budget
-        crossed = math.floor(ctx["passes"] + 1e-12) > last_floor
-        if crossed or exhausted:
-            last_floor = math.floor(ctx["passes"] + 1e-12)
-            row = log_row()
-            if satisfied(row) or exhausted:
-                break
-    record.image = ctx["x"].clone()
-    return record
+def _full_gradient_config(config: SolverConfig) -> SolverConfig:
+    """The reference's ISTA / FISTA keep only these fields of the caller's
+    config (solvers.py:346-350,371-375): full gradient, no skipping."""
+    return SolverConfig(gamma=config.gamma, max_data_passes=config.max_data_passes,
+                        tolerance=config.tolerance, time_budget=config.time_budget,
+                        seed=config.seed)
 
 
 def run_ista(config: SolverConfig, problem: TomoProblem, x0=None, reference=None,
-             ground_truth=None, record_objective: bool = False) -> RunRecord:
-    """x+ = prox_gamma(x - gamma grad f(x)) (:339-364)."""
-    gamma = config.gamma
-
-    def step(ctx):
-        grad = est.full_gradient(ctx["x"], problem.projector, problem.device_data())
-        ctx["x"], ctx["warm"] = _apply_prox_simple(ctx["x"] - gamma * grad, gamma, problem,
-                                                   ctx["warm"])
-        ctx["prox"] += 1
-        ctx["k"] += 1
-        ctx["passes"] += 1.0
-
-    return _full_loop(config, problem, x0, reference, ground_truth, record_objective, step)
+             ground_truth=None, record_objective: bool = False, stream=None,
+             data_parallel: bool = False) -> RunRecord:
+    """x+ = prox_gamma(x - gamma grad f(x)) (:339-364), on the native executor:
+    ProxSkip with the full-gradient estimator at p = 1 is exactly this step
+    (hcoef = gamma - gamma/p = 0, so h never reaches x), with the same pass
+    accounting (1 per iteration) and rows."""
+    return _run(_full_gradient_config(config), problem, x0, reference, ground_truth,
+                record_objective, stream, data_parallel, "sectors")
 
 
 def run_fista(config: SolverConfig, problem: TomoProblem, x0=None, reference=None,
-              ground_truth=None, record_objective: bool = False) -> RunRecord:
-    """Accelerated variant, prox every iteration (:367-392)."""
-    gamma = config.gamma
-    aux = {"y": None, "t": 1.0}
-
-    def step(ctx):
-        if aux["y"] is None:
-            aux["y"] = ctx["x"].clone()
-        grad = est.full_gradient(aux["y"], problem.projector, problem.device_data())
-        x_next, ctx["warm"] = _apply_prox_simple(aux["y"] - gamma * grad, gamma, problem,
-                                                 ctx["warm"])
-        ctx["prox"] += 1
-        t_next = (1.0 + math.sqrt(1.0 + 4.0 * aux["t"] * aux["t"])) / 2.0
-        aux["y"] = x_next + ((aux["t"] - 1.0) / t_next) * (x_next - ctx["x"])
-        aux["t"] = t_next
-        ctx["x"] = x_next
-        ctx["k"] += 1
-        ctx["passes"] += 1.0
-
-    return _full_loop(config, problem, x0, reference, ground_truth, record_objective, step)
+              ground_truth=None, record_objective: bool = False, stream=None,
+              data_parallel: bool = False) -> RunRecord:
+    """Accelerated variant, prox every iteration (:367-392), on the native
+    executor: per step one fused full-gradient pass at the momentum point y
+    (forward - b, gather + y - gamma g), the TV prox, and one momentum kernel
+    (x+ finite check, y = x+ + beta_k (x+ - x)); t_k is kept in float64 on the
+    host side of the session.  No host synchronisation between log rows."""
+    return _run(_full_gradient_config(config), problem, x0, reference, ground_truth,
+                record_objective, stream, data_parallel, "sectors", kind="fista")
 
 
 def run_pdhg_reference(problem: TomoProblem, n_iterations: int, snapshot_at: int | None = None):

@@ -160,6 +160,42 @@ def pdhg_fixtures():
     return out
 
 
+def fista_fixtures():
+    """The reference's run_fista / run_ista (solvers.py:339-392): the 16x16
+    small problem (TV, 40 passes; and without a regulariser) and 20 FISTA
+    passes of BASELINE config 0 from its golden problem."""
+    from proxtomo.solvers import run_fista, run_ista
+    g = P.ParallelGeometry.uniform(10, 23)
+    proj = P.Projector(g, 16, 16)
+    rng = np.random.default_rng(0)
+    truth = np.zeros((16, 16))
+    truth[4:12, 5:11] = 1.0
+    data = proj.forward(truth) + 0.1 * rng.standard_normal((10, 23))
+    lip = proj.norm_sq(iterations=100, seed=0)
+    out = {}
+    for tag, tv in (("tv", TvProxConfig(alpha=0.5, inner_iterations=10)), ("plain", None)):
+        problem = TomoProblem(proj, data, tv=tv)
+        for name, fn in (("fista", run_fista), ("ista", run_ista)):
+            rec = fn(SolverConfig(gamma=1.0 / lip, max_data_passes=40, seed=0), problem,
+                     record_objective=True)
+            key = f"small_{name}_{tag}"
+            out[key + "_image"] = rec.image
+            out[key + "_obj"] = rec.column("objective")
+            out[key + "_prox"] = rec.column("prox_calls")
+            out[key + "_iters"] = np.array(rec.iterations)
+    c0 = np.load(os.path.join(HERE, "reference_c0.npz"))
+    cfg = problems.CONFIGS["c0"]
+    proj = P.Projector(P.ParallelGeometry.uniform(cfg.n_angles, cfg.n_bins), cfg.size, cfg.size)
+    problem = TomoProblem(proj, c0["c0_b"], tv=TvProxConfig(alpha=float(c0["c0_alpha"]),
+                                                            inner_iterations=cfg.fgp_inner))
+    rec = run_fista(SolverConfig(gamma=1.0 / float(c0["c0_L"]), max_data_passes=20, seed=0),
+                    problem, record_objective=True)
+    out["c0_fista_image"] = rec.image
+    out["c0_fista_obj"] = rec.column("objective")
+    out["c0_fista_iters"] = np.array(rec.iterations)
+    return out
+
+
 def config_run(name: str, record_objective=True):
     cfg = problems.CONFIGS[name]
     g = P.ParallelGeometry.uniform(cfg.n_angles, cfg.n_bins)
@@ -203,8 +239,12 @@ def main():
     np.savez_compressed(os.path.join(HERE, "reference_pdhg.npz"), **pdhg_fixtures())
     if "--pdhg-only" in sys.argv:
         return
+    if "--fista-only" in sys.argv:
+        np.savez_compressed(os.path.join(HERE, "reference_fista.npz"), **fista_fixtures())
+        return
     c0 = config_run("c0")
     np.savez_compressed(os.path.join(HERE, "reference_c0.npz"), **c0)
+    np.savez_compressed(os.path.join(HERE, "reference_fista.npz"), **fista_fixtures())
     print("c0 reference work_seconds", float(c0["c0_work_seconds"]), "prox",
           c0["c0_prox"][-1], "iters", c0["c0_iters"][-1])
     if "--c1" in sys.argv:

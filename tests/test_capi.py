@@ -60,3 +60,19 @@ def test_product_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 src = open(os.path.join(root, f), encoding="utf-8").read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_geometry_desc_layout_matches_the_library():
+    lib = N.load()
+    assert lib.pt_geometry_desc_size() == ctypes.sizeof(N.GeometryDesc)
+
+
+def test_reference_binding_loads_standalone():
+    """The Option B binding dlopens the library from its own
+    struct definition and checks the layout; no device needed to load."""
+    from paper_2602_09527_b200 import reference_binding as RB
+    lib = RB.load_library()
+    assert lib.pt_geometry_desc_size() == ctypes.sizeof(RB._GeometryDesc)
+    src = open(RB.__file__, encoding="utf-8").read()
+    # standalone: a maintainer copies this one file next to proxtomo/projector.py
+    assert "from . import" not in src and "from .." not in src

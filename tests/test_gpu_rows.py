@@ -104,3 +104,44 @@ def test_rows_nccl_on_one_rank_is_bitwise_identical(estimator):
         assert b.rows[-1][5] > 0  # prox calls happened
     finally:
         dist.destroy_process_group()
+
+
+def test_rows_snapshot_residual_on_a_nonzero_rank():
+    """In the rows layout every rank owns every angle, so the SVRG snapshot
+    residual A x_snap - b is indexed from angle 0 on every rank (it was once
+    offset by the angle-sector start A*rank/world).  A one-rank communicator
+    whose session is told it is rank 1 of 2 (no TV prox, so no halo traffic)
+    must reproduce the single-GPU SVRG trajectory bit for bit."""
+    import socket
+    import torch.distributed as dist
+    from paper_2602_09527_b200 import SolverConfig, TomoProblem
+    from paper_2602_09527_b200 import distributed as D
+    from paper_2602_09527_b200.solvers import _init_state, _plan_segment
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        proj, data = _small_2d()
+        lip = proj.norm_sq(20, 0)
+        cfg = SolverConfig(gamma=1.0 / lip, skip_probability=0.3, n_subsets=6, estimator="svrg",
+                           max_data_passes=1e9, seed=5)
+        outs = []
+        for rows in (False, True):
+            problem = TomoProblem(proj, data)
+            if rows:
+                H = proj.height
+                st = _init_state(cfg, D.rowslab_problem(problem, 0, H), None,
+                                 rowslab=(0, H, H))
+                N.check(N.lib().pt_session_override_rank(st.session.handle, 1, 2), "override")
+                st.session.init()
+            else:
+                st = _init_state(cfg, problem, None)
+            subs, th, rf, _, _ = _plan_segment(st, cfg, 1 << 40, max_steps=20)
+            assert rf.any()  # a refresh inside the segment
+            st.session.run(subs, th, rf, 0)
+            outs.append(st.x.clone())
+        assert torch.equal(outs[0], outs[1])
+    finally:
+        dist.destroy_process_group()

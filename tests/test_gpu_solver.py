@@ -145,16 +145,70 @@ def test_scalar_contraction_any_p():
             assert float(st.x[0, 0]) == pytest.approx(value, rel=1e-5)
 
 
-def test_ista_fista(small_runs):
+@pytest.fixture(scope="module")
+def fista_ref():
+    import os
+    from conftest import GOLDEN
+    return np.load(os.path.join(GOLDEN, "reference_fista.npz"))
+
+
+@pytest.mark.parametrize("name,tag", [("fista", "tv"), ("fista", "plain"), ("ista", "tv"),
+                                      ("ista", "plain")])
+def test_fista_ista_match_reference(small_runs, fista_ref, name, tag):
+    """Native FISTA (momentum kernel, t_k in float64 on the host side of the
+    session) and ISTA (ProxSkip full/p=1) vs the reference's run_fista /
+    run_ista (solvers.py:339-392): 40 passes, rows and objective."""
+    problem, lip = small_problem(small_runs)
+    if tag == "plain":
+        problem = TomoProblem(problem.projector, small_runs["small_data"])
+    fn = run_fista if name == "fista" else run_ista
+    # estimator / skipping fields are ignored by both (solvers.py:346-350)
+    cfg = SolverConfig(gamma=1.0 / lip, skip_probability=0.3, n_subsets=5, estimator="svrg",
+                       max_data_passes=40, seed=0)
+    rec = fn(cfg, problem, record_objective=True)
+    key = f"small_{name}_{tag}"
+    assert rel_l2(cpu(rec.image), fista_ref[key + "_image"]) <= TOL
+    assert rec.iterations == list(fista_ref[key + "_iters"])
+    assert np.array_equal(rec.column("prox_calls"), fista_ref[key + "_prox"])
+    assert np.allclose(rec.column("objective"), fista_ref[key + "_obj"], rtol=TOL)
+
+
+def test_fista_config0_matches_reference(c0_ref, fista_ref):
+    """20 FISTA passes of BASELINE config 0 (the config-4 f* solver's path)."""
+    cfg = problems.CONFIGS["c0"]
+    proj = Projector(ParallelGeometry.uniform(cfg.n_angles, cfg.n_bins), cfg.size, cfg.size)
+    problem = TomoProblem(proj, c0_ref["c0_b"], tv=TvProxConfig(alpha=float(c0_ref["c0_alpha"]),
+                                                                 inner_iterations=cfg.fgp_inner))
+    rec = run_fista(SolverConfig(gamma=1.0 / float(c0_ref["c0_L"]), max_data_passes=20),
+                    problem, record_objective=True)
+    assert rel_l2(cpu(rec.image), fista_ref["c0_fista_image"]) <= TOL
+    assert np.allclose(rec.column("objective"), fista_ref["c0_fista_obj"], rtol=TOL)
+    assert rec.iterations == list(fista_ref["c0_fista_iters"])
+
+
+def test_fista_one_pass_equals_ista(small_runs):
     problem, lip = small_problem(small_runs)
     cfg = SolverConfig(gamma=1.0 / lip, max_data_passes=1, seed=0)
-    a = run_fista(cfg, problem)
-    b = run_ista(cfg, problem)
-    assert torch.equal(a.image, b.image)
-    cfg = SolverConfig(gamma=1.99 / lip, skip_probability=1.0, estimator="full",
-                       max_data_passes=20, seed=1)
-    ista = run_ista(cfg, problem)
-    assert rel_l2(cpu(ista.image), small_runs["small_full_p1.0_s1_image"]) <= TOL
+    assert torch.equal(run_fista(cfg, problem).image, run_ista(cfg, problem).image)
+
+
+def test_fista_angle_sectors_match_single_device(small_runs):
+    """FISTA on emulated angle sectors (partial gradients summed, then the
+    shared epilogue / prox / momentum): the single-device trajectory."""
+    from paper_2602_09527_b200 import distributed as D
+    from paper_2602_09527_b200.solvers import _full_gradient_config, _init_state, _plan_segment
+    problem, lip = small_problem(small_runs)
+    cfg = _full_gradient_config(SolverConfig(gamma=1.0 / lip, max_data_passes=1e9))
+    outs = []
+    for w in (1, 3):
+        st = _init_state(cfg, TomoProblem(problem.projector, small_runs["small_data"],
+                                          tv=problem.tv), None, kind="fista")
+        if w > 1:
+            D.emulate_sectors(st.session, w)
+        subs, th, rf, _, _ = _plan_segment(st, cfg, 1 << 40, max_steps=25)
+        st.session.run(subs, th, rf, 0)
+        outs.append(cpu(st.x))
+    assert rel_l2(outs[1], outs[0]) <= 1e-5
 
 
 def test_objective(small_runs):
