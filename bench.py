@@ -393,6 +393,11 @@ def roofline_record(cfg, msa, cnt, alg, peak, peak_kind):
     tot = sum(msa[idx[k]] for k in ("fwd_band", "fwd_reduce", "gather_step", "fgp_call",
                                      "snapshot", "other"))
     rec["share_of_profiled_step"] = round(ms[top] / tot, 4) if tot else None
+    sub_name = {"fwd_band": "fwd_band", "gather": "gather_step"}.get(top)
+    if sub_name:  # per launch: the subset launches and the snapshot's all-angle launch
+        i, j = idx[sub_name], idx["snap_" + ("fwd_band" if top == "fwd_band" else "gather")]
+        rec["subset_launch_us"] = round(1e3 * msa[i] / cnt[i], 2) if cnt[i] else None
+        rec["snapshot_launch_us"] = round(1e3 * msa[j] / cnt[j], 2) if cnt[j] else None
     b = ncu_binding(cfg.name, kernel)
     if b:
         fr = {"issue": b.get("issue_frac"), "lsu": b.get("lsu_shared_frac"),

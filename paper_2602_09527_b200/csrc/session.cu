@@ -331,7 +331,7 @@ int full_gradient(pt_session* s, const float* x, float* out, float* res, cudaStr
             }
             // the residual rows of sector g start at its first angle
             const size_t off = (size_t)sg->h_angle[0] * P->Z * P->B;
-            rc = pt::launch_adjoint(P, sg, res + off, out, 1.f, g > 0, nullptr, st);
+            rc = pt::launch_adjoint(P, sg, res + off, out, 1.f, g > 0, nullptr, st, &s->ws);
             if (rc) return rc;
         }
         return PT_OK;
@@ -339,7 +339,7 @@ int full_gradient(pt_session* s, const float* x, float* out, float* res, cudaStr
     if (s->own_all->n == 0) {
         PT_CHECK_CUDA(cudaMemsetAsync(out, 0, s->n * 4, st));
     } else {
-        rc = pt::launch_adjoint(P, s->own_all, res, out, 1.f, 0, nullptr, st);
+        rc = pt::launch_adjoint(P, s->own_all, res, out, 1.f, 0, nullptr, st, &s->ws);
         if (rc) return rc;
     }
     return allreduce(s, out, st);
