@@ -114,7 +114,8 @@ EXPORTED_SYMBOLS = tuple(_SIGS)
 
 
 def library_path() -> str:
-    return _build.LIB
+    """The in-tree library; PT_LIB_OVERRIDE (A/B timing of two builds only)."""
+    return os.environ.get("PT_LIB_OVERRIDE") or _build.LIB
 
 
 def load(build_if_missing: bool = True):
@@ -123,7 +124,7 @@ def load(build_if_missing: bool = True):
     with _lock:
         if _lib is not None:
             return _lib
-        path = _build.LIB
+        path = library_path()
         if not os.path.exists(path):
             if not build_if_missing:
                 raise RuntimeError(f"native library missing: {path}")
