@@ -45,6 +45,47 @@ bool pdl_enabled()
     return on;
 }
 
+typedef CUresult (*fn_encode_tiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static fn_encode_tiled encode_tiled()
+{
+    static fn_encode_tiled fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+                cudaSuccess || q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return (fn_encode_tiled)p;
+    }();
+    return fn;
+}
+
+bool tma_available() { return encode_tiled() != nullptr; }
+
+// float32 tensor of `rank` dims (innermost first, dense), box `box`; zero fill
+// outside the tensor
+int make_map(CUtensorMap* m, const float* base, int rank, const cuuint64_t* dims,
+                    const cuuint32_t* box)
+{
+    fn_encode_tiled enc = encode_tiled();
+    if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return PT_ECUDA; }
+    cuuint64_t strides[4];
+    cuuint64_t acc = 4;
+    for (int d = 0; d + 1 < rank; ++d) {
+        acc *= dims[d];
+        strides[d] = acc;
+    }
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, (void*)base, dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed (%d)", (int)r); return PT_ECUDA; }
+    return PT_OK;
+}
+
 int ensure_smem(const void* kernel, size_t bytes)
 {
     if (bytes <= 48 * 1024) return PT_OK;

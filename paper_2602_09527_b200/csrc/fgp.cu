@@ -1514,44 +1514,6 @@ static int fgp3d_exchange(const Fgp3Slab* sl, int G, int H, int W, int which, bo
     return PT_OK;
 }
 
-typedef CUresult (*fn_encode_tiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static fn_encode_tiled encode_tiled()
-{
-    static fn_encode_tiled fn = [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
-                cudaSuccess || q != cudaDriverEntryPointSuccess)
-            p = nullptr;
-        return (fn_encode_tiled)p;
-    }();
-    return fn;
-}
-
-// float32 tensor of `rank` dims (innermost first, dense), box `box`
-static int make_map(CUtensorMap* m, const float* base, int rank, const cuuint64_t* dims,
-                    const cuuint32_t* box)
-{
-    fn_encode_tiled enc = encode_tiled();
-    if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return PT_ECUDA; }
-    cuuint64_t strides[4];
-    cuuint64_t acc = 4;
-    for (int d = 0; d + 1 < rank; ++d) {
-        acc *= dims[d];
-        strides[d] = acc;
-    }
-    const cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, (void*)base, dims,
-                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed (%d)", (int)r); return PT_ECUDA; }
-    return PT_OK;
-}
-
 template <int TX, int TY, int NS, bool TMA, bool PQ>
 static int fgp3d_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
 {
@@ -1629,7 +1591,7 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
               int sm_count, cudaStream_t st)
 {
     // TMA needs 16-byte row pitch; 64 x 8 tiles, 3-stage ring
-    const bool tma = (W % 4) == 0 && encode_tiled() != nullptr;
+    const bool tma = (W % 4) == 0 && tma_available();
     // PQ form (40 B/voxel, R formed on chip) by default: 14.1 vs 15.35 ms per
     // FGP-100 at 256^3 for the R-state form (52 B/voxel); PT_FGP3_PQ=0 selects it
     static const int pq_env = [] {

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "pt_internal.cuh"
 #include "pt_simd.cuh"
@@ -93,6 +94,7 @@ void forward_config(int cfg, int32_t* ty, int32_t* tx)
 }
 
 struct FwdArgs {
+    int tma;  // row-branch tiles by TMA (W % 4 == 0, 16-byte aligned image)
     const float* x;
     float* partial;
     const AngleTab* tab;
@@ -111,7 +113,7 @@ template <int TY, int TX>
 struct FwdTile {
     static constexpr int HL = ((TY / 2 + 3) + 3) & ~3;     // halo, a multiple of 4 lanes
     static constexpr int NL = TX + 2 * HL;                 // lanes staged per band
-    static constexpr int PITCH_R = NL + 4;                  // row branch: [TY][PITCH_R], 16-B rows
+    static constexpr int PITCH_R = NL;                      // row branch: [TY][NL] (the TMA box)
     static constexpr int PITCH_C = TY + 1;                  // column branch: [NL][PITCH_C]
     static constexpr int BUF = (TY * PITCH_R > NL * PITCH_C) ? TY * PITCH_R : NL * PITCH_C;
     static constexpr int SMEM = BUF * 4;
@@ -316,11 +318,38 @@ __device__ __forceinline__ float ray_band_sum(uint32_t tile_u32, int st_a, int s
     return acc0 + acc1;
 }
 
+// Row-branch tile by TMA: the image as a 4D tensor (4, W/4, H, Z) and one box
+// (4, NL/4, TY, 1) lands as the dense [TY][NL] tile; coordinates outside the
+// image (negative lane origin, the last band, the last tile) are zero-filled
+// by the copy engine, which is exactly the reference's "rays outside the grid
+// contribute 0".  One elected thread issues it; completion on an mbarrier.
+__device__ __forceinline__ void fwd_tma_issue(const CUtensorMap* map, uint32_t dst, uint32_t bar,
+                                              int lane_org, int s0, int z, uint32_t bytes)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes));
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+        "l"(map), "r"(0), "r"(lane_org >> 2), "r"(s0), "r"(z), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void fwd_mbar_wait(uint32_t bar)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "FW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+        "@!p bra FW_%=;\n}" ::"r"(bar));
+}
+
 template <int TY, int TX, int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
+__global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P,
+                                                            const __grid_constant__ CUtensorMap tmap)
 {
     using T = FwdTile<TY, TX>;
-    extern __shared__ float sm[];
+    extern __shared__ __align__(128) float sm[];
+    __shared__ __align__(8) uint64_t s_bar;
     constexpr int CH = 32;
     __shared__ int s_pref[CH + 1];
     __shared__ int2 s_bk[CH];       // {first owned ray, selection slot}
@@ -334,10 +363,18 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
     // warp 0 builds the first chunk's ray tables (static data) while the
     // predecessor drains; the other warps wait for it and stage the image tile
     const bool stager = tid >= 32;
+    const bool tma = P.tma && it.branch == 0;
+    const uint32_t bar = smem_u32(&s_bar);
     if (stager) {
         pdl_wait();  // the image is the predecessor's output
-        stage_tile<TY, TX, NT>(P, it, tile_u32, 32, NT - 32);
-        cp_async_commit();
+        if (tma) {
+            if (tid == 32)
+                fwd_tma_issue(&tmap, tile_u32, bar, it.tile * TX - T::HL, it.band * TY, it.z,
+                              (uint32_t)(TY * T::NL * 4));
+        } else {
+            stage_tile<TY, TX, NT>(P, it, tile_u32, 32, NT - 32);
+            cp_async_commit();
+        }
     }
 
     const int branch = it.branch;
@@ -403,11 +440,14 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P)
             if (tid == 0) s_pref[0] = 0;
         }
         if (!waited) {
-            if (stager) cp_async_wait_all();
-            else pdl_wait();
-            waited = true;
+            if (!stager) pdl_wait();
+            else if (!tma) cp_async_wait_all();
         }
         __syncthreads();
+        if (!waited) {
+            if (tma) fwd_mbar_wait(bar);  // after the barrier: the mbarrier is initialised
+            waited = true;
+        }
         const int total = s_pref[nc];
         int j = 0;
         for (int w = tid; w < total; w += NT) {
@@ -550,6 +590,21 @@ static int run_forward_cfg(pt_plan* plan, Workspace* ws, const pt_selection* sel
         PT_CHECK_LAUNCH();
         x = ws->image;
     }
+    // row-branch tiles by TMA when the image rows are 16-byte granular
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof(tmap));
+    static const bool tma_env = [] {
+        const char* e = getenv("PT_FWD_TMA");
+        return !(e && e[0] == '0');
+    }();
+    int tma_ok = tma_env && (plan->W % 4 == 0) && (((uintptr_t)x & 15) == 0) && T::NL / 4 <= 256;
+    if (tma_ok) {
+        const cuuint64_t dims[4] = {4, (cuuint64_t)plan->W / 4, (cuuint64_t)plan->H,
+                                    (cuuint64_t)plan->Z};
+        const cuuint32_t box[4] = {4, (cuuint32_t)(T::NL / 4), (cuuint32_t)TY, 1};
+        const int rc = make_map(&tmap, x, 4, dims, box);
+        if (rc) return rc;
+    }
     const int nb_row = (plan->H + TY - 1) / TY;
     const int nb_col = (plan->W + TY - 1) / TY;
     const int n_bands = plan->n_bands;
@@ -620,10 +675,11 @@ static int run_forward_cfg(pt_plan* plan, Workspace* ws, const pt_selection* sel
             return PT_EINVAL;
         }
         const dim3 grid(n_tiles, (unsigned)(n_bands * groups), 2 * plan->Z);
+        a.tma = tma_ok;
         {
             ProfScope ps(ws, PT_PROF_FWD_BAND, st);
             PT_CHECK_CUDA(launch_pdl(fwd_band_kernel<TY, TX, NT, MINB>, grid, dim3(NT),
-                                     (size_t)T::SMEM, st, a));
+                                     (size_t)T::SMEM, st, a, tmap));
             PT_CHECK_LAUNCH();
         }
 

@@ -1,6 +1,7 @@
 // Internal declarations shared by the sm_100a kernels and the C ABI.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -148,6 +149,12 @@ struct ProfScope {
     }
     ~ProfScope() { if (p) p->end(st); }
 };
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda):
+// a dense float32 tensor of `rank` dims (innermost first), box `box`, zero
+// fill outside.
+int make_map(CUtensorMap* m, const float* base, int rank, const cuuint64_t* dims,
+             const cuuint32_t* box);
+bool tma_available();
 void workspace_sizes(const pt_plan* plan, size_t* partial_floats, size_t* red_doubles,
                      size_t* image_floats);
 int workspace_alloc(const pt_plan* plan, Workspace* ws);
