@@ -33,6 +33,8 @@
 
 namespace pt {
 
+constexpr int kFgpMaxT = 12;  // inner iterations per launch (2D)
+
 struct FgpArgs {
     int H, W;  // the image (H = global rows)
     // the arrays hold rows [grow0, grow0 + Ha) of the image (row slab with
@@ -43,7 +45,7 @@ struct FgpArgs {
     const float *p_in, *q_in, *r_in, *s_in;  // r_in == nullptr: r = p, s = q (call start)
     float *p_out, *q_out, *r_out, *s_out;
     float lam, eta;
-    float beta[8];
+    float beta[kFgpMaxT];
     int n_iter;
     int halo;
     int nonneg;
@@ -447,7 +449,7 @@ static int fgp2d_tmax(int H, int W)
 {
     static const int env = [] {
         const char* e = getenv("PT_FGP_T");
-        return e ? std::max(1, std::min(8, atoi(e))) : 0;
+        return e ? std::max(1, std::min(kFgpMaxT, atoi(e))) : 0;
     }();
     if (env) return env;
     const int m = std::min(H, W);
@@ -497,9 +499,12 @@ static int run_fgp2d(pt_plan* plan, const float* v, double lam, int inner, int n
         }
         a.lam = (float)lam;
         a.eta = (float)(1.0 / (8.0 * lam));
-        for (int k = 0; k < 8; ++k) a.beta[k] = (k < iters) ? (float)betas[done + k] : 0.f;
+        for (int k = 0; k < kFgpMaxT; ++k) a.beta[k] = (k < iters) ? (float)betas[done + k] : 0.f;
         a.n_iter = iters;
-        a.halo = iters + 1;
+        // T iterations make T rings of the region inexact (each iteration's
+        // stencil reaches one point in every direction); the final launch's
+        // x = v - lam D^T(p, q) needs one ring more
+        a.halo = fin ? iters + 1 : iters;
         a.nonneg = nonneg;
         a.final_ = fin ? 1 : 0;
         a.x_out = x_out;
@@ -619,9 +624,12 @@ static int fgp2d_rows_run_t(const Fgp2Slab* sl, int G, int H, int W, double lam,
             }
             a.lam = (float)lam;
             a.eta = (float)(1.0 / (8.0 * lam));
-            for (int k = 0; k < 8; ++k) a.beta[k] = (k < iters) ? (float)betas[done + k] : 0.f;
+            for (int k = 0; k < kFgpMaxT; ++k) a.beta[k] = (k < iters) ? (float)betas[done + k] : 0.f;
             a.n_iter = iters;
-            a.halo = iters + 1;
+            // T iterations make T rings of the region inexact (each iteration's
+        // stencil reaches one point in every direction); the final launch's
+        // x = v - lam D^T(p, q) needs one ring more
+        a.halo = fin ? iters + 1 : iters;
             a.nonneg = nonneg;
             a.final_ = fin ? 1 : 0;
             a.x_out = sl[g].x_out;
@@ -663,7 +671,8 @@ int fgp2d_rows_run(const Fgp2Slab* sl, int G, int H, int W, double lam, int inne
     // the whole-image tile choice (launch_tv_prox), so T and tiles match
     if (fgp2d_big(H, W))
         return fgp2d_rows_run_t<64, 64, 8>(sl, G, H, W, lam, inner, nonneg, pog, iteration,
-                                           bad_iter, halo, fgp2d_tmax(H, W), st);
+                                           bad_iter, halo,
+                                           std::min(fgp2d_tmax(H, W), kRowGhost - 1), st);
     return fgp2d_rows_run_t<32, 32, 8>(sl, G, H, W, lam, inner, nonneg, pog, iteration, bad_iter,
                                        halo, 3, st);
 }

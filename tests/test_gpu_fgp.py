@@ -156,3 +156,39 @@ def test_fgp_3d_pair_pass_bitwise(tmp_path):
         outs.append(np.load(path))
     for o in outs[1:]:
         assert np.array_equal(outs[0], o)
+
+
+_T_SNIPPET = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {repo!r})
+from paper_2602_09527_b200 import TvProxConfig, tv_prox
+out = []
+for (h, w, inner) in ((2048, 2048, 100), (300, 701, 37), (1000, 130, 13)):
+    rng = np.random.default_rng(h + w)
+    v = torch.tensor(rng.standard_normal((h, w)).cumsum(axis=0) * 0.05 + 0.2, device="cuda",
+                     dtype=torch.float32)
+    x, st = tv_prox(v, 1.0, TvProxConfig(alpha=0.07, inner_iterations=inner))
+    x2, st2 = tv_prox(v, 1.0, TvProxConfig(alpha=0.07, inner_iterations=inner), warm=st)
+    for t in (x, st.p, st.q, x2):
+        out.append(t.detach().cpu().numpy().ravel())
+np.save(sys.argv[1], np.concatenate(out))
+"""
+
+
+def test_fgp_2d_iterations_per_launch_bitwise(tmp_path):
+    """Temporal blocking computes only exact points: any number T of inner
+    iterations per launch (halo T rings, T + 1 on the final launch) gives the
+    bits of one iteration per launch (PT_FGP_T = 1)."""
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for t in ("1", "2", "5", "8", "10", "11", "12", ""):
+        path = tmp_path / f"t{t or 'default'}.npy"
+        env = dict(os.environ, PT_FGP_T=t)
+        subprocess.run([sys.executable, "-c", _T_SNIPPET.format(repo=repo), str(path)],
+                       check=True, env=env, timeout=300)
+        outs.append(np.load(path))
+    for o in outs[1:]:
+        assert np.array_equal(outs[0], o)
