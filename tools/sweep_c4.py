@@ -5,7 +5,14 @@ time-to-objective within 1e-3 relative of a 2000-iteration FISTA reference
 reference has no objective-based stop); plus the projector-only forward +
 adjoint throughput at 4096^2 / 3600 angles / 5800 bins.
 
-    python tools/sweep_c4.py [--fista 2000] [--epochs 100] [--out profiles/sweep_c4.json]
+    python tools/sweep_c4.py [--fista 2000] [--epochs 100] [--max-epochs 3000]
+                             [--out profiles/sweep_c4.json]
+
+Every cell runs up to --max-epochs (same seed, so its first --epochs epochs
+are the BASELINE cell): the JSON reports the time / passes to each relative
+objective gap both within BASELINE's budget and, for the gaps it does not
+reach, how many epochs the same trajectory needed (None: not within
+--max-epochs either).
 """
 
 from __future__ import annotations
@@ -95,6 +102,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--fista", type=int, default=2000)
     ap.add_argument("--epochs", type=int, default=100)
+    ap.add_argument("--max-epochs", type=int, default=3000)
     ap.add_argument("--out", default="profiles/sweep_c4.json")
     ap.add_argument("--harness-dir", default=None,
                     help="also run the reference-schema sweep harness (sweep.run_sweep: per-cell "
@@ -113,18 +121,30 @@ def main():
     cells = []
     for est in ("full", "sgd", "saga", "svrg"):
         for p in (1.0, 0.5, 0.1, 0.05, 0.01):
-            passes = args.epochs * (3.0 if est == "svrg" else 1.0)
+            per_epoch = 3.0 if est == "svrg" else 1.0
             scfg = SolverConfig(gamma=default_gamma(est, lip), skip_probability=p,
                                 n_subsets=cfg.n_subsets if est != "full" else 1, estimator=est,
-                                max_data_passes=passes, seed=0)
+                                max_data_passes=args.max_epochs * per_epoch, seed=0)
             rec = run(scfg, problem, record_objective=True)
+            passes = rec.column("data_passes")
+            within = passes <= args.epochs * per_epoch + 1e-9
+            obj = rec.column("objective")
+            wall = rec.column("wall_seconds")
+            base = int(np.count_nonzero(within)) - 1  # last row inside the BASELINE budget
             tt, tp = time_to_target(rec, target)
+            inside = tp is not None and tp <= args.epochs * per_epoch + 1e-9
             cells.append({"estimator": est, "p": p, "epochs": args.epochs,
-                          "final_objective": float(rec.column("objective")[-1]),
-                          "final_rel_gap": float(rec.column("objective")[-1] / f_star - 1.0),
-                          "prox_calls": int(rec.column("prox_calls")[-1]),
-                          "work_seconds": float(rec.column("wall_seconds")[-1]),
-                          "time_to_1e-3_s": tt, "passes_to_1e-3": tp,
+                          "final_objective": float(obj[base]),
+                          "final_rel_gap": float(obj[base] / f_star - 1.0),
+                          "prox_calls": int(rec.column("prox_calls")[base]),
+                          "work_seconds": float(wall[base]),
+                          "time_to_1e-3_s": tt if inside else None,
+                          "passes_to_1e-3": tp if inside else None,
+                          "epochs_needed_for_1e-3": None if tp is None else tp / per_epoch,
+                          "seconds_needed_for_1e-3": tt,
+                          "long_run": {"epochs": args.max_epochs,
+                                       "final_rel_gap": float(obj[-1] / f_star - 1.0),
+                                       "work_seconds": float(wall[-1])},
                           "time_to_rel_gap": times_to(rec, f_star)})
             print(json.dumps(cells[-1]), flush=True)
     result = {"workload": "BASELINE config 4: 512^2, 720x768, 20 subsets, FGP-TV 100",
