@@ -1,0 +1,12 @@
+#!/bin/bash
+# A round's evidence in one gpurun call: the GPU test suite, bench lines of
+# configs 0-3 (driver defaults for c2), the reference arm.  Outputs in gpurun_out/.
+set -u
+O=gpurun_out; mkdir -p $O
+timeout 2400 python -m pytest tests -m gpu -q -rf --durations=15 > $O/gpu_tests.log 2>&1
+echo "pytest rc=$?" >> $O/gpu_tests.log
+timeout 900 python bench.py --steps 20 --warmup 5 > $O/bench_c2.json 2> $O/bench_c2.err
+timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > $O/bench_ref.json 2> $O/bench_ref.err
+for c in c3 c1 c0; do
+  timeout 900 python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline > $O/bench_$c.json 2> $O/bench_$c.err
+done
