@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "pt_internal.cuh"
@@ -1562,6 +1563,328 @@ static int fgp3d_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
     return PT_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Two inner iterations per HBM pass, register-column form (single slab, TMA,
+// PQ).  A thread owns two x-adjacent columns (f32x2 math) of a BY x 2*BX2
+// tile (the core minus a 2-point ring that the two iterations make inexact)
+// and marches them along z; its columns' values live in registers, only the
+// stencil's in-plane neighbours cross threads (R_y / R_x of the point above /
+// left, u of the point below / right) through shared-memory planes that are
+// double-buffered by step parity, so ONE barrier per plane step serves both
+// iterations.  The iterations run as lagged phases: at step s phase 0 turns
+// the staged P_k, P_{k-1}, v of plane s + 1 into u_k(s + 1) and P_{k+1}(s) and
+// hands R_{k+1}(s) to phase 1 in registers; phase 1 turns it into
+// u_{k+1}(s - 1) and P_{k+2}(s - 2).  Inputs arrive by TMA (one box per array
+// and plane, 16-byte aligned origin, zero fill off the volume) into a 3-stage
+// ring.  Tiles strictly inside the image skip every guard.  Every value is
+// the one-iteration kernel's expression in its operation order, so the pass
+// is bitwise equal to two fgp3d_iter_kernel launches.
+// ---------------------------------------------------------------------------
+template <int BX2, int BY>
+struct Fgp3Col {
+    static constexpr int NT = BX2 * BY;
+    static constexpr int BXP = 2 * BX2;       // tile width in points
+    static constexpr int NS = 3;              // TMA ring stages (planes)
+    static constexpr int BW = BXP + 4;        // staged box width (origin two points left)
+    static constexpr int PL = BW * BY;        // one staged array plane (floats)
+    static constexpr int STAGE = 7 * PL;      // P_k (3), P_{k-1} (3), v
+    static constexpr int XPL = 2 * (NT + 1);  // exchange plane: float2 per thread + zero slot
+    static constexpr int XR = NS * STAGE;     // [2 parity][R_y0, R_x0, R_y1, R_x1][XPL]
+    static constexpr int XU = XR + 8 * XPL;   // [2 parity][u0, u1][XPL]
+    static constexpr int SMEM_FLOATS = XU + 4 * XPL;
+    static constexpr uint32_t TMA_BYTES = (uint32_t)STAGE * 4u;
+    static constexpr int CX = BXP - 4, CY = BY - 4;  // exact core (two rings)
+    static_assert(CX % 4 == 0, "16-byte aligned tile origins (TMA)");
+    static_assert((STAGE * 4) % 128 == 0 && (PL * 4) % 128 == 0, "128-byte aligned TMA boxes");
+};
+
+__device__ __forceinline__ f2 ldx2(const float* p) { return ld2s(p); }
+// per-lane select (lanes a / b)
+__device__ __forceinline__ f2 sel2(bool ca, bool cb, f2 x, f2 y)
+{
+    float xa, xb, ya, yb;
+    upk(x, xa, xb);
+    upk(y, ya, yb);
+    return pk(ca ? xa : ya, cb ? xb : yb);
+}
+
+template <int BX2, int BY, int MINB>
+__global__ void __launch_bounds__(BX2 * BY, MINB)
+    fgp3d_col_kernel(Fgp3Args a, const __grid_constant__ Fgp3Maps m)
+{
+    using T = Fgp3Col<BX2, BY>;
+    constexpr int NT = T::NT, XPL = T::XPL;
+    extern __shared__ __align__(128) float fsm[];
+    __shared__ __align__(8) uint64_t mbar[T::NS];
+    const int tid = threadIdx.x;
+    const int tx = tid % BX2, ty = tid / BX2;
+    const int j0 = blockIdx.x * T::CX - 2, i0 = blockIdx.y * T::CY - 2;
+    const int zb = blockIdx.z * a.zchunk;
+    const int ze = min(a.Zl, zb + a.zchunk);
+    const int H = a.H, W = a.W;  // W even: a pair is inside or outside the image as a whole
+    const size_t HW = (size_t)H * W;
+    const int i = i0 + ty, ja = j0 + 2 * tx;
+    const bool inimg = i >= 0 && i < H && ja >= 0 && ja < W;
+    const bool i_lt = i < H - 1, i_gt = i > 0;
+    const bool jgt_a = ja > 0, jlt_b = ja + 1 < W - 1;  // lane b is never at j = 0, lane a never at W - 1
+    const bool core = tx >= 1 && tx < BX2 - 1 && ty >= 2 && ty < BY - 2 && inimg;
+    // the whole tile and one point around it strictly inside the image: no guards
+    const bool interior = i0 >= 1 && i0 + BY <= H - 1 && j0 >= 1 && j0 + T::BXP <= W - 1;
+    // neighbour slots (float2 index) of the exchange planes; the zero slot off the tile
+    const int n_up = ty > 0 ? tid - BX2 : NT, n_down = ty < BY - 1 ? tid + BX2 : NT;
+    const int n_left = tx > 0 ? tid - 1 : NT, n_right = tx < BX2 - 1 ? tid + 1 : NT;
+    const int own = ty * T::BW + 2 * tx + 2;  // this pair in a staged plane
+    const f2 br2 = pk(a.beta_r, a.beta_r), bk2 = pk(a.beta, a.beta);
+    const f2 eta2 = pk(a.eta, a.eta), nlam2 = pk(-a.lam, -a.lam);
+    const f2 z2 = pk(0.f, 0.f), nz2 = pk(-0.f, -0.f);
+    const bool nonneg = a.nonneg != 0;
+    const int Zg = a.Zg;
+    const uint32_t fsm_u32 = (uint32_t)__cvta_generic_to_shared(fsm);
+    float* XR = fsm + T::XR;
+    float* XU = fsm + T::XU;
+
+    if (tid == 0) {
+        for (int k = 0; k < T::NS; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                (uint32_t)__cvta_generic_to_shared(&mbar[k])));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    if (tid < 12) {  // zero slots of the twelve exchange planes
+        float* pl = (tid < 8 ? XR + tid * XPL : XU + (tid - 8) * XPL) + 2 * NT;
+        pl[0] = 0.f;
+        pl[1] = 0.f;
+    }
+    __syncthreads();
+    pdl_wait();  // the dual sets are the predecessor's output
+    const int pfirst = zb - 2, plast = ze + 2;  // input planes of this run
+    auto issue = [&](int p, int st) {
+        const uint32_t sb = fsm_u32 + (uint32_t)(st * T::STAGE) * 4u;
+        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&mbar[st]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"(T::TMA_BYTES));
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb),
+            "l"(&m.R), "r"(j0 - 2), "r"(i0), "r"(0), "r"(p + 1), "r"(bar) : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb + (uint32_t)(3 * T::PL) * 4u),
+            "l"(&m.P), "r"(j0 - 2), "r"(i0), "r"(0), "r"(p + 1), "r"(bar) : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(sb + (uint32_t)(6 * T::PL) * 4u),
+            "l"(&m.V), "r"(j0 - 2), "r"(i0), "r"(p), "r"(bar) : "memory");
+    };
+    if (tid == 0)
+        for (int k = 0; k < T::NS; ++k) issue(pfirst + k, k);
+
+    // carried state (zeros before the run: they only feed planes outside the
+    // exact cone of [zb, ze))
+    f2 r0p[3] = {z2, z2, z2}, r1p[3] = {z2, z2, z2};  // R_k(s), R_{k+1}(s - 2)
+    f2 r1in[3] = {z2, z2, z2};                        // R_{k+1}(s - 1) (handoff)
+    f2 u0p = z2, u1p = z2;                            // u_k(s), u_{k+1}(s - 2)
+    f2 pk_own[3] = {z2, z2, z2};                      // P_k(s)
+    f2 vq0 = z2, vq1 = z2;                            // v(s), v(s - 1)
+    const ptrdiff_t plane3 = 3 * (ptrdiff_t)HW;
+    const size_t gij = core ? (size_t)i * W + ja : 0;
+    float* o1 = a.Pn + plane3 * (zb - 3) + gij;  // P_{k+1}(s): set index s + 1
+    float* o2 = a.Rn + plane3 * (zb - 5) + gij;  // P_{k+2}(s - 2): set index s - 1
+
+    // u = clamp(v - lam D^T R) in _diff_adjoint's order (+ z).  XYI: the tile
+    // is strictly inside the image (no in-plane guards); ZI: every z guard of
+    // the step holds.  Specialised at compile time so the common case has no
+    // selects and no predicated merges.
+    auto u_of = [&](auto XYI, auto ZI, const f2 (&r)[3], f2 rup, f2 rleft, f2 r2low, f2 v,
+                    bool zhi, bool zlo) {
+        f2 x;
+        if constexpr (decltype(XYI)::value) {
+            x = add2(sub2(add2(sub2(nz2, r[0]), rup), r[1]), rleft);
+        } else {
+            x = i_lt ? sub2(nz2, r[0]) : z2;
+            x = i_gt ? add2(x, rup) : x;
+            x = sel2(true, jlt_b, sub2(x, r[1]), x);
+            x = sel2(jgt_a, true, add2(x, rleft), x);
+        }
+        if constexpr (decltype(ZI)::value) {
+            x = add2(sub2(x, r[2]), r2low);
+        } else {
+            x = zhi ? sub2(x, r[2]) : x;
+            x = zlo ? add2(x, r2low) : x;
+        }
+        float ua, ub;
+        upk(fma2(x, nlam2, v), ua, ub);
+        ua = (nonneg && ua < 0.f) ? 0.f : ua;
+        ub = (nonneg && ub < 0.f) ? 0.f : ub;
+        if constexpr (!decltype(XYI)::value) {
+            ua = inimg ? ua : 0.f;
+            ub = inimg ? ub : 0.f;
+        }
+        return pk(ua, ub);
+    };
+    // the dual step: R + eta D u, projected; zero off the image / volume
+    auto dual = [&](auto XYI, auto ZI, const f2 (&r)[3], f2 uo, f2 udown, f2 uright, f2 uz,
+                    bool top, bool zlive, f2 (&pn)[3]) {
+        f2 gv = sub2(udown, uo), gh = sub2(uright, uo);
+        if constexpr (!decltype(XYI)::value) {
+            gv = i_lt ? gv : z2;
+            gh = sel2(true, jlt_b, gh, z2);
+        }
+        f2 gz;
+        if constexpr (decltype(ZI)::value) gz = sub2(uz, uo);
+        else gz = top ? sub2(uz, uo) : z2;
+        const f2 ph = fma2(gv, eta2, r[0]);
+        const f2 qh = fma2(gh, eta2, r[1]);
+        const f2 wh = fma2(gz, eta2, r[2]);
+        const f2 inv = inv_norm2(fma2(wh, wh, fma2(qh, qh, mul2(ph, ph))));  // pinned order
+        pn[0] = mul2(ph, inv);
+        pn[1] = mul2(qh, inv);
+        pn[2] = mul2(wh, inv);
+        if constexpr (!(decltype(XYI)::value && decltype(ZI)::value)) {
+            const bool live = zlive && inimg;
+            pn[0] = live ? pn[0] : z2;
+            pn[1] = live ? pn[1] : z2;
+            pn[2] = live ? pn[2] : z2;
+        }
+    };
+
+    int stg = 0;         // stage of plane s + 1
+    uint32_t phase = 0;  // bit k: parity of stage k's next completion
+    // One plane step.  The two-deep shift registers (R_{k+1}: previous /
+    // handoff, v: v(s) / v(s - 1)) and the one-deep ones are passed by role,
+    // so the loop below alternates roles every step instead of moving values.
+    auto step = [&](auto XYI, auto ZI, int s, f2 (&r1_prev)[3], f2 (&r1_in)[3],
+                    f2 (&r0_prev)[3], f2 (&r0_cur)[3], f2 (&pk_prev)[3], f2 (&pk_cur)[3],
+                    f2& u0_prev, f2& u0_cur, f2& u1_prev, f2& u1_cur, f2& v_m1) {
+        const int par = s & 1;
+        mbar_wait((uint32_t)__cvta_generic_to_shared(&mbar[stg]), (phase >> stg) & 1u);
+        phase ^= 1u << stg;
+        const float* sp = fsm + stg * T::STAGE + own;
+        const f2 v1 = ldx2(sp + 6 * T::PL);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            pk_cur[c] = ldx2(sp + c * T::PL);
+            r0_cur[c] = fma2(sub2(pk_cur[c], ldx2(sp + (3 + c) * T::PL)), br2, pk_cur[c]);  // R_k(s + 1)
+        }
+        float* xr = XR + par * 4 * XPL;
+        st2s(xr + 2 * tid, r0_cur[0]);
+        st2s(xr + XPL + 2 * tid, r0_cur[1]);
+        st2s(xr + 2 * XPL + 2 * tid, r1_in[0]);
+        st2s(xr + 3 * XPL + 2 * tid, r1_in[1]);
+        __syncthreads();  // exchange planes of step s written; step s - 1 fully read
+        // the stage of plane s (read at step s - 1) takes plane s + NS
+        if (tid == 0 && s >= pfirst && s + T::NS <= plast)
+            issue(s + T::NS, stg == 0 ? T::NS - 1 : stg - 1);
+        stg = stg + 1 == T::NS ? 0 : stg + 1;
+        const float* xu_prev = XU + (par ^ 1) * 2 * XPL;
+        float* xu = XU + par * 2 * XPL;
+        const int z1 = a.z0 + s + 1, z0 = a.z0 + s, zm1 = a.z0 + s - 1, zm2 = a.z0 + s - 2;
+        // ---- phase 0: u_k(s + 1), P_{k+1}(s)
+        u0_cur = u_of(XYI, ZI, r0_cur, ldx2(xr + 2 * n_up),
+                      pk(xr[XPL + 2 * n_left + 1], lo_of(r0_cur[1])), r0_prev[2], v1,
+                      z1 < Zg - 1, z1 > 0);
+        st2s(xu + 2 * tid, u0_cur);
+        f2 p1[3];
+        dual(XYI, ZI, r0_prev, u0_prev, ldx2(xu_prev + 2 * n_down),
+             pk(hi_of(u0_prev), xu_prev[2 * n_right]), u0_cur, z0 < Zg - 1, z0 >= 0 && z0 < Zg,
+             p1);
+        // ---- phase 1: u_{k+1}(s - 1), P_{k+2}(s - 2)
+        u1_cur = u_of(XYI, ZI, r1_in, ldx2(xr + 2 * XPL + 2 * n_up),
+                      pk(xr[3 * XPL + 2 * n_left + 1], lo_of(r1_in[1])), r1_prev[2], v_m1,
+                      zm1 < Zg - 1, zm1 > 0);
+        st2s(xu + XPL + 2 * tid, u1_cur);
+        f2 p2[3];
+        dual(XYI, ZI, r1_prev, u1_prev, ldx2(xu_prev + XPL + 2 * n_down),
+             pk(hi_of(u1_prev), xu_prev[XPL + 2 * n_right]), u1_cur, zm2 < Zg - 1,
+             zm2 >= 0 && zm2 < Zg, p2);
+        // ---- outputs of the run's own planes (exact core only)
+        o1 += plane3;
+        o2 += plane3;
+        if (core && s >= zb && s < ze) {
+            st2s(o1, p1[0]); st2s(o1 + HW, p1[1]); st2s(o1 + 2 * HW, p1[2]);
+        }
+        if (core && s - 2 >= zb && s - 2 < ze) {
+            st2s(o2, p2[0]); st2s(o2 + HW, p2[1]); st2s(o2 + 2 * HW, p2[2]);
+        }
+        // R_{k+1}(s) for phase 1 (the R-form expression) takes the slot of
+        // R_{k+1}(s - 2), consumed above; v(s + 1) takes v(s - 1)'s
+#pragma unroll
+        for (int c = 0; c < 3; ++c) r1_prev[c] = fma2(sub2(p1[c], pk_prev[c]), bk2, p1[c]);
+        v_m1 = v1;
+    };
+    // roles: even steps (A) and odd steps (B); steps whose planes s - 2 .. s + 1
+    // are all inside [1, Zg - 2] pass every z guard (ZI)
+    f2 r0q[3] = {z2, z2, z2}, pkq[3] = {z2, z2, z2};
+    f2 u0q = z2, u1q = z2;
+    auto march = [&](auto XYI) {
+        const std::true_type zi{};
+        const std::false_type zg{};
+        int s = zb - 3;
+        for (; s + 1 <= ze + 1; s += 2) {
+            const int g0 = a.z0 + s;
+            if (g0 - 2 >= 1 && g0 + 2 <= Zg - 2) {
+                step(XYI, zi, s, r1p, r1in, r0p, r0q, pk_own, pkq, u0p, u0q, u1p, u1q, vq1);
+                step(XYI, zi, s + 1, r1in, r1p, r0q, r0p, pkq, pk_own, u0q, u0p, u1q, u1p, vq0);
+            } else {
+                step(XYI, zg, s, r1p, r1in, r0p, r0q, pk_own, pkq, u0p, u0q, u1p, u1q, vq1);
+                step(XYI, zg, s + 1, r1in, r1p, r0q, r0p, pkq, pk_own, u0q, u0p, u1q, u1p, vq0);
+            }
+        }
+        if (s <= ze + 1) step(XYI, zg, s, r1p, r1in, r0p, r0q, pk_own, pkq, u0p, u0q, u1p, u1q, vq1);
+    };
+    if (interior) march(std::true_type{});
+    else march(std::false_type{});
+    pdl_trigger();
+}
+
+template <int BX2, int BY, int MINB>
+static int fgp3d_col_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
+{
+    using T = Fgp3Col<BX2, BY>;
+    const size_t smem = (size_t)T::SMEM_FLOATS * 4;
+    {
+        const int rc = ensure_smem((const void*)fgp3d_col_kernel<BX2, BY, MINB>, smem);
+        if (rc) return rc;
+    }
+    int per_sm = 0;
+    PT_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, fgp3d_col_kernel<BX2, BY, MINB>, T::NT, smem));
+    Fgp3Maps m;
+    memset(&m, 0, sizeof(m));
+    const cuuint64_t W = a.W, H = a.H;
+    const cuuint64_t d4[4] = {W, H, 3, (cuuint64_t)a.Zl + 2};
+    const cuuint32_t b4[4] = {(cuuint32_t)T::BW, (cuuint32_t)BY, 3, 1};
+    const cuuint64_t d3[3] = {W, H, (cuuint64_t)a.Zl};
+    const cuuint32_t b3[3] = {(cuuint32_t)T::BW, (cuuint32_t)BY, 1};
+    int rc = make_map(&m.R, a.R, 4, d4, b4);
+    if (!rc) rc = make_map(&m.P, a.P, 4, d4, b4);
+    if (!rc) rc = make_map(&m.V, a.v, 3, d3, b3);
+    if (rc) return rc;
+    static const int zc_env = [] {
+        const char* e = getenv("PT_FGP3_ZCHUNK");
+        return e ? std::max(0, atoi(e)) : 0;
+    }();
+    const int tiles = ((a.W + T::CX - 1) / T::CX) * ((a.H + T::CY - 1) / T::CY);
+    // z-runs: each re-marches 5 planes; as few runs as fill whole waves
+    int zc = zc_env;
+    if (!zc) {
+        const int slots = sm_count * std::max(1, per_sm);
+        int best_cost = INT32_MAX;
+        zc = a.Zl;
+        for (int c = 1; c <= std::max(1, a.Zl / 8); ++c) {
+            const int run = (a.Zl + c - 1) / c;
+            const int waves = (tiles * c + slots - 1) / slots;
+            const int cost = waves * (run + 5);
+            if (cost < best_cost) { best_cost = cost; zc = run; }
+        }
+    }
+    a.zchunk = zc;
+    const dim3 grid((a.W + T::CX - 1) / T::CX, (a.H + T::CY - 1) / T::CY,
+                    (a.Zl + a.zchunk - 1) / a.zchunk);
+    PT_CHECK_CUDA(launch_pdl(fgp3d_col_kernel<BX2, BY, MINB>, grid, dim3(T::NT), smem, st, a, m));
+    PT_CHECK_LAUNCH();
+    return PT_OK;
+}
+
 template <int TX, int TY, int NT, bool X2>
 static int fgp3d_pair_launch(Fgp3Args& a, cudaStream_t st)
 {
@@ -1635,10 +1958,13 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
     // One slab holding the whole volume: two iterations per pass (sets 0/1 and
     // 2/3 alternate as {P_{k-1}, P_k} -> {P_{k+1}, P_{k+2}}; the first pass
     // reads set 0 twice, P_{-1} = P_0 with beta_r = 0), an odd last iteration
-    // by the one-iteration kernel.  PT_FGP3_PAIR=0 disables it.
+    // by the one-iteration kernel.  PT_FGP3_PAIR selects the pass kernel: 6
+    // (default) the register-column kernel with 32 x 16-point tiles; 5 / 7 / 8
+    // other column tiles; 1-4 the windowed pair kernel; 0 none (one iteration
+    // per pass).  256^3 FGP-100: 9.2 ms (6), 11.7 ms (1), 14.0 ms (0).
     static const int pair_env = [] {
         const char* e = getenv("PT_FGP3_PAIR");
-        return e ? atoi(e) : 1;
+        return (e && *e) ? atoi(e) : 6;
     }();
     if (G == 1 && (!halo || halo->world <= 1) && tma && pq && pair_env && inner >= 2 &&
         sl[0].z0 == 0 && sl[0].Zl == Zg) {
@@ -1661,12 +1987,15 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
             a.beta = (float)betas[kk];
             a.beta_r = kk == 0 ? 0.f : (float)betas[kk - 1];
             a.nonneg = nonneg;
-            // 256^3 FGP-100: 12.2 ms (64 x 8 tiles, 256 threads, 32-plane runs);
-            // 13.8 ms with 512 threads; 14.0 ms one iteration per pass
-            // point pairs with f32x2 math (X2, PT_FGP3_PAIR=1): 12.3 -> 11.7 ms;
-            // 2 / 3 / 4 select one point per lane with 512 threads, X2 with
-            // 384 threads (11.7 ms), one point per lane with 256 threads
-            rc = pair_env == 2 ? fgp3d_pair_launch<64, 8, 512, false>(a, st)
+            // windowed pair kernel, 256^3 FGP-100: 12.2 ms (64 x 8 tiles, 256
+            // threads, 32-plane runs), 13.8 ms with 512 threads; point pairs
+            // with f32x2 math (1): 11.7 ms; 2 / 3 / 4 one point per lane with
+            // 512 threads, X2 with 384 threads, one point per lane with 256
+            rc = pair_env == 5 ? fgp3d_col_launch<16, 16, 2>(a, sm_count, st)
+               : pair_env == 6 ? fgp3d_col_launch<16, 16, 3>(a, sm_count, st)
+               : pair_env == 7 ? fgp3d_col_launch<32, 16, 1>(a, sm_count, st)
+               : pair_env == 8 ? fgp3d_col_launch<16, 24, 2>(a, sm_count, st)
+               : pair_env == 2 ? fgp3d_pair_launch<64, 8, 512, false>(a, st)
                : pair_env == 3 ? fgp3d_pair_launch<64, 8, 384, true>(a, st)
                : pair_env == 4 ? fgp3d_pair_launch<64, 8, 256, false>(a, st)
                                : fgp3d_pair_launch<64, 8, 256, true>(a, st);

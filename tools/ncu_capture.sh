@@ -8,7 +8,7 @@ B="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-profile"
 cap() {  # config regex skip name per_call
   local cfg=$1 rx=$2 skip=$3 name=$4 pc=$5
   # reports stay on the box (/tmp): only the raw CSV digests come back (gpurun_out <= 64 MiB)
-  timeout 900 ncu --set full --import-source on --clock-control none -k regex:$rx -s $skip -c 1 \
+  timeout 900 ncu --set full --import-source on --clock-control none -f -k regex:$rx -s $skip -c 1 \
       -o /tmp/ncu_${cfg}_${name} $B --config $cfg > $O/ncu_${cfg}_${name}.log 2>&1
   ncu -i /tmp/ncu_${cfg}_${name}.ncu-rep --page raw --csv > $O/raw_${cfg}_${name}.csv 2>/dev/null
   python tools/ncu_roofline.py $O/ncu_roofline.json $cfg $name $O/raw_${cfg}_${name}.csv $pc
