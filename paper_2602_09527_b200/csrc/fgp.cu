@@ -711,12 +711,17 @@ struct Fgp3Args {
     float lam, eta, beta;  // beta = beta_k (momentum of the output)
     float beta_r;          // PQ form: R_k = P_k + beta_r (P_k - P_{k-1}) formed on chip
     int nonneg;
+    // register-column pass on a z-slab: planes -2, -1 / Zl, Zl + 1 come from
+    // 2-plane ghost buffers [side][P_k: 2 x 3 planes, P_{k-1}: 2 x 3, v: 2]
+    // (fgp3d_ghost_exchange) instead of the sets' one-plane ghosts
+    const float* ghost = nullptr;
 };
 
 // TMA descriptors of one launch: R_k and P_k as 4D tensors (W, H, 3, Zl + 2),
 // v as (W, H, Zl), its ghost plane as (W, H); zero fill outside.
 struct Fgp3Maps {
     CUtensorMap R, P, V, Vt;
+    CUtensorMap Rg[2], Pg[2], Vg[2];  // column pass on a z-slab: lower / upper ghosts
 };
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
@@ -1469,8 +1474,13 @@ __global__ void fgp3d_final_kernel(Fgp3Args a, float* p_out, float* q_out, float
 
 int64_t fgp3d_slab_floats(int Zl, int H, int W)
 {
-    // four sets (P, R ping-pong) + the ghost plane of v
-    return 12 * (int64_t)(Zl + 2) * H * W + (int64_t)H * W;
+    // four sets (P, R ping-pong) + the ghost plane of v + the column pass's
+    // 2-plane ghosts (2 sides x (2 x 3 + 2 x 3 + 2) planes)
+    return 12 * (int64_t)(Zl + 2) * H * W + (int64_t)H * W + 28 * (int64_t)H * W;
+}
+static inline float* fgp3d_ghost(float* work, int side, int Zl, int H, int W)
+{
+    return work + 12 * (size_t)(Zl + 2) * H * W + (size_t)H * W + (size_t)side * 14 * H * W;
 }
 
 // set k of a slab workspace: 0 / 1 = P, R of the even iterations, 2 / 3 = odd
@@ -1518,6 +1528,47 @@ static int fgp3d_exchange(const Fgp3Slab* sl, int G, int H, int W, int which, bo
         if (with_v) {
             rc = halo->exchange(halo->ctx, f.v, nullptr, nullptr, fgp3d_vtop(l.work, l.Zl, H, W),
                                 HW, st);
+            if (rc) return rc;
+        }
+    }
+    return PT_OK;
+}
+
+// The column pass's 2-plane ghosts of z-slab g: its lower buffer receives the
+// two top planes of slab g - 1, its upper buffer the two bottom planes of
+// slab g + 1, for the sets of P_k and P_{k-1} (and for v when with_v), by
+// device copies between local slabs and the halo callback (ncclSend /
+// ncclRecv) between ranks.  Buffers on the global boundary stay zero.
+static int fgp3d_ghost_exchange(const Fgp3Slab* sl, int G, int H, int W, int set_k, int set_m,
+                                bool with_v, const ZHalo* halo, cudaStream_t st)
+{
+    const size_t HW = (size_t)H * W, plane3 = 3 * HW;
+    // (source of the two planes [lo, lo + 1] of slab g, offset in a ghost side, count)
+    struct Arr { int kind; size_t goff, count; };  // kind 0: set k, 1: set m, 2: v
+    const Arr arrs[3] = {{0, 0, 2 * plane3}, {1, 6 * HW, 2 * plane3}, {2, 12 * HW, 2 * HW}};
+    auto src = [&](const Fgp3Slab& q, const Arr& ar, bool top) -> const float* {
+        if (ar.kind == 2) return q.v + (top ? (size_t)(q.Zl - 2) * HW : 0);
+        const float* set = fgp3d_set(q.work, ar.kind == 0 ? set_k : set_m, q.Zl, H, W);
+        return set + (top ? (size_t)(q.Zl - 1) * plane3 : plane3);  // set index = plane + 1
+    };
+    for (const Arr& ar : arrs) {
+        if (ar.kind == 2 && !with_v) continue;
+        for (int g = 0; g < G; ++g) {
+            float* lo = fgp3d_ghost(sl[g].work, 0, sl[g].Zl, H, W) + ar.goff;
+            float* hi = fgp3d_ghost(sl[g].work, 1, sl[g].Zl, H, W) + ar.goff;
+            if (g > 0)
+                PT_CHECK_CUDA(cudaMemcpyAsync(lo, src(sl[g - 1], ar, true), ar.count * 4,
+                                              cudaMemcpyDeviceToDevice, st));
+            if (g + 1 < G)
+                PT_CHECK_CUDA(cudaMemcpyAsync(hi, src(sl[g + 1], ar, false), ar.count * 4,
+                                              cudaMemcpyDeviceToDevice, st));
+        }
+        if (halo && halo->world > 1) {
+            const Fgp3Slab& f = sl[0];
+            const Fgp3Slab& l = sl[G - 1];
+            const int rc = halo->exchange(
+                halo->ctx, src(f, ar, false), fgp3d_ghost(f.work, 0, f.Zl, H, W) + ar.goff,
+                src(l, ar, true), fgp3d_ghost(l.work, 1, l.Zl, H, W) + ar.goff, ar.count, st);
             if (rc) return rc;
         }
     }
@@ -1660,20 +1711,28 @@ __global__ void __launch_bounds__(BX2 * BY, MINB)
     auto issue = [&](int p, int st) {
         const uint32_t sb = fsm_u32 + (uint32_t)(st * T::STAGE) * 4u;
         const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&mbar[st]);
+        // a slab's planes outside [0, Zl) come from its ghost buffers
+        const bool gh = a.ghost && (p < 0 || p >= a.Zl);
+        const int side = p < 0 ? 0 : 1;
+        const CUtensorMap* mr = gh ? &m.Rg[side] : &m.R;
+        const CUtensorMap* mp = gh ? &m.Pg[side] : &m.P;
+        const CUtensorMap* mv = gh ? &m.Vg[side] : &m.V;
+        const int pz = gh ? (p < 0 ? p + 2 : p - a.Zl) : p + 1;  // set / ghost plane index
+        const int vz = gh ? pz : p;
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
                      "r"(T::TMA_BYTES));
         asm volatile(
             "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
             " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb),
-            "l"(&m.R), "r"(j0 - 2), "r"(i0), "r"(0), "r"(p + 1), "r"(bar) : "memory");
+            "l"(mr), "r"(j0 - 2), "r"(i0), "r"(0), "r"(pz), "r"(bar) : "memory");
         asm volatile(
             "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
             " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb + (uint32_t)(3 * T::PL) * 4u),
-            "l"(&m.P), "r"(j0 - 2), "r"(i0), "r"(0), "r"(p + 1), "r"(bar) : "memory");
+            "l"(mp), "r"(j0 - 2), "r"(i0), "r"(0), "r"(pz), "r"(bar) : "memory");
         asm volatile(
             "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
             " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(sb + (uint32_t)(6 * T::PL) * 4u),
-            "l"(&m.V), "r"(j0 - 2), "r"(i0), "r"(p), "r"(bar) : "memory");
+            "l"(mv), "r"(j0 - 2), "r"(i0), "r"(vz), "r"(bar) : "memory");
     };
     if (tid == 0)
         for (int k = 0; k < T::NS; ++k) issue(pfirst + k, k);
@@ -1858,6 +1917,17 @@ static int fgp3d_col_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
     int rc = make_map(&m.R, a.R, 4, d4, b4);
     if (!rc) rc = make_map(&m.P, a.P, 4, d4, b4);
     if (!rc) rc = make_map(&m.V, a.v, 3, d3, b3);
+    if (a.ghost) {
+        const size_t HW = (size_t)a.W * a.H;
+        const cuuint64_t g4[4] = {W, H, 3, 2};
+        const cuuint64_t g3[3] = {W, H, 2};
+        for (int side = 0; side < 2 && !rc; ++side) {
+            const float* gb = a.ghost + (size_t)side * 14 * HW;
+            rc = make_map(&m.Rg[side], gb, 4, g4, b4);
+            if (!rc) rc = make_map(&m.Pg[side], gb + 6 * HW, 4, g4, b4);
+            if (!rc) rc = make_map(&m.Vg[side], gb + 12 * HW, 3, g3, b3);
+        }
+    }
     if (rc) return rc;
     static const int zc_env = [] {
         const char* e = getenv("PT_FGP3_ZCHUNK");
@@ -2034,6 +2104,98 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
                                  sl[0].q, sl[0].w, sl[0].x_out, sl[0].xhat, sl[0].h, pog,
                                  (long long)iteration, (long long*)bad_iter));
         PT_CHECK_LAUNCH();
+        return PT_OK;
+    }
+    // z-slabs (several local slabs and / or ranks) keep two iterations per HBM
+    // pass: before each pass every slab receives the two boundary planes of
+    // P_k and P_{k-1} of its neighbours (and of v, once per call) into its
+    // 2-plane ghost buffers, which the column pass reads for planes -2, -1 and
+    // Zl, Zl + 1 -- one exchange of 2-plane halos per two iterations instead of
+    // one per iteration.  Every slab must hold >= 2 planes (decided from the
+    // global plane count so that all ranks agree).
+    const int ranks = (halo && halo->world > 1) ? halo->world : 1;
+    bool col_slabs = tma && pq && pair_env >= 5 && inner >= 2 && Zg / (ranks * G) >= 2;
+    for (int g = 0; g < G; ++g) col_slabs = col_slabs && sl[g].Zl >= 2;
+    if (col_slabs) {
+        int rc = PT_OK;
+        for (int g = 0; g < G; ++g) {  // the volume's own boundary: zero ghosts
+            if (sl[g].z0 == 0)
+                PT_CHECK_CUDA(cudaMemsetAsync(fgp3d_ghost(sl[g].work, 0, sl[g].Zl, H, W), 0,
+                                              14 * (size_t)H * W * 4, st));
+            if (sl[g].z0 + sl[g].Zl == Zg)
+                PT_CHECK_CUDA(cudaMemsetAsync(fgp3d_ghost(sl[g].work, 1, sl[g].Zl, H, W), 0,
+                                              14 * (size_t)H * W * 4, st));
+        }
+        int sp = 0, sk = 0;  // sets of P_{k-1}, P_k (P_{-1} = P_0 with beta_r = 0)
+        int kk = 0;
+        for (; kk + 2 <= inner; kk += 2) {
+            rc = fgp3d_ghost_exchange(sl, G, H, W, sk, sp, kk == 0, halo, st);
+            if (rc) return rc;
+            const int o1 = (sk == 2 || sk == 3) ? 0 : 2;
+            for (int g = 0; g < G; ++g) {
+                const int Zl = sl[g].Zl;
+                Fgp3Args a;
+                a.Zl = Zl; a.H = H; a.W = W; a.z0 = sl[g].z0; a.Zg = Zg;
+                a.v = sl[g].v;
+                a.vtop = nullptr;
+                a.P = fgp3d_set(sl[g].work, sp, Zl, H, W);
+                a.R = fgp3d_set(sl[g].work, sk, Zl, H, W);
+                a.Pn = fgp3d_set(sl[g].work, o1, Zl, H, W);
+                a.Rn = fgp3d_set(sl[g].work, o1 + 1, Zl, H, W);
+                a.lam = (float)lam;
+                a.eta = (float)(1.0 / (12.0 * lam));
+                a.beta = (float)betas[kk];
+                a.beta_r = kk == 0 ? 0.f : (float)betas[kk - 1];
+                a.nonneg = nonneg;
+                a.ghost = fgp3d_ghost(sl[g].work, 0, Zl, H, W);
+                rc = fgp3d_col_launch<16, 16, 3>(a, sm_count, st);
+                if (rc) return rc;
+            }
+            sp = o1;
+            sk = o1 + 1;
+        }
+        if (kk < inner) {  // odd count: one more single iteration (one-plane set ghosts)
+            rc = fgp3d_exchange(sl, G, H, W, sk, true, halo, st);
+            if (!rc) rc = fgp3d_exchange(sl, G, H, W, sp, false, halo, st);
+            if (rc) return rc;
+            const int o = (sk == 2 || sk == 3) ? 0 : 2;
+            for (int g = 0; g < G; ++g) {
+                const int Zl = sl[g].Zl;
+                Fgp3Args a;
+                a.Zl = Zl; a.H = H; a.W = W; a.z0 = sl[g].z0; a.Zg = Zg;
+                a.v = sl[g].v;
+                a.vtop = fgp3d_vtop(sl[g].work, Zl, H, W);
+                a.P = fgp3d_set(sl[g].work, sp, Zl, H, W);
+                a.R = fgp3d_set(sl[g].work, sk, Zl, H, W);
+                a.Pn = fgp3d_set(sl[g].work, o, Zl, H, W);
+                a.Rn = nullptr;
+                a.lam = (float)lam;
+                a.eta = (float)(1.0 / (12.0 * lam));
+                a.beta = (float)betas[kk];
+                a.beta_r = kk == 0 ? 0.f : (float)betas[kk - 1];
+                a.nonneg = nonneg;
+                rc = fgp3d_launch<64, 8, 3, true, true>(a, sm_count, st);
+                if (rc) return rc;
+            }
+            sk = o;
+        }
+        rc = fgp3d_exchange(sl, G, H, W, sk, false, halo, st);  // P ghost below for D^T
+        if (rc) return rc;
+        for (int g = 0; g < G; ++g) {
+            const int Zl = sl[g].Zl;
+            Fgp3Args a;
+            a.Zl = Zl; a.H = H; a.W = W; a.z0 = sl[g].z0; a.Zg = Zg;
+            a.v = sl[g].v;
+            a.P = fgp3d_set(sl[g].work, sk, Zl, H, W);
+            a.lam = (float)lam;
+            a.nonneg = nonneg;
+            const size_t n = (size_t)Zl * H * W;
+            const int blocks = (int)std::min<size_t>((n + 255) / 256, (size_t)sm_count * 16);
+            PT_CHECK_CUDA(launch_pdl(fgp3d_final_kernel, dim3(blocks), dim3(256), 0, st, a,
+                                     sl[g].p, sl[g].q, sl[g].w, sl[g].x_out, sl[g].xhat, sl[g].h,
+                                     pog, (long long)iteration, (long long*)bad_iter));
+            PT_CHECK_LAUNCH();
+        }
         return PT_OK;
     }
     // R form: sets 0/1 = P, R of even iterations, 2/3 of odd ones.

@@ -330,12 +330,15 @@ def _problem_3d(Z=10, size=32, seed=4):
     return TomoProblem(proj, data, tv=TvProxConfig(alpha=0.05, inner_iterations=12)), proj
 
 
-@pytest.mark.parametrize("slabs", [2, 3, 10])
+@pytest.mark.parametrize("slabs", [2, 3, 5, 10])
 def test_zslab_decomposition_is_bitwise_identical(slabs):
     """3D z-slab data path emulated on one device: every virtual slab sees its
     neighbours only through the ghost planes the halo exchange fills; the
     trajectory must equal the single-volume run bit for bit (the projector is
-    slice-local, the slab FGP recomputes the same values)."""
+    slice-local, the slab FGP recomputes the same values).  Slabs of >= 2
+    planes (2, 3, 5 of 10) run the two-iteration column pass with 2-plane
+    ghosts exchanged once per pass; 1-plane slabs (10) the one-iteration
+    kernel with a halo round per iteration."""
     from paper_2602_09527_b200 import distributed as D
     from paper_2602_09527_b200.solvers import _init_state, _plan_segment
     problem, proj = _problem_3d()
