@@ -174,6 +174,120 @@ def _slab_fgp(v_loc, z0, Zg, lam, inner, nonneg, rank, world):
     return np.maximum(x, 0.0) if nonneg else x
 
 
+def _slab_fgp_pass2(v_loc, z0, Zg, lam, inner, nonneg, rank, world):
+    """The native two-iteration column pass on z-slabs (csrc/fgp.cu,
+    fgp3d_ghost_exchange): before each pass of two iterations a slab receives
+    the two boundary planes of P_k and P_{k-1} of its neighbours (and of v
+    once), computes P_{k+1} on its planes and one plane into each ghost
+    region, then P_{k+2} on its own planes; an odd last iteration uses the
+    one-plane protocol.  Restated in float64 numpy over gloo."""
+    import torch
+    zl, H, W = v_loc.shape
+    G = 2  # ghost planes per side; extended plane index e = z + G
+
+    def exchange2(A):
+        """A: [zl + 2G, ...]; ghosts <- the neighbours' two boundary planes"""
+        reqs, lo, hi = [], None, None
+        if rank > 0:
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(A[G:2 * G])), rank - 1))
+            lo = torch.empty(A[:G].shape, dtype=torch.float64)
+            reqs.append(dist.irecv(lo, rank - 1))
+        if rank + 1 < world:
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(A[zl:zl + G])), rank + 1))
+            hi = torch.empty(A[:G].shape, dtype=torch.float64)
+            reqs.append(dist.irecv(hi, rank + 1))
+        for r in reqs:
+            r.wait()
+        if lo is not None:
+            A[:G] = lo.numpy()
+        if hi is not None:
+            A[zl + G:] = hi.numpy()
+
+    def inside(z):
+        return 0 <= z0 + z < Zg
+
+    def u_plane(R, V, z):  # u at local plane z (global guards), extended arrays
+        if not inside(z):
+            return np.zeros((H, W))
+        e, zg = z + G, z0 + z
+        p, q, w = R[e, 0], R[e, 1], R[e, 2]
+        x = np.zeros((H, W))
+        x[:-1] -= p[:-1]
+        x[1:] += p[:-1]
+        x[:, :-1] -= q[:, :-1]
+        x[:, 1:] += q[:, :-1]
+        if zg < Zg - 1:
+            x -= w
+        if zg > 0:
+            x += R[e - 1, 2]
+        u = V[e] - lam * x
+        return np.maximum(u, 0.0) if nonneg else u
+
+    def step(P, Q, beta_r, V, lo, hi):
+        """one FGP iteration on local planes [lo, hi): P_{k+1}"""
+        R = P + beta_r * (P - Q)
+        eta = 1.0 / (12.0 * lam)
+        Pn = np.zeros_like(P)
+        U = {z: u_plane(R, V, z) for z in range(lo, hi + 1)}
+        for z in range(lo, hi):
+            if not inside(z):
+                continue
+            u = U[z]
+            gv = np.zeros((H, W)); gv[:-1] = u[1:] - u[:-1]
+            gh = np.zeros((H, W)); gh[:, :-1] = u[:, 1:] - u[:, :-1]
+            gz = (U[z + 1] - u) if z0 + z < Zg - 1 else np.zeros((H, W))
+            e = z + G
+            ph = R[e, 0] + eta * gv
+            qh = R[e, 1] + eta * gh
+            wh = R[e, 2] + eta * gz
+            nrm = np.maximum(1.0, np.sqrt(ph * ph + qh * qh + wh * wh))
+            Pn[e] = np.stack([ph / nrm, qh / nrm, wh / nrm])
+        return Pn
+
+    V = np.zeros((zl + 2 * G, H, W))
+    V[G:G + zl] = v_loc
+    exchange2(V)
+    P = np.zeros((zl + 2 * G, 3, H, W))
+    Q = P.copy()
+    t, betas = 1.0, []
+    for _ in range(inner):
+        tn = (1.0 + np.sqrt(1.0 + 4.0 * t * t)) / 2.0
+        betas.append((t - 1.0) / tn)
+        t = tn
+    k = 0
+    while k + 2 <= inner:
+        exchange2(P)
+        exchange2(Q)
+        br = 0.0 if k == 0 else betas[k - 1]
+        P1 = step(P, Q, br, V, -1, zl + 1)   # own planes and one into each ghost region
+        P2 = step(P1, P, betas[k], V, 0, zl)
+        Q, P = P1, P2
+        k += 2
+    if k < inner:
+        exchange2(P)
+        exchange2(Q)
+        br = 0.0 if k == 0 else betas[k - 1]
+        Q, P = P, step(P, Q, br, V, 0, zl)
+    exchange2(P)
+    R = P
+    x = []
+    for z in range(zl):
+        e, zg = z + G, z0 + z
+        p, q, w = R[e, 0], R[e, 1], R[e, 2]
+        d = np.zeros((H, W))
+        d[:-1] -= p[:-1]
+        d[1:] += p[:-1]
+        d[:, :-1] -= q[:, :-1]
+        d[:, 1:] += q[:, :-1]
+        if zg < Zg - 1:
+            d -= w
+        if zg > 0:
+            d += R[e - 1, 2]
+        x.append(v_loc[z] - lam * d)
+    x = np.stack(x)
+    return np.maximum(x, 0.0) if nonneg else x
+
+
 def _zworker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -210,6 +324,14 @@ def _zworker(rank, world, port, q):
             xt = gather_zslabs(torch.from_numpy(xs), Z).numpy()
             xo, _ = O.tv_prox(v, 1.0, 0.3, 12, nn)
             out[f"fgp_err_{int(nn)}"] = float(np.abs(xt - xo).max())
+        # (5) the two-iteration pass protocol (2-plane ghosts once per pass),
+        # even and odd iteration counts
+        if min(b - a for a, b in spans) >= 2:
+            for inner in (12, 7):
+                xs = _slab_fgp_pass2(v[z0:z1], z0, Z, 0.3, inner, True, rank, world)
+                xt = gather_zslabs(torch.from_numpy(xs), Z).numpy()
+                xo, _ = O.tv_prox(v, 1.0, 0.3, inner, True)
+                out[f"pass2_err_{inner}"] = float(np.abs(xt - xo).max())
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -231,6 +353,9 @@ def test_zslab_logic_and_halo_protocol_over_gloo(world):
         res = results[r]
         assert res["tiles"] and res["slab_ok"] and res["gather_ok"], res
         assert res["fgp_err_0"] <= 1e-12 and res["fgp_err_1"] <= 1e-12, res
+        for inner in (12, 7):
+            if f"pass2_err_{inner}" in res:
+                assert res[f"pass2_err_{inner}"] <= 1e-12, res
 
 
 # ---------------------------------------------------------------------------
@@ -378,3 +503,6 @@ def test_rows_logic_and_protocols_over_gloo(world):
         assert res["tiles"] and res["slab_ok"] and res["gather_ok"] and res["adj_rows"], res
         assert res["fwd_err"] <= 1e-13, res
         assert res["fgp_err_0"] <= 1e-12 and res["fgp_err_1"] <= 1e-12, res
+        for inner in (12, 7):
+            if f"pass2_err_{inner}" in res:
+                assert res[f"pass2_err_{inner}"] <= 1e-12, res
