@@ -430,14 +430,16 @@ int64_t fgp_workspace_floats(const pt_plan* plan)
     return 8 * (int64_t)plan->H * plan->W;
 }
 
-// 64 x 64 regions (T up to 8) unless the image is tiny, then 32 x 32 (T = 3)
-// (PT_FGP_BIG_MIN: the smallest min(H, W) that uses 64 x 64 regions).
-// FGP-100 measured: 128^2 153 vs 170 us, 256^2 157 us with 64 x 64 regions.
+// 64 x 64 regions (T up to 8) from 256 x 256 images up, 32 x 32 regions with
+// T = 10 below (PT_FGP_BIG_MIN: the smallest min(H, W) that uses 64 x 64
+// regions; PT_FGP_T_SMALL: T of the 32 x 32 regions).  A 128^2 image is
+// latency bound: 32 x 32 regions with a 10-ring halo give 121 CTAs per launch
+// (64 x 64 regions: 9) and five launches per FGP-50: 82 -> 50 us.
 static bool fgp2d_big(int H, int W)
 {
     static const int big_min = [] {
         const char* e = getenv("PT_FGP_BIG_MIN");
-        return e ? atoi(e) : 64;
+        return e ? atoi(e) : 256;
     }();
     return std::min(H, W) >= big_min;
 }
@@ -675,7 +677,7 @@ int fgp2d_rows_run(const Fgp2Slab* sl, int G, int H, int W, double lam, int inne
                                            bad_iter, halo,
                                            std::min(fgp2d_tmax(H, W), kRowGhost - 1), st);
     return fgp2d_rows_run_t<32, 32, 8>(sl, G, H, W, lam, inner, nonneg, pog, iteration, bad_iter,
-                                       halo, 3, st);
+                                       halo, 3, st);  // rows: T <= kRowGhost - 1
 }
 
 // ---------------------------------------------------------------------------
@@ -2285,8 +2287,12 @@ int launch_tv_prox(pt_plan* plan, const float* v, double lam, int inner, int non
         return run_fgp2d<64, 64, 8>(plan, v, lam, inner, nonneg, p, q, x_out, xhat, h,
                                     p_over_gamma, iteration, bad_iter, work, st,
                                     fgp2d_tmax(plan->H, plan->W));
+    static const int t_small = [] {
+        const char* e = getenv("PT_FGP_T_SMALL");
+        return e ? std::max(1, std::min(kFgpMaxT, atoi(e))) : 10;
+    }();
     return run_fgp2d<32, 32, 8>(plan, v, lam, inner, nonneg, p, q, x_out, xhat, h,
-                                p_over_gamma, iteration, bad_iter, work, st, 3);
+                                p_over_gamma, iteration, bad_iter, work, st, t_small);
 }
 
 }  // namespace pt

@@ -166,7 +166,8 @@ import sys, numpy as np, torch
 sys.path.insert(0, {repo!r})
 from paper_2602_09527_b200 import TvProxConfig, tv_prox
 out = []
-for (h, w, inner) in ((2048, 2048, 100), (300, 701, 37), (1000, 130, 13)):
+for (h, w, inner) in ((2048, 2048, 100), (300, 701, 37), (1000, 130, 13), (128, 128, 50),
+                      (77, 200, 23)):
     rng = np.random.default_rng(h + w)
     v = torch.tensor(rng.standard_normal((h, w)).cumsum(axis=0) * 0.05 + 0.2, device="cuda",
                      dtype=torch.float32)
@@ -180,16 +181,18 @@ np.save(sys.argv[1], np.concatenate(out))
 
 def test_fgp_2d_iterations_per_launch_bitwise(tmp_path):
     """Temporal blocking computes only exact points: any number T of inner
-    iterations per launch (halo T rings, T + 1 on the final launch) gives the
-    bits of one iteration per launch (PT_FGP_T = 1)."""
+    iterations per launch (halo T rings, T + 1 on the final launch), in the
+    64 x 64 regions (PT_FGP_T) and in the 32 x 32 regions of small images
+    (PT_FGP_T_SMALL), gives the bits of one iteration per launch."""
     import os
     import subprocess
     import sys
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
-    for t in ("1", "2", "5", "8", "10", "11", "12", ""):
-        path = tmp_path / f"t{t or 'default'}.npy"
-        env = dict(os.environ, PT_FGP_T=t)
+    for t, ts in (("1", "1"), ("2", "3"), ("5", "5"), ("8", "12"), ("10", "7"), ("11", "2"),
+                  ("12", "10"), ("", "")):
+        path = tmp_path / f"t{t or 'default'}_{ts or 'default'}.npy"
+        env = dict(os.environ, PT_FGP_T=t, PT_FGP_T_SMALL=ts)
         subprocess.run([sys.executable, "-c", _T_SNIPPET.format(repo=repo), str(path)],
                        check=True, env=env, timeout=300)
         outs.append(np.load(path))

@@ -82,10 +82,10 @@ for name, (size, A, B, NS) in {"c2": (2048, 1800, 2900, 60), "c1": (512, 720, 76
             y = torch.randn((A, B), device="cuda")
             line += f"  full adj {timed(lambda: plan.adjoint_into(y, img, None), 5):.1f} us"
         print(line, flush=True)
-    if "fgp" in want and name in ("c2", "c1"):
-        cfg = TvProxConfig(alpha=0.02, inner_iterations=100)
+    if "fgp" in want:
+        cfg = TvProxConfig(alpha=0.02, inner_iterations=50 if name == "c0" else 100)
         out, st = tv_prox(x, 1.0, cfg)
-        print(f"{name} fgp100 {timed(lambda: tv_prox(x, 1.0, cfg, warm=st), 10) / 1e3:.3f} ms",
+        print(f"{name} fgp{cfg.inner_iterations} {timed(lambda: tv_prox(x, 1.0, cfg, warm=st), 10) / 1e3:.3f} ms",
               flush=True)
 if "fgp3" in want:
     Z = 256
