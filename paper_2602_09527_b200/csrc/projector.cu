@@ -803,6 +803,10 @@ struct AdjArgs {
     float* out;
     int32_t mode;  // 0 plain adjoint, 1 fused step epilogue
     pt_step_epilogue ep;
+    // plain adjoint split over angle parts (small images, long selections):
+    // grid.z = Z * n_parts, part p sums angle chunks [p cpp, (p+1) cpp) into
+    // out + p * Z * H * W; a combine kernel adds the parts in order
+    int32_t n_parts, chunks_per_part;
 };
 
 // The estimator + ProxSkip step of one pixel (estimators.py:55,92-94,146;
@@ -878,8 +882,18 @@ __device__ __forceinline__ void step_epilogue(const pt_step_epilogue& ep, size_t
 }
 
 template <int TR, int TC, int NT, int NA, bool TWO_TAP, int EPI>
-__global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_kernel(AdjArgs P)
+__global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_kernel(AdjArgs P0)
 {
+    // this CTA's angle part (P0.n_parts == 1: the whole selection)
+    AdjArgs P = P0;
+    const int part = (int)blockIdx.z / P0.Z;
+    if (P0.n_parts > 1) {
+        const int s0 = part * P0.chunks_per_part * NA;
+        P.sel_angle = P0.sel_angle + s0;
+        P.y = P0.y + (size_t)s0 * P0.Z * P0.B;
+        P.n_sel = max(0, min(P0.n_sel - s0, P0.chunks_per_part * NA));
+        P.out = P0.out + (size_t)part * P0.Z * P0.H * P0.W;
+    }
     constexpr int PIX = TR * TC / NT;  // pixels per thread
     constexpr int NEPI = epi_planes(EPI);
     constexpr int ROWSTEP = NT / TC;
@@ -897,7 +911,7 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
     const int rg = tid / TC;
     const int r0 = blockIdx.y * TR;
     const int c0 = blockIdx.x * TC;
-    const int z = blockIdx.z;
+    const int z = (int)blockIdx.z - part * P0.Z;
     const size_t plane = (size_t)P.H * P.W;
     const uint32_t stage_u32 = smem_u32(smem);
     const uint32_t epi_u32 = stage_u32 + (uint32_t)(P.nbuf * NA * P.slot) * 4u;
@@ -1187,7 +1201,7 @@ static int run_gather_e(pt_plan* plan, const AdjArgs& a, cudaStream_t st)
         const int rc = ensure_smem((const void*)adj_gather_kernel<TR, TC, kNT, kNA, TWO, EPI>, smem);
         if (rc) return rc;
     }
-    dim3 grid((plan->W + TC - 1) / TC, (plan->H + TR - 1) / TR, plan->Z);
+    dim3 grid((plan->W + TC - 1) / TC, (plan->H + TR - 1) / TR, plan->Z * a.n_parts);
     PT_CHECK_CUDA(launch_pdl(adj_gather_kernel<TR, TC, kNT, kNA, TWO, EPI>, grid, dim3(kNT), smem,
                              st, a));
     PT_CHECK_LAUNCH();
@@ -1220,6 +1234,23 @@ static int run_gather(pt_plan* plan, const AdjArgs& a, cudaStream_t st)
     }
 }
 
+// out = alpha * (part_0 + part_1 + ...) (+ out): the angle parts of a split
+// adjoint, summed in part order (deterministic)
+__global__ void combine_parts_kernel(const float* parts, int n_parts, size_t n, float* out,
+                                     float alpha, int accumulate)
+{
+    pdl_wait();
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        float s = parts[i];
+        for (int p = 1; p < n_parts; ++p) s += parts[(size_t)p * n + i];
+        float v = alpha * s;
+        if (accumulate) v += out[i];
+        out[i] = v;
+    }
+    pdl_trigger();
+}
+
 int launch_adjoint(pt_plan* plan, const pt_selection* sel, const float* y, float* x_out,
                    float alpha, int accumulate, const pt_step_epilogue* ep, cudaStream_t st,
                    Workspace* ws, int cat)
@@ -1247,8 +1278,40 @@ int launch_adjoint(pt_plan* plan, const pt_selection* sel, const float* y, float
         memset(&a.ep, 0, sizeof(a.ep));
         a.n_epi = 0;
     }
-    if (plan->cand_half == 1) return run_gather<true>(plan, a, st);
-    return run_gather<false>(plan, a, st);
+    // A long plain adjoint on an image too small to fill the GPU (config 0's
+    // snapshot: 32 tiles x 180 angles) splits its angle chunks over CTAs; the
+    // parts land in the workspace's band-partial buffer (free between a
+    // forward's reduction and the next forward) and are summed in part order.
+    a.n_parts = 1;
+    a.chunks_per_part = 0;
+    const int n_chunks = (sel->n + kNA - 1) / kNA;
+    const int tr = kGatherTiles[plan->gather_tile][0], tc = kGatherTiles[plan->gather_tile][1];
+    const long long tiles = (long long)((plan->W + tc - 1) / tc) * ((plan->H + tr - 1) / tr) * plan->Z;
+    const size_t npx = (size_t)plan->Z * plan->H * plan->W;
+    static const bool split_env = [] {
+        const char* e = getenv("PT_GATHER_SPLIT");
+        return !(e && e[0] == '0');
+    }();
+    if (!ep && split_env && ws && n_chunks >= 2 && tiles < plan->sm_count) {
+        int parts = (int)std::min<long long>(n_chunks, (2LL * plan->sm_count + tiles - 1) / tiles);
+        while (parts > 1 && (size_t)parts * npx > ws->partial_floats) --parts;
+        if (parts > 1) {
+            a.chunks_per_part = (n_chunks + parts - 1) / parts;
+            a.n_parts = (n_chunks + a.chunks_per_part - 1) / a.chunks_per_part;
+            a.nbuf = a.chunks_per_part > 1 ? 2 : 1;
+            a.out = ws->partial;
+            a.alpha = 1.f;
+            a.accumulate = 0;
+        }
+    }
+    const int rc = (plan->cand_half == 1) ? run_gather<true>(plan, a, st)
+                                          : run_gather<false>(plan, a, st);
+    if (rc || a.n_parts == 1) return rc;
+    const int blocks = (int)std::min<size_t>((npx + 255) / 256, (size_t)plan->sm_count * 8);
+    PT_CHECK_CUDA(launch_pdl(combine_parts_kernel, dim3(blocks), dim3(256), 0, st,
+                             (const float*)ws->partial, a.n_parts, npx, x_out, alpha, accumulate));
+    PT_CHECK_LAUNCH();
+    return PT_OK;
 }
 
 int launch_epilogue(pt_plan* plan, const float* g, const pt_step_epilogue* ep, cudaStream_t st)
