@@ -241,6 +241,14 @@ int pt_session_init(pt_session* s, void* stream);
 int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
                    const uint8_t* host_theta, const uint8_t* host_refresh, int64_t k0,
                    void* stream);
+/* The same for a whole run planned on the host: after step host_marks[m]
+ * (cumulative, ascending) the cudaEvent_t events[m] is recorded on `stream`
+ * (the log rows' device times, solvers.py:304-322), so a run whose rows need
+ * no metric is one call.  No host sync. */
+int pt_session_run_marked(pt_session* s, int32_t n_steps, const int32_t* host_subset,
+                          const uint8_t* host_theta, const uint8_t* host_refresh, int64_t k0,
+                          int32_t n_marks, const int32_t* host_marks, void* const* events,
+                          void* stream);
 /* Device pointers of the live state (valid until the next run call). */
 float* pt_session_x(pt_session* s);
 float* pt_session_h(pt_session* s);

@@ -83,6 +83,10 @@ _SIGS = {
     "pt_session_run": (ctypes.c_int, [c_vp, c_i32, ctypes.POINTER(c_i32),
                                       ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(ctypes.c_uint8),
                                       c_i64, c_vp]),
+    "pt_session_run_marked": (ctypes.c_int, [c_vp, c_i32, ctypes.POINTER(c_i32),
+                                             ctypes.POINTER(ctypes.c_uint8),
+                                             ctypes.POINTER(ctypes.c_uint8), c_i64, c_i32,
+                                             ctypes.POINTER(c_i32), ctypes.POINTER(c_vp), c_vp]),
     "pt_session_x": (c_vp, [c_vp]),
     "pt_session_h": (c_vp, [c_vp]),
     "pt_session_buffer": (c_vp, [c_vp, c_i32]),

@@ -786,6 +786,35 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
     return PT_OK;
 }
 
+int pt_session_run_marked(pt_session* s, int32_t n_steps, const int32_t* host_subset,
+                          const uint8_t* host_theta, const uint8_t* host_refresh, int64_t k0,
+                          int32_t n_marks, const int32_t* host_marks, void* const* events,
+                          void* stream)
+{
+    if (!s || n_steps < 0 || n_marks < 0 || (n_marks && (!host_marks || !events))) {
+        pt::set_error("bad argument");
+        return PT_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    int32_t done = 0;
+    for (int32_t m = 0; m < n_marks; ++m) {
+        const int32_t upto = host_marks[m];
+        if (upto < done || upto > n_steps) { pt::set_error("marks must ascend within the steps"); return PT_EINVAL; }
+        const int rc = pt_session_run(s, upto - done, host_subset ? host_subset + done : nullptr,
+                                      host_theta ? host_theta + done : nullptr,
+                                      host_refresh ? host_refresh + done : nullptr, k0 + done,
+                                      stream);
+        if (rc) return rc;
+        PT_CHECK_CUDA(cudaEventRecord((cudaEvent_t)events[m], st));
+        done = upto;
+    }
+    if (done < n_steps)
+        return pt_session_run(s, n_steps - done, host_subset ? host_subset + done : nullptr,
+                              host_theta ? host_theta + done : nullptr,
+                              host_refresh ? host_refresh + done : nullptr, k0 + done, stream);
+    return PT_OK;
+}
+
 int pt_session_set_profiling(pt_session* s, int32_t on)
 {
     if (!s) { pt::set_error("null session"); return PT_EINVAL; }

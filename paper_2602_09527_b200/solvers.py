@@ -175,6 +175,22 @@ class _Session:
             r.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), int(k0),
             N.stream_handle(self.stream)), "run")
 
+    def run_marked(self, subs, thetas, refresh, k0: int, marks, events):
+        """Enqueue all steps in one native call; events[m] is recorded on the
+        session stream after step marks[m] (cumulative step counts)."""
+        n = len(subs)
+        s = np.ascontiguousarray(subs, dtype=np.int32)
+        t = np.ascontiguousarray(thetas, dtype=np.uint8)
+        r = np.ascontiguousarray(refresh, dtype=np.uint8)
+        mk = np.ascontiguousarray(marks, dtype=np.int32)
+        ev = (ctypes.c_void_p * len(events))(*[int(e.cuda_event) for e in events])
+        N.check(N.lib().pt_session_run_marked(
+            self.handle, n, s.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+            t.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
+            r.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), int(k0), len(mk),
+            mk.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), ev,
+            N.stream_handle(self.stream)), "run")
+
     def view(self, address) -> torch.Tensor:
         return N.device_view(address, self.shape)
 
@@ -539,6 +555,44 @@ def _run_loop(state: IterateState, config, problem, reference, ground_truth,
         return record
     last_floor = math.floor(state.data_passes + 1e-12)
     budget = config.time_budget
+    if not need_metrics and budget is None:
+        # Nothing needs a value before the end: plan every segment on the host
+        # (the draws are data independent), then enqueue the whole run in one
+        # native call that records an event at each log row.
+        parts, marks = [], []
+        n_total = 0
+        while True:
+            subs, thetas, refr, passes, exhausted = _plan_segment(state, config, last_floor)
+            parts.append((subs, thetas, refr))
+            n_total += len(subs)
+            state.prox_calls += int(np.count_nonzero(thetas))
+            state.data_passes = passes
+            marks.append(n_total)
+            last_floor = math.floor(state.data_passes + 1e-12)
+            record.rows.append((state.data_passes, None, None, None, None, state.prox_calls,
+                                None))
+            record.iterations.append(state.k + n_total)
+            if exhausted:
+                break
+        row_events = [torch.cuda.Event(enable_timing=True) for _ in marks]
+        for ev in row_events:
+            ev.record(stream)  # materialise the handles; the native call re-records them
+        state.session.run_marked(np.concatenate([p[0] for p in parts]),
+                                 np.concatenate([p[1] for p in parts]),
+                                 np.concatenate([p[2] for p in parts]), state.k, marks,
+                                 row_events)
+        state.k += n_total
+        stream.synchronize()
+        for ri, ev in enumerate(row_events, start=1):
+            r = record.rows[ri]
+            record.rows[ri] = (r[0], events[0].elapsed_time(ev) / 1e3) + tuple(r[2:])
+        state.work_seconds = record.rows[-1][1]
+        bad = _bad_iteration(state)
+        if bad is not None:
+            raise _diverged(bad, config, record)
+        record.image = state.full_x().clone()
+        record.state = state
+        return record
     while True:
         subs, thetas, refr, passes, exhausted = _plan_segment(
             state, config, last_floor, max_steps=1 if budget is not None else None)
