@@ -258,7 +258,8 @@ def test_config1_whole_run_matches_reference(oracle):
     """BASELINE config 1 whole: 512^2, 720x768, SAGA N=20 (20x512^2 table),
     p=0.05, FGP 100, 100 epochs = 2000 iterations, against the reference's
     own run (tests/golden/reference_c1.npz; b regenerated with the pinned
-    oracle)."""
+    oracle): final image, row schedule, prox calls and the objective of
+    every row."""
     import os
     from conftest import GOLDEN
     from test_oracle import config1_problem
@@ -270,11 +271,13 @@ def test_config1_whole_run_matches_reference(oracle):
     scfg = SolverConfig(gamma=float(c1["c1_gamma"]), skip_probability=cfg.p,
                         n_subsets=cfg.n_subsets, estimator=cfg.estimator,
                         max_data_passes=cfg.max_data_passes, seed=cfg.solver_seed)
-    rec = run(scfg, problem)
+    rec = run(scfg, problem, record_objective="c1_obj" in c1.files)
     assert rel_l2(cpu(rec.image), c1["c1_image"]) <= TOL
     assert np.array_equal(rec.column("data_passes"), c1["c1_passes"])
     assert np.array_equal(rec.column("prox_calls"), c1["c1_prox"])
     assert rec.iterations == list(c1["c1_iters"])
+    if "c1_obj" in c1.files:  # the objective at each of the 101 rows
+        assert np.allclose(rec.column("objective"), c1["c1_obj"], rtol=TOL)
     assert proj.norm_sq(50, 0) == pytest.approx(float(c1["c1_L"]), rel=1e-5)
 
 
