@@ -446,17 +446,18 @@ static bool fgp2d_big(int H, int W)
 
 // inner iterations per launch of the 64 x 64 regions (PT_FGP_T overrides).
 // The result does not depend on T (exact points only), the time does, through
-// launches x ragged last regions x waves; measured FGP-100: 512^2 T = 6/7/8:
-// 175/162/200 us; 1024^2: 412/390/376 us; 2048^2: 1.19/1.065/1.056 ms.
+// launches x ragged last regions x waves; FGP-100 with the T-ring halo:
+// 2048^2 T = 8 0.996 ms (T = 5 / 6 / 7 / 9..12: 1.01-1.19 ms), 512^2 T = 8
+// 156 us (T = 5 / 6 / 7: 188 / 174 / 166 us).
 static int fgp2d_tmax(int H, int W)
 {
     static const int env = [] {
         const char* e = getenv("PT_FGP_T");
         return e ? std::max(1, std::min(kFgpMaxT, atoi(e))) : 0;
     }();
-    if (env) return env;
-    const int m = std::min(H, W);
-    return (m >= 384 && m < 768) ? 7 : 8;
+    (void)H;
+    (void)W;
+    return env ? env : 8;
 }
 
 template <int RW, int RH, int STRIP>
