@@ -1634,11 +1634,11 @@ static int fgp3d_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
 // the one-iteration kernel's expression in its operation order, so the pass
 // is bitwise equal to two fgp3d_iter_kernel launches.
 // ---------------------------------------------------------------------------
-template <int BX2, int BY>
+template <int BX2, int BY, int NS_ = 3>
 struct Fgp3Col {
     static constexpr int NT = BX2 * BY;
     static constexpr int BXP = 2 * BX2;       // tile width in points
-    static constexpr int NS = 3;              // TMA ring stages (planes)
+    static constexpr int NS = NS_;            // TMA ring stages (planes)
     static constexpr int BW = BXP + 4;        // staged box width (origin two points left)
     static constexpr int PL = BW * BY;        // one staged array plane (floats)
     static constexpr int STAGE = 7 * PL;      // P_k (3), P_{k-1} (3), v
@@ -1662,11 +1662,11 @@ __device__ __forceinline__ f2 sel2(bool ca, bool cb, f2 x, f2 y)
     return pk(ca ? xa : ya, cb ? xb : yb);
 }
 
-template <int BX2, int BY, int MINB>
+template <int BX2, int BY, int MINB, int NS = 3>
 __global__ void __launch_bounds__(BX2 * BY, MINB)
     fgp3d_col_kernel(Fgp3Args a, const __grid_constant__ Fgp3Maps m)
 {
-    using T = Fgp3Col<BX2, BY>;
+    using T = Fgp3Col<BX2, BY, NS>;
     constexpr int NT = T::NT, XPL = T::XPL;
     extern __shared__ __align__(128) float fsm[];
     __shared__ __align__(8) uint64_t mbar[T::NS];
@@ -1898,18 +1898,18 @@ __global__ void __launch_bounds__(BX2 * BY, MINB)
     pdl_trigger();
 }
 
-template <int BX2, int BY, int MINB>
+template <int BX2, int BY, int MINB, int NS = 3>
 static int fgp3d_col_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
 {
-    using T = Fgp3Col<BX2, BY>;
+    using T = Fgp3Col<BX2, BY, NS>;
     const size_t smem = (size_t)T::SMEM_FLOATS * 4;
     {
-        const int rc = ensure_smem((const void*)fgp3d_col_kernel<BX2, BY, MINB>, smem);
+        const int rc = ensure_smem((const void*)fgp3d_col_kernel<BX2, BY, MINB, NS>, smem);
         if (rc) return rc;
     }
     int per_sm = 0;
     PT_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, fgp3d_col_kernel<BX2, BY, MINB>, T::NT, smem));
+        &per_sm, fgp3d_col_kernel<BX2, BY, MINB, NS>, T::NT, smem));
     Fgp3Maps m;
     memset(&m, 0, sizeof(m));
     const cuuint64_t W = a.W, H = a.H;
@@ -1953,7 +1953,7 @@ static int fgp3d_col_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
     a.zchunk = zc;
     const dim3 grid((a.W + T::CX - 1) / T::CX, (a.H + T::CY - 1) / T::CY,
                     (a.Zl + a.zchunk - 1) / a.zchunk);
-    PT_CHECK_CUDA(launch_pdl(fgp3d_col_kernel<BX2, BY, MINB>, grid, dim3(T::NT), smem, st, a, m));
+    PT_CHECK_CUDA(launch_pdl(fgp3d_col_kernel<BX2, BY, MINB, NS>, grid, dim3(T::NT), smem, st, a, m));
     PT_CHECK_LAUNCH();
     return PT_OK;
 }
