@@ -556,14 +556,33 @@ def _run_loop(state: IterateState, config, problem, reference, ground_truth,
     last_floor = math.floor(state.data_passes + 1e-12)
     budget = config.time_budget
     if not need_metrics and budget is None:
-        # Nothing needs a value before the end: plan every segment on the host
-        # (the draws are data independent), then enqueue the whole run in one
-        # native call that records an event at each log row.
-        parts, marks = [], []
-        n_total = 0
+        # Nothing needs a value before the end: the draws are data independent,
+        # so segments are planned on the host and enqueued in batches of 1, 2,
+        # 4, ... segments (one native call each, an event recorded at each log
+        # row): the device starts after the first segment is planned and the
+        # rest is planned while it runs.
+        row_events = []
+        pending, marks = [], []
+        n_total = n_sent = 0
+        batch = 1
+
+        def flush():
+            nonlocal pending, marks, n_sent, batch
+            evs = [torch.cuda.Event(enable_timing=True) for _ in marks]
+            for ev in evs:
+                ev.record(stream)  # materialise the handles; the native call re-records them
+            state.session.run_marked(np.concatenate([p[0] for p in pending]),
+                                     np.concatenate([p[1] for p in pending]),
+                                     np.concatenate([p[2] for p in pending]),
+                                     state.k + n_sent, [m - n_sent for m in marks], evs)
+            row_events.extend(evs)
+            n_sent = n_total
+            pending, marks = [], []
+            batch *= 2
+
         while True:
             subs, thetas, refr, passes, exhausted = _plan_segment(state, config, last_floor)
-            parts.append((subs, thetas, refr))
+            pending.append((subs, thetas, refr))
             n_total += len(subs)
             state.prox_calls += int(np.count_nonzero(thetas))
             state.data_passes = passes
@@ -572,15 +591,10 @@ def _run_loop(state: IterateState, config, problem, reference, ground_truth,
             record.rows.append((state.data_passes, None, None, None, None, state.prox_calls,
                                 None))
             record.iterations.append(state.k + n_total)
+            if exhausted or len(pending) >= batch:
+                flush()
             if exhausted:
                 break
-        row_events = [torch.cuda.Event(enable_timing=True) for _ in marks]
-        for ev in row_events:
-            ev.record(stream)  # materialise the handles; the native call re-records them
-        state.session.run_marked(np.concatenate([p[0] for p in parts]),
-                                 np.concatenate([p[1] for p in parts]),
-                                 np.concatenate([p[2] for p in parts]), state.k, marks,
-                                 row_events)
         state.k += n_total
         stream.synchronize()
         for ri, ev in enumerate(row_events, start=1):

@@ -52,6 +52,8 @@ def once(mode):
         e0.record(stream)
         st.session.run_marked(subs, th, rf, 0, marks, evs)
     elif mode == "end":
+        e1.record(stream)  # materialise the handle
+        e0.record(stream)
         st.session.run_marked(subs, th, rf, 0, [marks[-1]], [e1])
     else:
         st.session.run(subs, th, rf, 0)
