@@ -631,9 +631,9 @@ static int fgp2d_rows_run_t(const Fgp2Slab* sl, int G, int H, int W, double lam,
             for (int k = 0; k < kFgpMaxT; ++k) a.beta[k] = (k < iters) ? (float)betas[done + k] : 0.f;
             a.n_iter = iters;
             // T iterations make T rings of the region inexact (each iteration's
-        // stencil reaches one point in every direction); the final launch's
-        // x = v - lam D^T(p, q) needs one ring more
-        a.halo = fin ? iters + 1 : iters;
+            // stencil reaches one point in every direction); the final launch's
+            // x = v - lam D^T(p, q) needs one ring more
+            a.halo = fin ? iters + 1 : iters;
             a.nonneg = nonneg;
             a.final_ = fin ? 1 : 0;
             a.x_out = sl[g].x_out;
