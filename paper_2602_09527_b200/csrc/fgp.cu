@@ -980,48 +980,6 @@ __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
     pdl_trigger();
 }
 
-// ---------------------------------------------------------------------------
-// Two inner iterations per HBM pass (one slab = the whole volume, TMA, PQ form).
-// A pass reads P_{k-1}, P_k (3 components each) and v, and writes P_{k+1} and
-// P_{k+2}: 52 B per voxel per two iterations instead of 80.  The CTA marches
-// its TY x TX column along z with four lagged phases per plane:
-//   A(z)  u_k(z)       on rows -1..TY+1, cols -1..TX+1  (staged P_k, P_{k-1}, v)
-//   B(z)  R_{k+1}(z)   on rows -1..TY,   cols -1..TX    (u_k(z), u_k(z+1)); P_{k+1} out
-//   C(z)  u_{k+1}(z)   on rows  0..TY,   cols  0..TX    (R_{k+1}(z), R_{k+1}(z-1))
-//   D(z)  P_{k+2}(z)   on rows  0..TY-1, cols  0..TX-1  (u_{k+1}(z), u_{k+1}(z+1))
-// (step s runs A(s+2), B(s+1), C(s+1), D(s)).  Every shared-memory window has
-// the staged layout (row pitch TX + 8, origin (-2, -4)), so one offset per
-// point addresses all of them; image-boundary guards are selects, not
-// branches.  Every value is the expression the one-iteration kernel evaluates
-// (R formed as p + beta (p - p_prev), the same D^T order), so both paths give
-// the same bits; the xy halo is recomputed (~25% more math).
-// ---------------------------------------------------------------------------
-template <int TX, int TY, int NT_>
-struct Fgp3Pair {
-    // X2 path: x-adjacent point pairs (even columns) per thread, f32x2 math
-    static constexpr int CP_AB = TX / 2 + 2, CP_C = TX / 2 + 1, CP_D = TX / 2;
-    static constexpr int NPA = (TY + 3) * CP_AB, NPB = (TY + 2) * CP_AB;
-    static constexpr int NPC = (TY + 1) * CP_C, NPD = TY * CP_D;
-    static constexpr int NT = NT_;
-    static constexpr int NS = 3;
-    static constexpr int SW = TX + 8, SR = TY + 4, SA = SR * SW;  // window (all arrays)
-    static constexpr int WIN3 = (3 * SA + 31) & ~31;
-    static constexpr int QOFF = WIN3, VOFF = 2 * WIN3;
-    static constexpr int STAGE = (VOFF + SA + 31) & ~31;
-    static constexpr int NA = (TY + 3) * (TX + 3);  // phase point counts
-    static constexpr int NB = (TY + 2) * (TX + 2);
-    static constexpr int NC = (TY + 1) * (TX + 1);
-    static constexpr int UKO = NS * STAGE;          // u_k      [2][SA]
-    static constexpr int RKO = UKO + 2 * SA;        // R_{k+1}  [2][3][SA]
-    static constexpr int UK1O = RKO + 6 * SA;       // u_{k+1}  [2][SA]
-    static constexpr int SMEM_FLOATS = UK1O + 2 * SA;
-    static constexpr int KA = (NA + NT - 1) / NT, KB = (NB + NT - 1) / NT, KC = (NC + NT - 1) / NT;
-    static constexpr int KD = TX * TY / NT;
-    static constexpr int KA2 = (NPA + NT - 1) / NT, KB2 = (NPB + NT - 1) / NT;
-    static constexpr int KC2 = (NPC + NT - 1) / NT, KD2 = (NPD + NT - 1) / NT;
-    static constexpr uint32_t TMA_BYTES = 7u * SA * 4u;
-};
-
 __device__ __forceinline__ f2 ld2s(const float* p)
 {
     const float2 v = *reinterpret_cast<const float2*>(p);
@@ -1033,397 +991,12 @@ __device__ __forceinline__ void st2s(float* p, f2 v)
     upk(v, w.x, w.y);
     *reinterpret_cast<float2*>(p) = w;
 }
-// the one-point kernels' clamp (nonneg: u < 0 -> 0, NaN kept) per lane
-__device__ __forceinline__ f2 clamp2(f2 u, bool nonneg, bool in)
-{
-    float a, b;
-    upk(u, a, b);
-    if (nonneg) {
-        a = (a < 0.f) ? 0.f : a;
-        b = (b < 0.f) ? 0.f : b;
-    }
-    return in ? pk(a, b) : pk(0.f, 0.f);
-}
 // (n2 > 1 ? rsqrt(n2) : 1) per lane
 __device__ __forceinline__ f2 inv_norm2(f2 n2)
 {
     float a, b;
     upk(n2, a, b);
     return pk((a > 1.f) ? rsqrt_ftz(a) : 1.f, (b > 1.f) ? rsqrt_ftz(b) : 1.f);
-}
-
-// Fgp3Args use: R = P_k set, P = P_{k-1} set, Pn = P_{k+1} set, Rn = P_{k+2}
-// set; beta_r = beta_{k-1} (forms R_k), beta = beta_k (forms R_{k+1}).
-template <int TX, int TY, int NT_, bool X2>
-__global__ void __launch_bounds__(NT_, 2)
-    fgp3d_pair_kernel(Fgp3Args a, const __grid_constant__ Fgp3Maps m)
-{
-    using T = Fgp3Pair<TX, TY, NT_>;
-    constexpr int NT = T::NT, SW = T::SW, SA = T::SA;
-    extern __shared__ __align__(128) float fsm[];
-    __shared__ __align__(8) uint64_t mbar[T::NS];
-    const uint32_t fsm_u32 = (uint32_t)__cvta_generic_to_shared(fsm);
-
-    const int tid = threadIdx.x;
-    const int i0 = blockIdx.y * TY, j0 = blockIdx.x * TX;
-    const int zb = blockIdx.z * a.zchunk;
-    const int ze = min(a.Zl, zb + a.zchunk);
-    const int H = a.H, W = a.W;
-    const size_t HW = (size_t)H * W;
-    if (tid == 0) {
-        for (int k = 0; k < T::NS; ++k)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
-                (uint32_t)__cvta_generic_to_shared(&mbar[k])));
-        asm volatile("fence.mbarrier_init.release.cluster;");
-    }
-    __syncthreads();
-    pdl_wait();  // the dual sets are the predecessor's output
-
-    // plane p (zb - 2 <= p <= ze + 1) lives in stage (p - zb + 2) % 3; planes
-    // outside the volume land as zeros (ghost planes / out-of-bounds boxes)
-    auto issue = [&](int p) {
-        if (tid != 0) return;
-        const int s = (p - zb + 2) % T::NS;
-        const uint32_t sb = fsm_u32 + (uint32_t)(s * T::STAGE) * 4u;
-        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&mbar[s]);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                     "r"(T::TMA_BYTES));
-        asm volatile(
-            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-            " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb),
-            "l"(&m.R), "r"(j0 - 4), "r"(i0 - 2), "r"(0), "r"(p + 1), "r"(bar) : "memory");
-        asm volatile(
-            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-            " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb + (uint32_t)T::QOFF * 4u),
-            "l"(&m.P), "r"(j0 - 4), "r"(i0 - 2), "r"(0), "r"(p + 1), "r"(bar) : "memory");
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-            " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(sb + (uint32_t)T::VOFF * 4u),
-            "l"(&m.V), "r"(j0 - 4), "r"(i0 - 2), "r"(p), "r"(bar) : "memory");
-    };
-    auto landed = [&](int p) {
-        const int u = p - zb + 2;
-        mbar_wait((uint32_t)__cvta_generic_to_shared(&mbar[u % T::NS]),
-                  (uint32_t)((u / T::NS) & 1));
-    };
-
-    // window points of this thread: offset (bits 0-15) and guards (16: i < H-1,
-    // 17: i > 0, 18: j < W-1, 19: j > 0, 20: inside the image); -1 = none
-    auto pack = [&](int r, int c) -> int {
-        const int gi = i0 + r, gj = j0 + c;
-        const bool in = gi >= 0 && gi < H && gj >= 0 && gj < W;
-        return ((r + 2) * SW + (c + 4)) | ((int)(gi < H - 1) << 16) | ((int)(gi > 0) << 17) |
-               ((int)(gj < W - 1) << 18) | ((int)(gj > 0) << 19) | ((int)in << 20);
-    };
-    int ptA[T::KA], ptB[T::KB], ptC[T::KC];
-    int gB[T::KB];  // in-plane HBM offset of a centre-tile B point, else -1
-#pragma unroll
-    for (int k = 0; k < T::KA; ++k) {
-        const int idx = tid + k * NT;
-        ptA[k] = idx < T::NA ? pack(idx / (TX + 3) - 1, idx % (TX + 3) - 1) : -1;
-    }
-#pragma unroll
-    for (int k = 0; k < T::KB; ++k) {
-        const int idx = tid + k * NT;
-        const int r = idx / (TX + 2) - 1, c = idx % (TX + 2) - 1;
-        ptB[k] = idx < T::NB ? pack(r, c) : -1;
-        const bool centre = idx < T::NB && r >= 0 && r < TY && c >= 0 && c < TX &&
-                            i0 + r < H && j0 + c < W;
-        gB[k] = centre ? (i0 + r) * W + (j0 + c) : -1;
-    }
-#pragma unroll
-    for (int k = 0; k < T::KC; ++k) {
-        const int idx = tid + k * NT;
-        ptC[k] = idx < T::NC ? pack(idx / (TX + 1), idx % (TX + 1)) : -1;
-    }
-    // X2: pair descriptors (offset of the even point | 16: i < H-1 | 17: i > 0 |
-    // 20: inside the image | 21: the odd point is column W-1); -1 = none.  W is
-    // even (TMA), so a pair never straddles the image's x edges.
-    auto pack2 = [&](int r, int c) -> int {
-        const int gi = i0 + r, gj = j0 + c;
-        const bool in = gi >= 0 && gi < H && gj >= 0 && gj < W;
-        return ((r + 2) * SW + (c + 4)) | ((int)(gi < H - 1) << 16) | ((int)(gi > 0) << 17) |
-               ((int)in << 20) | ((int)(gj == W - 2) << 21);
-    };
-    int qA[T::KA2], qB[T::KB2], qC[T::KC2], qD[T::KD2], hB[T::KB2], hD[T::KD2];
-    if constexpr (X2) {
-#pragma unroll
-        for (int k = 0; k < T::KA2; ++k) {
-            const int idx = tid + k * NT;
-            qA[k] = idx < T::NPA ? pack2(idx / T::CP_AB - 1, 2 * (idx % T::CP_AB) - 2) : -1;
-        }
-#pragma unroll
-        for (int k = 0; k < T::KB2; ++k) {
-            const int idx = tid + k * NT;
-            const int r = idx / T::CP_AB - 1, c = 2 * (idx % T::CP_AB) - 2;
-            qB[k] = idx < T::NPB ? pack2(r, c) : -1;
-            const bool centre = idx < T::NPB && r >= 0 && r < TY && c >= 0 && c < TX &&
-                                i0 + r < H && j0 + c < W;
-            hB[k] = centre ? (i0 + r) * W + (j0 + c) : -1;
-        }
-#pragma unroll
-        for (int k = 0; k < T::KC2; ++k) {
-            const int idx = tid + k * NT;
-            qC[k] = idx < T::NPC ? pack2(idx / T::CP_C, 2 * (idx % T::CP_C)) : -1;
-        }
-#pragma unroll
-        for (int k = 0; k < T::KD2; ++k) {
-            const int idx = tid + k * NT;
-            const int r = idx / T::CP_D, c = 2 * (idx % T::CP_D);
-            const bool ok = idx < T::NPD && i0 + r < H && j0 + c < W;
-            qD[k] = ok ? pack2(r, c) : -1;
-            hD[k] = ok ? (i0 + r) * W + (j0 + c) : -1;
-        }
-    }
-    const int tx = tid % TX, ty = tid / TX;
-    const float lam = a.lam, eta = a.eta, br = a.beta_r, bk = a.beta;
-    const bool nonneg = a.nonneg != 0;
-    const f2 br2 = pk(br, br), bk2 = pk(bk, bk), eta2 = pk(eta, eta), nlam2 = pk(-lam, -lam);
-    const f2 z2 = pk(0.f, 0.f), nz2 = pk(-0.f, -0.f);
-    // D^T of a pair in the one-point order: x = -a0 [i < H-1]; + a1 [i > 0];
-    // - a2 [j < W-1, the odd point of the last pair skips it: x + (-0) a2];
-    // + a3 (j > 0: at j = 0 a3 is the zero-filled column -1); - a4 [z]; + a5 [z]
-    auto divT2 = [&](int q, f2 a0, f2 a1, f2 a2, f2 a3, f2 a4, f2 a5, bool zhi, bool zlo) -> f2 {
-        f2 x = (q & (1 << 16)) ? sub2(nz2, a0) : z2;
-        if (q & (1 << 17)) x = add2(x, a1);
-        x = fma2(a2, (q & (1 << 21)) ? pk(-1.f, -0.f) : pk(-1.f, -1.f), x);
-        x = add2(x, a3);
-        if (zhi) x = sub2(x, a4);
-        if (zlo) x = add2(x, a5);
-        return x;
-    };
-    const float* sUK = fsm + T::UKO;
-    const float* sRK = fsm + T::RKO;
-    const float* sUK1 = fsm + T::UK1O;
-    // R_k from the staged P_k / P_{k-1} windows (the one-iteration kernel's rv)
-    auto rk = [&](const float* st, int o) -> float {
-        const float pv = st[o];
-        return pv + br * (pv - st[T::QOFF + o]);
-    };
-    // D^T in the reference's _diff_adjoint order (+ z), guards as selects
-    auto divT = [&](int g, float a0, float a1, float a2, float a3, float a4, float a5, bool zhi,
-                    bool zlo) -> float {
-        float x = (g & (1 << 16)) ? -a0 : 0.f;
-        x = (g & (1 << 17)) ? x + a1 : x;
-        x = (g & (1 << 18)) ? x - a2 : x;
-        x = (g & (1 << 19)) ? x + a3 : x;
-        x = zhi ? x - a4 : x;
-        x = zlo ? x + a5 : x;
-        return x;
-    };
-    auto clampu = [&](float u, int g) -> float {
-        if (nonneg) u = (u < 0.f) ? 0.f : u;
-        return (g & (1 << 20)) ? u : 0.f;
-    };
-
-    // prologue: planes zb - 2 .. zb in flight
-    issue(zb - 2);
-    issue(zb - 1);
-    issue(zb);
-    landed(zb - 2);
-    landed(zb - 1);
-    // stage slots of planes s + 1 (c1) and s + 2 (c2) at step s; plane s - 1's is c0
-    int c0 = 2, c1 = 0, c2 = 1;
-    for (int s = zb - 3; s < ze; ++s) {
-        // step s = zb - 3 is the prologue's A(zb - 1) only
-        if (s > zb - 3) {
-            __syncthreads();  // step s - 1 done: the stage of plane s is free
-            if (s + 3 <= ze + 1) issue(s + 3);
-            landed(s + 2);
-        }
-        const int pA = s + 2;
-        {  // A(pA): u_k
-            const int zg = a.z0 + pA;
-            const bool zlo = zg > 0, zhi = zg < a.Zg - 1;
-            const float* st = fsm + c2 * T::STAGE;
-            const float* st1 = fsm + c1 * T::STAGE;
-            float* U = fsm + T::UKO + (pA & 1) * SA;
-            if constexpr (X2) {
-                auto rk2 = [&](const float* sp, int o) -> f2 {
-                    const f2 pv = ld2s(sp + o);
-                    return fma2(sub2(pv, ld2s(sp + T::QOFF + o)), br2, pv);
-                };
-#pragma unroll
-                for (int k = 0; k < T::KA2; ++k) {
-                    const int q = qA[k];
-                    if (q < 0) continue;
-                    const int o = q & 0xffff;
-                    const f2 a2 = rk2(st, SA + o);
-                    const float pm = st[SA + o - 1];
-                    const float rm = fmaf(pm - st[T::QOFF + SA + o - 1], br, pm);
-                    const f2 x = divT2(q, rk2(st, o), rk2(st, o - SW), a2, pk(rm, lo_of(a2)),
-                                       rk2(st, 2 * SA + o), rk2(st1, 2 * SA + o), zhi, zlo);
-                    st2s(U + o, clamp2(fma2(x, nlam2, ld2s(st + T::VOFF + o)), nonneg,
-                                       (q & (1 << 20)) != 0));
-                }
-            } else
-#pragma unroll
-            for (int k = 0; k < T::KA; ++k) {
-                const int pt = ptA[k];
-                if (pt < 0) continue;
-                const int o = pt & 0xffff;
-                const float x = divT(pt, rk(st, o), rk(st, o - SW), rk(st, SA + o),
-                                     rk(st, SA + o - 1), rk(st, 2 * SA + o), rk(st1, 2 * SA + o),
-                                     zhi, zlo);
-                U[o] = clampu(st[T::VOFF + o] - lam * x, pt);
-            }
-        }
-        if (s > zb - 3) {
-            __syncthreads();
-            const int pB = s + 1;
-            {  // B(pB): P_{k+1} -> R_{k+1}; centre P_{k+1} to HBM
-                const int zg = a.z0 + pB;
-                const bool top = zg < a.Zg - 1;
-                const bool own = pB >= zb && pB < ze;
-                const float* st = fsm + c1 * T::STAGE;
-                const float* U0 = sUK + (pB & 1) * SA;
-                const float* U1 = sUK + ((pB + 1) & 1) * SA;
-                float* R1 = fsm + T::RKO + (pB & 1) * 3 * SA;
-                float* __restrict__ pn = a.Pn + ((size_t)(pB + 1) * 3) * HW;
-                if constexpr (X2) {
-#pragma unroll
-                    for (int k = 0; k < T::KB2; ++k) {
-                        const int q = qB[k];
-                        if (q < 0) continue;
-                        const int o = q & 0xffff;
-                        const f2 uo = ld2s(U0 + o);
-                        const f2 gv = (q & (1 << 16)) ? sub2(ld2s(U0 + o + SW), uo) : z2;
-                        const f2 gh = sub2(pk(hi_of(uo), U0[o + 2]), uo);
-                        const f2 gz = top ? sub2(ld2s(U1 + o), uo) : z2;
-                        const f2 k0 = ld2s(st + o), k1 = ld2s(st + SA + o), k2 = ld2s(st + 2 * SA + o);
-                        const f2 ph = fma2(gv, eta2, fma2(sub2(k0, ld2s(st + T::QOFF + o)), br2, k0));
-                        const f2 qh = fma2(gh, (q & (1 << 21)) ? pk(eta, 0.f) : eta2,
-                                           fma2(sub2(k1, ld2s(st + T::QOFF + SA + o)), br2, k1));
-                        const f2 wh = fma2(gz, eta2,
-                                           fma2(sub2(k2, ld2s(st + T::QOFF + 2 * SA + o)), br2, k2));
-                        const f2 inv = inv_norm2(fma2(wh, wh, fma2(qh, qh, mul2(ph, ph))));
-                        const f2 p0 = mul2(ph, inv), p1 = mul2(qh, inv), p2 = mul2(wh, inv);
-                        const bool in = (q & (1 << 20)) != 0;
-                        st2s(R1 + o, in ? fma2(sub2(p0, k0), bk2, p0) : z2);
-                        st2s(R1 + SA + o, in ? fma2(sub2(p1, k1), bk2, p1) : z2);
-                        st2s(R1 + 2 * SA + o, in ? fma2(sub2(p2, k2), bk2, p2) : z2);
-                        if (own && hB[k] >= 0) {
-                            st2s(pn + hB[k], p0);
-                            st2s(pn + HW + hB[k], p1);
-                            st2s(pn + 2 * HW + hB[k], p2);
-                        }
-                    }
-                } else
-#pragma unroll
-                for (int k = 0; k < T::KB; ++k) {
-                    const int pt = ptB[k];
-                    if (pt < 0) continue;
-                    const int o = pt & 0xffff;
-                    const float uo = U0[o];
-                    const float gv = (pt & (1 << 16)) ? U0[o + SW] - uo : 0.f;
-                    const float gh = (pt & (1 << 18)) ? U0[o + 1] - uo : 0.f;
-                    const float gz = top ? U1[o] - uo : 0.f;
-                    const float k0 = st[o], k1 = st[SA + o], k2 = st[2 * SA + o];
-                    const float ph = (k0 + br * (k0 - st[T::QOFF + o])) + eta * gv;
-                    const float qh = (k1 + br * (k1 - st[T::QOFF + SA + o])) + eta * gh;
-                    const float wh = (k2 + br * (k2 - st[T::QOFF + 2 * SA + o])) + eta * gz;
-                    const float n2 = fmaf(wh, wh, fmaf(qh, qh, __fmul_rn(ph, ph)));  // pinned order (all 3D paths)
-                    const float inv = (n2 > 1.f) ? rsqrt_ftz(n2) : 1.f;
-                    const float p0 = ph * inv, p1 = qh * inv, p2 = wh * inv;
-                    const bool in = pt & (1 << 20);
-                    R1[o] = in ? p0 + bk * (p0 - k0) : 0.f;
-                    R1[SA + o] = in ? p1 + bk * (p1 - k1) : 0.f;
-                    R1[2 * SA + o] = in ? p2 + bk * (p2 - k2) : 0.f;
-                    if (own && gB[k] >= 0) {
-                        pn[gB[k]] = p0;
-                        pn[HW + gB[k]] = p1;
-                        pn[2 * HW + gB[k]] = p2;
-                    }
-                }
-            }
-            __syncthreads();
-            if (pB >= zb) {  // C(pB): u_{k+1}
-                const int zg = a.z0 + pB;
-                const bool zlo = zg > 0, zhi = zg < a.Zg - 1;
-                const float* st = fsm + c1 * T::STAGE;
-                const float* R0 = sRK + (pB & 1) * 3 * SA;
-                const float* Rm = sRK + ((pB - 1) & 1) * 3 * SA;
-                float* U = fsm + T::UK1O + (pB & 1) * SA;
-                if constexpr (X2) {
-#pragma unroll
-                    for (int k = 0; k < T::KC2; ++k) {
-                        const int q = qC[k];
-                        if (q < 0) continue;
-                        const int o = q & 0xffff;
-                        const f2 a2 = ld2s(R0 + SA + o);
-                        const f2 x = divT2(q, ld2s(R0 + o), ld2s(R0 + o - SW), a2,
-                                           pk(R0[SA + o - 1], lo_of(a2)), ld2s(R0 + 2 * SA + o),
-                                           ld2s(Rm + 2 * SA + o), zhi, zlo);
-                        st2s(U + o, clamp2(fma2(x, nlam2, ld2s(st + T::VOFF + o)), nonneg,
-                                           (q & (1 << 20)) != 0));
-                    }
-                } else
-#pragma unroll
-                for (int k = 0; k < T::KC; ++k) {
-                    const int pt = ptC[k];
-                    if (pt < 0) continue;
-                    const int o = pt & 0xffff;
-                    const float x = divT(pt, R0[o], R0[o - SW], R0[SA + o], R0[SA + o - 1],
-                                         R0[2 * SA + o], Rm[2 * SA + o], zhi, zlo);
-                    U[o] = clampu(st[T::VOFF + o] - lam * x, pt);
-                }
-            }
-            __syncthreads();
-            const int pD = s;
-            if (pD >= zb) {  // D(pD): P_{k+2}, centre tile
-                const int zg = a.z0 + pD;
-                const bool top = zg < a.Zg - 1;
-                const float* U0 = sUK1 + (pD & 1) * SA;
-                const float* U1 = sUK1 + ((pD + 1) & 1) * SA;
-                const float* R0 = sRK + (pD & 1) * 3 * SA;
-                float* __restrict__ pn2 = a.Rn + ((size_t)(pD + 1) * 3) * HW;
-                if constexpr (X2) {
-#pragma unroll
-                    for (int k = 0; k < T::KD2; ++k) {
-                        const int q = qD[k];
-                        if (q < 0) continue;
-                        const int o = q & 0xffff;
-                        const f2 uo = ld2s(U0 + o);
-                        const f2 gv = (q & (1 << 16)) ? sub2(ld2s(U0 + o + SW), uo) : z2;
-                        const f2 gh = sub2(pk(hi_of(uo), U0[o + 2]), uo);
-                        const f2 gz = top ? sub2(ld2s(U1 + o), uo) : z2;
-                        const f2 ph = fma2(gv, eta2, ld2s(R0 + o));
-                        const f2 qh = fma2(gh, (q & (1 << 21)) ? pk(eta, 0.f) : eta2, ld2s(R0 + SA + o));
-                        const f2 wh = fma2(gz, eta2, ld2s(R0 + 2 * SA + o));
-                        const f2 inv = inv_norm2(fma2(wh, wh, fma2(qh, qh, mul2(ph, ph))));
-                        st2s(pn2 + hD[k], mul2(ph, inv));
-                        st2s(pn2 + HW + hD[k], mul2(qh, inv));
-                        st2s(pn2 + 2 * HW + hD[k], mul2(wh, inv));
-                    }
-                } else
-#pragma unroll
-                for (int rr = 0; rr < T::KD; ++rr) {
-                    const int r = ty + rr * (NT / TX), gi = i0 + r, gj = j0 + tx;
-                    if (gi >= H || gj >= W) continue;
-                    const int o = (r + 2) * SW + (tx + 4);
-                    const float uo = U0[o];
-                    const float gv = (gi < H - 1) ? U0[o + SW] - uo : 0.f;
-                    const float gh = (gj < W - 1) ? U0[o + 1] - uo : 0.f;
-                    const float gz = top ? U1[o] - uo : 0.f;
-                    const float ph = R0[o] + eta * gv;
-                    const float qh = R0[SA + o] + eta * gh;
-                    const float wh = R0[2 * SA + o] + eta * gz;
-                    const float n2 = fmaf(wh, wh, fmaf(qh, qh, __fmul_rn(ph, ph)));  // pinned order (all 3D paths)
-                    const float inv = (n2 > 1.f) ? rsqrt_ftz(n2) : 1.f;
-                    const int g = gi * W + gj;
-                    pn2[g] = ph * inv;
-                    pn2[HW + g] = qh * inv;
-                    pn2[2 * HW + g] = wh * inv;
-                }
-            }
-        }
-        // rotate the stage slots: plane s + 3 goes where plane s was
-        const int t = c0;
-        c0 = c1;
-        c1 = c2;
-        c2 = t;
-    }
-    pdl_trigger();
 }
 
 // caller duals (three [Zl][H][W] arrays) -> interiors of the P and R sets
@@ -1958,39 +1531,6 @@ static int fgp3d_col_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
     return PT_OK;
 }
 
-template <int TX, int TY, int NT, bool X2>
-static int fgp3d_pair_launch(Fgp3Args& a, cudaStream_t st)
-{
-    using T = Fgp3Pair<TX, TY, NT>;
-    const size_t smem = (size_t)T::SMEM_FLOATS * 4;
-    {
-        const int rc = ensure_smem((const void*)fgp3d_pair_kernel<TX, TY, NT, X2>, smem);
-        if (rc) return rc;
-    }
-    Fgp3Maps m;
-    memset(&m, 0, sizeof(m));
-    const cuuint64_t W = a.W, H = a.H;
-    const cuuint64_t d4[4] = {W, H, 3, (cuuint64_t)a.Zl + 2};
-    const cuuint32_t b4[4] = {(cuuint32_t)T::SW, (cuuint32_t)T::SR, 3, 1};
-    const cuuint64_t d3[3] = {W, H, (cuuint64_t)a.Zl};
-    const cuuint32_t b3[3] = {(cuuint32_t)T::SW, (cuuint32_t)T::SR, 1};
-    int rc = make_map(&m.R, a.R, 4, d4, b4);
-    if (!rc) rc = make_map(&m.P, a.P, 4, d4, b4);
-    if (!rc) rc = make_map(&m.V, a.v, 3, d3, b3);
-    if (rc) return rc;
-    static const int zc_env = [] {
-        const char* e = getenv("PT_FGP3_ZCHUNK");
-        return e ? std::max(0, atoi(e)) : 0;  // 0 / empty: the default
-    }();
-    // runs of 32 planes (A and B start two planes early): 256^3 FGP-100 in
-    // 12.8 / 12.6 / 12.2 / 13.1 ms for runs of 16 / 24 / 32 / 64
-    a.zchunk = zc_env ? zc_env : 32;
-    const dim3 grid((a.W + TX - 1) / TX, (a.H + TY - 1) / TY, (a.Zl + a.zchunk - 1) / a.zchunk);
-    PT_CHECK_CUDA(launch_pdl(fgp3d_pair_kernel<TX, TY, NT, X2>, grid, dim3(T::NT), smem, st, a, m));
-    PT_CHECK_LAUNCH();
-    return PT_OK;
-}
-
 int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int inner,
               int nonneg, float pog, int64_t iteration, int64_t* bad_iter, const ZHalo* halo,
               int sm_count, cudaStream_t st)
@@ -2033,8 +1573,8 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
     // reads set 0 twice, P_{-1} = P_0 with beta_r = 0), an odd last iteration
     // by the one-iteration kernel.  PT_FGP3_PAIR selects the pass kernel: 6
     // (default) the register-column kernel with 32 x 16-point tiles; 5 / 7 / 8
-    // other column tiles; 1-4 the windowed pair kernel; 0 none (one iteration
-    // per pass).  256^3 FGP-100: 9.2 ms (6), 11.7 ms (1), 14.0 ms (0).
+    // other column tiles; 0 none (one iteration per pass).  256^3 FGP-100:
+    // 9.2 ms (6), 14.0 ms (0); the windowed pair kernel this replaced: 11.7 ms.
     static const int pair_env = [] {
         const char* e = getenv("PT_FGP3_PAIR");
         return (e && *e) ? atoi(e) : 6;
@@ -2060,18 +1600,10 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
             a.beta = (float)betas[kk];
             a.beta_r = kk == 0 ? 0.f : (float)betas[kk - 1];
             a.nonneg = nonneg;
-            // windowed pair kernel, 256^3 FGP-100: 12.2 ms (64 x 8 tiles, 256
-            // threads, 32-plane runs), 13.8 ms with 512 threads; point pairs
-            // with f32x2 math (1): 11.7 ms; 2 / 3 / 4 one point per lane with
-            // 512 threads, X2 with 384 threads, one point per lane with 256
             rc = pair_env == 5 ? fgp3d_col_launch<16, 16, 2>(a, sm_count, st)
-               : pair_env == 6 ? fgp3d_col_launch<16, 16, 3>(a, sm_count, st)
                : pair_env == 7 ? fgp3d_col_launch<32, 16, 1>(a, sm_count, st)
                : pair_env == 8 ? fgp3d_col_launch<16, 24, 2>(a, sm_count, st)
-               : pair_env == 2 ? fgp3d_pair_launch<64, 8, 512, false>(a, st)
-               : pair_env == 3 ? fgp3d_pair_launch<64, 8, 384, true>(a, st)
-               : pair_env == 4 ? fgp3d_pair_launch<64, 8, 256, false>(a, st)
-                               : fgp3d_pair_launch<64, 8, 256, true>(a, st);
+                               : fgp3d_col_launch<16, 16, 3>(a, sm_count, st);
             if (rc) return rc;
             sp = o1;
             sk = o1 + 1;
@@ -2117,7 +1649,7 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
     // one per iteration.  Every slab must hold >= 2 planes (decided from the
     // global plane count so that all ranks agree).
     const int ranks = (halo && halo->world > 1) ? halo->world : 1;
-    bool col_slabs = tma && pq && pair_env >= 5 && inner >= 2 && Zg / (ranks * G) >= 2;
+    bool col_slabs = tma && pq && pair_env && inner >= 2 && Zg / (ranks * G) >= 2;
     for (int g = 0; g < G; ++g) col_slabs = col_slabs && sl[g].Zl >= 2;
     if (col_slabs) {
         int rc = PT_OK;

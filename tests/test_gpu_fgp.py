@@ -140,19 +140,18 @@ np.save(sys.argv[1], np.concatenate(out))
 
 
 def test_fgp_3d_pair_pass_bitwise(tmp_path):
-    """Two iterations per HBM pass -- the register-column kernel (default, 5-8:
-    tile shapes) and the windowed pair kernel (1 / 3: point pairs with f32x2
-    math, 2 / 4: one point per lane) -- give the same values as one iteration
-    per pass (0); odd counts, ragged tiles, image-edge and interior tiles and
-    z-runs included."""
+    """Two iterations per HBM pass -- the register-column kernel (default 6,
+    5 / 7 / 8: other tile shapes, explicit z-run lengths) -- give the same
+    values as one iteration per pass (0); odd counts, ragged tiles, image-edge
+    and interior tiles and z-runs included."""
     import os
     import subprocess
     import sys
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
-    for flag, zc in (("", ""), ("0", ""), ("1", ""), ("2", "16"), ("3", ""), ("4", ""),
-                     ("1", "16"), ("5", ""), ("6", "19"), ("7", ""), ("8", "")):
-        path = tmp_path / f"pair{flag}.npy"
+    for flag, zc in (("", ""), ("0", ""), ("0", "16"), ("5", ""), ("6", "19"), ("6", "7"),
+                     ("7", ""), ("8", "")):
+        path = tmp_path / f"pair{flag}_{zc}.npy"
         env = dict(os.environ, PT_FGP3_PAIR=flag, PT_FGP3_ZCHUNK=zc)
         subprocess.run([sys.executable, "-c", _PAIR_SNIPPET.format(repo=repo), str(path)],
                        check=True, env=env, timeout=300)

@@ -17,7 +17,7 @@ for k in fwd_band adj_gather fgp2d fwd_reduce; do
       -o $O/p_$k python tools/prof_kernels.py > $O/ncu_$k.log 2>&1
   ncu -i $O/p_$k.ncu-rep --page raw --csv > $O/raw_$k.csv 2>/dev/null
 done
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:fgp3d_pair -s 5 -c 1 \
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:fgp3d_col -s 5 -c 1 \
     -o $O/p_fgp3d python tools/fgp3_timing.py > $O/ncu_fgp3d.log 2>&1
 ncu -i $O/p_fgp3d.ncu-rep --page raw --csv > $O/raw_fgp3d.csv 2>/dev/null
 PT_FGP3_PAIR=0 timeout 600 ncu --set full --import-source on --clock-control none -k regex:fgp3d_iter \
