@@ -707,12 +707,12 @@ struct Fgp3Args {
     int Zl, H, W, z0, Zg, zchunk;
     const float* v;     // [Zl][H][W]
     const float* vtop;  // v of global plane z0 + Zl (ghost)
-    const float* P;     // P_k      [Zl + 2][3][H][W]
-    const float* R;     // R_k
+    const float* P;     // P_{k-1}  [Zl + 2][3][H][W]
+    const float* R;     // P_k
     float* Pn;          // P_{k+1}
-    float* Rn;          // R_{k+1}
+    float* Rn;          // P_{k+2} (two-iteration pass)
     float lam, eta, beta;  // beta = beta_k (momentum of the output)
-    float beta_r;          // PQ form: R_k = P_k + beta_r (P_k - P_{k-1}) formed on chip
+    float beta_r;          // R_k = P_k + beta_r (P_k - P_{k-1}) formed on chip
     int nonneg;
     // register-column pass on a z-slab: planes -2, -1 / Zl, Zl + 1 come from
     // 2-plane ghost buffers [side][P_k: 2 x 3 planes, P_{k-1}: 2 x 3, v: 2]
@@ -741,32 +741,30 @@ __device__ __forceinline__ void cpa4(uint32_t dst, const float* src, bool valid)
                  "r"(valid ? 4 : 0));
 }
 
-// Stage layout of one plane: R box [3][TY+2][TX+8] (rows i0-1 .., columns
-// j0-4 ..), v box [TY+2][TX+8] (same window), P box [3][TY][TX].
-// PQ form: the R box holds P_k, a second window box (same shape, at QOFF)
-// holds P_{k-1}, and R is formed on chip; no P box.  40 B per voxel of HBM
-// traffic instead of 52, more shared-memory reads and FMAs.
-template <int TX, int TY, int NS, bool PQ = false>
+// Stage layout of one plane: the P_k box [3][TY+2][TX+8] (rows i0-1 ..,
+// columns j0-4 ..), the P_{k-1} box (same shape, at QOFF) and the v box
+// [TY+2][TX+8] (same window); R_k is formed on chip ("PQ" form: 40 B per
+// voxel of HBM traffic; storing R as a state of its own took 52 B and was
+// slower, 15.35 vs 14.1 ms per 256^3 FGP-100).
+template <int TX, int TY, int NS>
 struct Fgp3Tile {
     static constexpr int NT = TX * TY / 2;      // 2 output rows per thread
     static constexpr int RW = TX + 8, RR = TY + 2, ARR = RR * RW;
     static constexpr int WIN3 = (3 * ARR + 31) & ~31;
-    static constexpr int QOFF = WIN3;                      // PQ only
-    static constexpr int VOFF = PQ ? 2 * WIN3 : WIN3;
-    static constexpr int POFF = (VOFF + ARR + 31) & ~31;   // R form only
-    static constexpr int PARR = TX * TY;
-    static constexpr int STAGE = PQ ? ((VOFF + ARR + 31) & ~31) : ((POFF + 3 * PARR + 31) & ~31);
+    static constexpr int QOFF = WIN3;
+    static constexpr int VOFF = 2 * WIN3;
+    static constexpr int STAGE = (VOFF + ARR + 31) & ~31;
     static constexpr int NWW = (TY + 1) * (TX + 1);   // u window
     static constexpr int SMEM_FLOATS = NS * STAGE + 2 * NWW;
     static constexpr int TMA_BYTES_RV = 4 * ARR * 4;
-    static constexpr int TMA_BYTES_P = PQ ? 3 * ARR * 4 : 3 * PARR * 4;
+    static constexpr int TMA_BYTES_P = 3 * ARR * 4;
 };
 
-template <int TX, int TY, int NS, bool TMA, bool PQ>
+template <int TX, int TY, int NS, bool TMA>
 __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
                                                                  const __grid_constant__ Fgp3Maps m)
 {
-    using T = Fgp3Tile<TX, TY, NS, PQ>;
+    using T = Fgp3Tile<TX, TY, NS>;
     constexpr int NT = T::NT, RW = T::RW, RR = T::RR, ARR = T::ARR, NWW = T::NWW;
     constexpr int KU = (NWW + NT - 1) / NT;
     extern __shared__ __align__(128) float fsm[];
@@ -805,16 +803,10 @@ __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
                 "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
                 " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb),
                 "l"(&m.R), "r"(j0 - 4), "r"(i0 - 1), "r"(0), "r"(p + 1), "r"(bar) : "memory");
-            if (PQ)  // P_{k-1} window
-                asm volatile(
-                    "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-                    " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb + (uint32_t)T::QOFF * 4u),
-                    "l"(&m.P), "r"(j0 - 4), "r"(i0 - 1), "r"(0), "r"(p + 1), "r"(bar) : "memory");
-            else     // P_k centre
-                asm volatile(
-                    "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-                    " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb + (uint32_t)T::POFF * 4u),
-                    "l"(&m.P), "r"(j0), "r"(i0), "r"(0), "r"(p + 1), "r"(bar) : "memory");
+            asm volatile(  // P_{k-1} window
+                "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb + (uint32_t)T::QOFF * 4u),
+                "l"(&m.P), "r"(j0 - 4), "r"(i0 - 1), "r"(0), "r"(p + 1), "r"(bar) : "memory");
             if (withv && p < a.Zl)
                 asm volatile(
                     "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
@@ -839,25 +831,14 @@ __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
                 cpa4(sb + (uint32_t)((arr < 3 ? arr * ARR : T::VOFF) + r * RW + 3 + c) * 4u,
                      src + (ok ? gi * W + gj : 0), ok);
             }
-            if (PQ) {
-                constexpr int NQ = 3 * RR * CW;  // P_{k-1} windows
-                for (int idx = tid; idx < NQ; idx += NT) {
-                    const int arr = idx / (RR * CW), rem = idx - arr * (RR * CW);
-                    const int r = rem / CW, c = rem - r * CW;
-                    const int gi = i0 - 1 + r, gj = j0 - 1 + c;
-                    const bool ok = gi >= 0 && gi < H && gj >= 0 && gj < W;
-                    cpa4(sb + (uint32_t)(T::QOFF + arr * ARR + r * RW + 3 + c) * 4u,
-                         a.P + b0 + arr * HW + (ok ? gi * W + gj : 0), ok);
-                }
-            } else {
-                for (int idx = tid; idx < 3 * T::PARR; idx += NT) {
-                    const int comp = idx / T::PARR, rem = idx - comp * T::PARR;
-                    const int r = rem / TX, c = rem - r * TX;
-                    const int gi = i0 + r, gj = j0 + c;
-                    const bool ok = gi < H && gj < W;
-                    cpa4(sb + (uint32_t)(T::POFF + idx) * 4u,
-                         a.P + b0 + comp * HW + (ok ? gi * W + gj : 0), ok);
-                }
+            constexpr int NQ = 3 * RR * CW;  // P_{k-1} windows
+            for (int idx = tid; idx < NQ; idx += NT) {
+                const int arr = idx / (RR * CW), rem = idx - arr * (RR * CW);
+                const int r = rem / CW, c = rem - r * CW;
+                const int gi = i0 - 1 + r, gj = j0 - 1 + c;
+                const bool ok = gi >= 0 && gi < H && gj >= 0 && gj < W;
+                cpa4(sb + (uint32_t)(T::QOFF + arr * ARR + r * RW + 3 + c) * 4u,
+                     a.P + b0 + arr * HW + (ok ? gi * W + gj : 0), ok);
             }
             asm volatile("cp.async.commit_group;");
         }
@@ -884,15 +865,11 @@ __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
                                ((gj > 0) << 3) | ((gi < H && gj < W) << 4))
                             : -1;
     }
-    // R at staged offset o (PQ: formed from P_k and P_{k-1}, the same
-    // expression the R-state form stores, so both forms give identical bits)
+    // R_k at staged offset o, formed from P_k and P_{k-1}
     const float br = a.beta_r;
     auto rv = [&](const float* st, int o) -> float {
-        if (PQ) {
-            const float pv = st[o];
-            return pv + br * (pv - st[T::QOFF + o]);
-        }
-        return st[o];
+        const float pv = st[o];
+        return pv + br * (pv - st[T::QOFF + o]);
     };
     // u of plane z (its stage s) into sU[z & 1]; R_w of z - 1 from stage s1
     auto compute_U = [&](int z, int s, int s1) {
@@ -947,7 +924,6 @@ __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
         const float* U0 = sU + (z & 1) * NWW;
         const float* U1 = sU + ((z + 1) & 1) * NWW;
         float* __restrict__ pn = a.Pn + ((size_t)(z + 1) * 3) * HW;
-        float* __restrict__ rn = PQ ? nullptr : a.Rn + ((size_t)(z + 1) * 3) * HW;
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
             const int r = ty + rr * RSTEP, gi = i0 + r;
@@ -968,12 +944,6 @@ __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
             pn[g] = p0;
             pn[HW + g] = p1;
             pn[2 * HW + g] = p2;
-            if (!PQ) {
-                const float* pc = st + T::POFF + r * TX + tx;
-                rn[g] = p0 + a.beta * (p0 - pc[0]);
-                rn[HW + g] = p1 + a.beta * (p1 - pc[T::PARR]);
-                rn[2 * HW + g] = p2 + a.beta * (p2 - pc[2 * T::PARR]);
-            }
         }
     }
     if (!TMA) asm volatile("cp.async.wait_group 0;");
@@ -1151,13 +1121,13 @@ static int fgp3d_ghost_exchange(const Fgp3Slab* sl, int G, int H, int W, int set
     return PT_OK;
 }
 
-template <int TX, int TY, int NS, bool TMA, bool PQ>
+template <int TX, int TY, int NS, bool TMA>
 static int fgp3d_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
 {
-    using T = Fgp3Tile<TX, TY, NS, PQ>;
+    using T = Fgp3Tile<TX, TY, NS>;
     const size_t smem = (size_t)T::SMEM_FLOATS * 4;
     {
-        const int rc = ensure_smem((const void*)fgp3d_iter_kernel<TX, TY, NS, TMA, PQ>, smem);
+        const int rc = ensure_smem((const void*)fgp3d_iter_kernel<TX, TY, NS, TMA>, smem);
         if (rc) return rc;
     }
     Fgp3Maps m;
@@ -1166,11 +1136,10 @@ static int fgp3d_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
         const cuuint64_t W = a.W, H = a.H;
         const cuuint64_t d4[4] = {W, H, 3, (cuuint64_t)a.Zl + 2};
         const cuuint32_t bR[4] = {(cuuint32_t)T::RW, (cuuint32_t)T::RR, 3, 1};
-        const cuuint32_t bP[4] = {(cuuint32_t)TX, (cuuint32_t)TY, 3, 1};
         const cuuint64_t d3[3] = {W, H, (cuuint64_t)a.Zl};
         const cuuint32_t b3[3] = {(cuuint32_t)T::RW, (cuuint32_t)T::RR, 1};
         int rc = make_map(&m.R, a.R, 4, d4, bR);
-        if (!rc) rc = make_map(&m.P, a.P, 4, d4, PQ ? bR : bP);
+        if (!rc) rc = make_map(&m.P, a.P, 4, d4, bR);
         if (!rc) rc = make_map(&m.V, a.v, 3, d3, b3);
         if (!rc) rc = make_map(&m.Vt, a.vtop, 2, d3, b3);
         if (rc) return rc;
@@ -1184,8 +1153,8 @@ static int fgp3d_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
     // 8 -> 155 us, 16 -> 153 us, 32 -> 165 us, 64 -> 189 us per iteration
     a.zchunk = zc_env ? zc_env : 16;
     dim3 grid(gx, gy, (a.Zl + a.zchunk - 1) / a.zchunk);
-    PT_CHECK_CUDA(launch_pdl(fgp3d_iter_kernel<TX, TY, NS, TMA, PQ>, grid, dim3(T::NT), smem, st,
-                             a, m));
+    PT_CHECK_CUDA(launch_pdl(fgp3d_iter_kernel<TX, TY, NS, TMA>, grid, dim3(T::NT), smem, st, a,
+                             m));
     PT_CHECK_LAUNCH();
     return PT_OK;
 }
@@ -1537,13 +1506,6 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
 {
     // TMA needs 16-byte row pitch; 64 x 8 tiles, 3-stage ring
     const bool tma = (W % 4) == 0 && tma_available();
-    // PQ form (40 B/voxel, R formed on chip) by default: 14.1 vs 15.35 ms per
-    // FGP-100 at 256^3 for the R-state form (52 B/voxel); PT_FGP3_PQ=0 selects it
-    static const int pq_env = [] {
-        const char* e = getenv("PT_FGP3_PQ");
-        return e ? atoi(e) : 1;
-    }();
-    const bool pq = pq_env != 0;
     std::vector<double> betas(inner);
     double t = 1.0;
     for (int k = 0; k < inner; ++k) {
@@ -1579,7 +1541,7 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
         const char* e = getenv("PT_FGP3_PAIR");
         return (e && *e) ? atoi(e) : 6;
     }();
-    if (G == 1 && (!halo || halo->world <= 1) && tma && pq && pair_env && inner >= 2 &&
+    if (G == 1 && (!halo || halo->world <= 1) && tma && pair_env && inner >= 2 &&
         sl[0].z0 == 0 && sl[0].Zl == Zg) {
         const int Zl = sl[0].Zl;
         int rc = PT_OK;
@@ -1623,7 +1585,7 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
             a.beta = (float)betas[kk];
             a.beta_r = kk == 0 ? 0.f : (float)betas[kk - 1];
             a.nonneg = nonneg;
-            rc = fgp3d_launch<64, 8, 3, true, true>(a, sm_count, st);
+            rc = fgp3d_launch<64, 8, 3, true>(a, sm_count, st);
             if (rc) return rc;
             sk = o;
         }
@@ -1649,7 +1611,7 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
     // one per iteration.  Every slab must hold >= 2 planes (decided from the
     // global plane count so that all ranks agree).
     const int ranks = (halo && halo->world > 1) ? halo->world : 1;
-    bool col_slabs = tma && pq && pair_env && inner >= 2 && Zg / (ranks * G) >= 2;
+    bool col_slabs = tma && pair_env && inner >= 2 && Zg / (ranks * G) >= 2;
     for (int g = 0; g < G; ++g) col_slabs = col_slabs && sl[g].Zl >= 2;
     if (col_slabs) {
         int rc = PT_OK;
@@ -1709,7 +1671,7 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
                 a.beta = (float)betas[kk];
                 a.beta_r = kk == 0 ? 0.f : (float)betas[kk - 1];
                 a.nonneg = nonneg;
-                rc = fgp3d_launch<64, 8, 3, true, true>(a, sm_count, st);
+                rc = fgp3d_launch<64, 8, 3, true>(a, sm_count, st);
                 if (rc) return rc;
             }
             sk = o;
@@ -1733,23 +1695,13 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
         }
         return PT_OK;
     }
-    // R form: sets 0/1 = P, R of even iterations, 2/3 of odd ones.
-    // PQ form: sets 0, 1, 2 rotate P_{k-1}, P_k -> P_{k+1} (set 1 starts as a copy of P_0).
-    int rc = fgp3d_exchange(sl, G, H, W, pq ? 0 : 1, true, halo, st);
+    // one iteration per pass: sets 0, 1, 2 rotate P_{k-1}, P_k -> P_{k+1}
+    int rc = fgp3d_exchange(sl, G, H, W, 0, true, halo, st);
     if (rc) return rc;
     for (int kk = 0; kk < inner; ++kk) {
-        int set_p, set_r, set_pn, set_rn;
-        if (pq) {
-            set_r = kk % 3;                          // P_k (windows)
-            set_p = kk == 0 ? 0 : (kk + 2) % 3;      // P_{k-1}
-            set_pn = (kk + 1) % 3;
-            set_rn = -1;
-        } else {
-            set_p = (kk & 1) ? 2 : 0;
-            set_r = set_p + 1;
-            set_pn = (kk & 1) ? 0 : 2;
-            set_rn = set_pn + 1;
-        }
+        const int set_r = kk % 3;                      // P_k (windows)
+        const int set_p = kk == 0 ? 0 : (kk + 2) % 3;  // P_{k-1}
+        const int set_pn = (kk + 1) % 3;
         for (int g = 0; g < G; ++g) {
             const int Zl = sl[g].Zl;
             Fgp3Args a;
@@ -1759,28 +1711,20 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
             a.P = fgp3d_set(sl[g].work, set_p, Zl, H, W);
             a.R = fgp3d_set(sl[g].work, set_r, Zl, H, W);
             a.Pn = fgp3d_set(sl[g].work, set_pn, Zl, H, W);
-            a.Rn = set_rn >= 0 ? fgp3d_set(sl[g].work, set_rn, Zl, H, W) : nullptr;
+            a.Rn = nullptr;
             a.lam = (float)lam;
             a.eta = (float)(1.0 / (12.0 * lam));
             a.beta = (float)betas[kk];
             a.beta_r = kk == 0 ? 0.f : (float)betas[kk - 1];
             a.nonneg = nonneg;
-            if (pq)
-                rc = tma ? fgp3d_launch<64, 8, 3, true, true>(a, sm_count, st)
-                         : fgp3d_launch<32, 8, 3, false, true>(a, sm_count, st);
-            else
-                rc = tma ? fgp3d_launch<64, 8, 3, true, false>(a, sm_count, st)
-                         : fgp3d_launch<32, 8, 3, false, false>(a, sm_count, st);
+            rc = tma ? fgp3d_launch<64, 8, 3, true>(a, sm_count, st)
+                     : fgp3d_launch<32, 8, 3, false>(a, sm_count, st);
             if (rc) return rc;
         }
-        rc = fgp3d_exchange(sl, G, H, W, pq ? set_pn : set_rn, false, halo, st);
+        rc = fgp3d_exchange(sl, G, H, W, set_pn, false, halo, st);
         if (rc) return rc;
     }
-    const int fin = pq ? inner % 3 : ((inner & 1) ? 2 : 0);
-    if (!pq) {
-        rc = fgp3d_exchange(sl, G, H, W, fin, false, halo, st);  // P ghost below for D^T
-        if (rc) return rc;
-    }
+    const int fin = inner % 3;
     for (int g = 0; g < G; ++g) {
         const int Zl = sl[g].Zl;
         Fgp3Args a;
