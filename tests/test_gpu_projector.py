@@ -228,3 +228,34 @@ def test_every_gather_tile_matches_oracle(tile):
     out = subprocess.run([sys.executable, "-c", _TILE_SNIPPET.format(repo=repo)], env=env,
                          check=True, capture_output=True, text=True, timeout=300)
     assert float(out.stdout.strip().splitlines()[-1]) <= 1e-5
+
+
+_FWD_CFG_SNIPPET = r"""
+import sys, numpy as np
+sys.path.insert(0, {repo!r})
+import oracle as O
+from paper_2602_09527_b200 import ParallelGeometry, forward_project
+g = ParallelGeometry.uniform(41, 771)
+x = np.random.default_rng(5).random((530, 512))
+sub = tuple(range(1, 41, 3))
+got = forward_project(x, g, sub).double().cpu().numpy()
+O.set_mode("fast")
+ref = O.forward_project(x, g, sub)
+print(float(np.linalg.norm(got - ref) / np.linalg.norm(ref)))
+"""
+
+
+@pytest.mark.parametrize("cfg,tma", [(c, "1") for c in range(8)] + [(3, "0"), (4, "0")])
+def test_every_forward_tile_config_matches_oracle(cfg, tma):
+    """Each forward band/tile configuration (PT_FWD_CFG, images from 512 up;
+    the plan's default is 3), with row-branch tiles by TMA or by cp.async
+    (PT_FWD_TMA=0), against the oracle on a non-square image with ragged bands
+    and tiles."""
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PT_FWD_CFG=str(cfg), PT_FWD_TMA=tma)
+    out = subprocess.run([sys.executable, "-c", _FWD_CFG_SNIPPET.format(repo=repo)], env=env,
+                         check=True, capture_output=True, text=True, timeout=300)
+    assert float(out.stdout.strip().splitlines()[-1]) <= 1e-5
