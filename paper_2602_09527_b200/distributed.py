@@ -1,15 +1,17 @@
-"""Multi-GPU data parallelism (one process per GPU): image rows or angle
-sectors (2D), z-slabs (slice-stacked 3D).
+"""Multi-GPU data parallelism (one process per GPU): angle sectors or image
+rows (2D), z-slabs (slice-stacked 3D).
 
-Image rows (the 2D default): rank g owns image rows [g*H/G, (g+1)*H/G) with a
-row-slab plan; each forward's partial line integrals are summed in float64 by
-ncclAllReduce (8 |S_i| B bytes per step: 0.7 MB at config 2), the gather,
-ProxSkip step and TV prox touch only the own rows (ghost rows exchanged with
-ranks g -+ 1 per FGP launch).  The per-step exchange is 23x smaller than the
-sector layout's image-sized allreduce and the prox is sharded too.
+Image rows (``decomposition="rows"``): rank g owns image rows
+[g*H/G, (g+1)*H/G) with a row-slab plan; each forward's partial line
+integrals are summed in float64 by ncclAllReduce (8 |S_i| B bytes per step:
+0.7 MB at config 2), the gather, ProxSkip step and TV prox touch only the own
+rows (ghost rows exchanged with ranks g -+ 1 per FGP launch).  The per-step
+exchange is 23x smaller than the sector layout's image-sized allreduce and
+the prox is sharded too.
 
-Rank g of G owns the contiguous sinogram rows of angles
-[g*A/G, (g+1)*A/G) (geometry.angle_sector).  Staggered subsets therefore
+Angle sectors (the 2D default, north_star's layout): rank g of G owns the
+contiguous sinogram rows of angles [g*A/G, (g+1)*A/G)
+(geometry.angle_sector).  Staggered subsets therefore
 split across all ranks, so every stochastic step is parallel; the per-step
 partial gradient A_i^T r (4 * n_px bytes) and the snapshot full gradient are
 summed by ncclAllReduce inside the native executor on the solver stream; the
@@ -32,7 +34,10 @@ from . import _native as N
 
 
 def nccl_library_path() -> str:
-    """The libnccl.so.2 torch is using (nvidia-nccl wheel), else the system one."""
+    """The libnccl.so.2 torch is using (nvidia-nccl wheel), else the system one
+    (PT_NCCL_LIB names another build, e.g. the tests' host-staged shim)."""
+    if os.environ.get("PT_NCCL_LIB"):
+        return os.environ["PT_NCCL_LIB"]
     try:
         import nvidia.nccl  # type: ignore
         base = list(nvidia.nccl.__path__)[0]
