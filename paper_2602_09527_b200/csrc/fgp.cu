@@ -1,9 +1,9 @@
 // FGP (Beck-Teboulle fast gradient projection on the dual) TV prox for
 // sm_100a, temporally blocked: one launch runs T inner iterations on a
-// (RH x RW) region held on chip, of which the central (RH-2T-2) x (RW-2T-2)
+// (RH x RW) region held on chip, of which the central (RH-2T) x (RW-2T)
 // points are exact after T iterations (each iteration's stencil reaches one
-// point further, pkg/src/proxtomo/regularizers.py:62-76); only those are
-// written back.  So a prox call with n inner iterations costs ceil(n/T)
+// point further, pkg/src/proxtomo/regularizers.py:62-76; the final launch's
+// x = v - lam D^T(p, q) needs one ring more); only those are written back.  So a prox call with n inner iterations costs ceil(n/T)
 // HBM round trips of the dual state instead of n.
 //
 // Per-iteration math (regularizers.py:112-129), lam = tau*alpha, eta = 1/(8 lam):
