@@ -45,6 +45,7 @@ typedef int (*fn_allreduce)(const void*, void*, size_t, int, int, nccl_comm, cud
 typedef int (*fn_destroy)(nccl_comm);
 typedef const char* (*fn_errstr)(int);
 typedef int (*fn_p2p)(const void*, size_t, int, int, nccl_comm, cudaStream_t);
+typedef int (*fn_bcast)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t);
 typedef int (*fn_group)(void);
 constexpr int kNcclFloat32 = 7;
 constexpr int kNcclFloat64 = 8;
@@ -58,6 +59,7 @@ struct NcclApi {
     fn_destroy destroy = nullptr;
     fn_errstr errstr = nullptr;
     fn_p2p send = nullptr, recv = nullptr;  // ncclSend / ncclRecv (z-slab halos)
+    fn_bcast bcast = nullptr;               // ncclBroadcast (row gathers of the sharded prox)
     fn_group group_start = nullptr, group_end = nullptr;
 };
 
@@ -77,6 +79,7 @@ int nccl_load(const char* path, NcclApi* api)
     api->recv = (fn_p2p)dlsym(api->so, "ncclRecv");
     api->group_start = (fn_group)dlsym(api->so, "ncclGroupStart");
     api->group_end = (fn_group)dlsym(api->so, "ncclGroupEnd");
+    api->bcast = (fn_bcast)dlsym(api->so, "ncclBroadcast");
     if (!api->get_uid || !api->init_rank || !api->allreduce || !api->destroy) {
         pt::set_error("libnccl is missing symbols");
         return PT_ENCCL;
@@ -206,6 +209,12 @@ struct pt_session {
     double* y64 = nullptr;       // partial line integrals (A rows x B), float64
     float* rows_work = nullptr;  // extended-row FGP state (fgp2d_slab_floats)
     pt::RowHalo rhalo;
+    // angle sectors with the 2D TV prox sharded by image rows: rank g runs
+    // the prox on rows [sr0, sr0 + sHl) (ghost rows over NCCL, bitwise the
+    // whole-image prox) and the new iterate's rows are gathered on every rank
+    bool sector_rows = false;
+    int sr0 = 0, sHl = 0;
+    bool duals_sharded = false;  // dual rows outside [sr0, sr0 + sHl) are stale
 };
 
 namespace {
@@ -407,6 +416,52 @@ int rows_tv_prox(pt_session* s, double lam, float pog, float* xn, int64_t k, cud
     a.x_out = xn; a.xhat = s->xhat; a.h = s->h; a.work = s->rows_work;
     return pt::fgp2d_rows_run(&a, 1, P->Hg, P->W, lam, s->d.tv_inner, s->d.tv_nonneg, pog, k,
                               s->bad, &s->rhalo, st);
+}
+
+// Rows [H g / G, H (g + 1) / G) of rank g (the image-row split of the sector
+// layout's sharded prox; distributed.rowslab_bounds uses the same formula).
+inline int sector_row(int H, int g, int world) { return (int)((long long)H * g / world); }
+
+// Every rank's rows of `a` (H x W, rank g's rows valid on rank g) on every
+// rank: one grouped ncclBroadcast per owner, in place.
+int gather_sector_rows(pt_session* s, float* a, cudaStream_t st)
+{
+    const NcclApi& api = s->nccl;
+    const int H = s->plan->H, W = s->plan->W;
+    int e = api.group_start();
+    for (int g = 0; g < s->world && !e; ++g) {
+        const int r0 = sector_row(H, g, s->world), r1 = sector_row(H, g + 1, s->world);
+        float* rows = a + (size_t)r0 * W;
+        e = api.bcast(rows, rows, (size_t)(r1 - r0) * W, kNcclFloat32, g, s->comm, st);
+    }
+    const int e2 = api.group_end();
+    if (e || e2) {
+        pt::set_error("NCCL row gather: %s", api.errstr ? api.errstr(e ? e : e2) : "error");
+        return PT_ENCCL;
+    }
+    return PT_OK;
+}
+
+// The 2D TV prox of an angle-sector rank, sharded by image rows: the rows
+// FGP driver on this rank's rows of the (replicated) image -- ghost rows from
+// ranks g -+ 1, bitwise the whole-image prox -- then the new iterate and the
+// control variate rows gathered on every rank.  The dual state keeps only the
+// own rows current (gathered at the end of a run call, see pt_session_run).
+int sector_rows_tv_prox(pt_session* s, double lam, float pog, float* xn, int64_t k,
+                        cudaStream_t st)
+{
+    pt_plan* P = s->plan;
+    const size_t off = (size_t)s->sr0 * P->W;
+    pt::Fgp2Slab a;
+    a.Hl = s->sHl; a.r0 = s->sr0;
+    a.v = s->v + off; a.p = s->dp + off; a.q = s->dq + off;
+    a.x_out = xn + off; a.xhat = s->xhat + off; a.h = s->h + off; a.work = s->rows_work;
+    int rc = pt::fgp2d_rows_run(&a, 1, P->H, P->W, lam, s->d.tv_inner, s->d.tv_nonneg, pog, k,
+                                s->bad, &s->rhalo, st);
+    s->duals_sharded = true;
+    if (!rc) rc = gather_sector_rows(s, xn, st);
+    if (!rc) rc = gather_sector_rows(s, s->h, st);
+    return rc;
 }
 
 // The 3D TV prox of a z-slab rank (halos over NCCL), or of G virtual slabs of
@@ -757,6 +812,8 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
                     rc = slab_tv_prox(s, lam, pog, xn, k, st);
                 else if (s->rows)
                     rc = rows_tv_prox(s, lam, pog, xn, k, st);
+                else if (s->sector_rows)
+                    rc = sector_rows_tv_prox(s, lam, pog, xn, k, st);
                 else
                     rc = pt::launch_tv_prox(P, s->v, lam, d.tv_inner, d.tv_nonneg, s->dp, s->dq,
                                             s->dw, xn, s->xhat, s->h, pog, k, s->bad,
@@ -782,6 +839,14 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
             if (rc) return rc;
         }
         s->cur = 1 - s->cur;
+    }
+    if (s->duals_sharded) {
+        // sharded sector prox: whole dual images at the API boundary (the
+        // state views, the next call's warm start reads only its own rows)
+        int rc = gather_sector_rows(s, s->dp, st);
+        if (!rc) rc = gather_sector_rows(s, s->dq, st);
+        if (rc) return rc;
+        s->duals_sharded = false;
     }
     return PT_OK;
 }
@@ -941,6 +1006,26 @@ int attach_sector(pt_session* s, const NcclApi& api, nccl_comm comm, int rank, i
     s->comm = comm;
     s->rank = rank;
     s->world = world;
+    pt_plan* P = s->plan;
+    // the replicated TV prox is sharded by image rows when every rank gets
+    // enough rows for the ghost exchange (PT_SECTOR_PROX=0 keeps it replicated)
+    static const bool env = [] {
+        const char* e = getenv("PT_SECTOR_PROX");
+        return !(e && e[0] == '0');
+    }();
+    if (env && world > 1 && P->Z == 1 && P->Hg == P->H && s->d.prox_kind == 1 &&
+        s->d.estimator != PT_EST_FISTA && api.send && api.recv && api.group_start &&
+        api.group_end && api.bcast && P->H / world >= pt::kRowGhost) {
+        s->sr0 = sector_row(P->H, rank, world);
+        s->sHl = sector_row(P->H, rank + 1, world) - s->sr0;
+        PT_CHECK_CUDA(cudaMalloc(&s->rows_work,
+                                 (size_t)pt::fgp2d_slab_floats(s->sHl, P->W) * sizeof(float)));
+        s->rhalo.rank = rank;
+        s->rhalo.world = world;
+        s->rhalo.ctx = s;
+        s->rhalo.exchange = nccl_rows_halo;
+        s->sector_rows = true;
+    }
     return build_selections(s);
 }
 

@@ -232,6 +232,7 @@ class IterateState:
     work_seconds: float = 0.0
     zslab: tuple | None = None  # (z0, z1, Z) when this rank holds a z-slab
     rowslab: tuple | None = None  # (r0, r1, H) when this rank holds image rows
+    sharded: bool = False  # attached to a multi-rank communicator (any layout)
 
     @property
     def x(self) -> torch.Tensor:
@@ -337,7 +338,8 @@ def _init_state(config: SolverConfig, problem: TomoProblem, x0, stream=None,
                          rng_subset=np.random.default_rng(streams[0]),
                          rng_theta=np.random.default_rng(streams[1]),
                          rng_refresh=np.random.default_rng(streams[2]), zslab=zslab,
-                         rowslab=rowslab)
+                         rowslab=rowslab, sharded=_multi_rank(data_parallel or zslab is not None
+                                                              or rowslab is not None))
     if kind == "fista":
         session.init()  # y = x0, t = 1 (solvers.py:378)
     if config.estimator in ("svrg", "lsvrg"):
@@ -656,11 +658,19 @@ def _run_loop(state: IterateState, config, problem, reference, ground_truth,
     return record
 
 
+def _multi_rank(attached: bool) -> bool:
+    if not attached:
+        return False
+    import torch.distributed as dist
+    return dist.is_initialized() and dist.get_world_size() > 1
+
+
 def _bad_iteration(state: IterateState) -> int | None:
-    """First non-finite iteration (z-slab ranks: the minimum over ranks, so
-    every rank raises together)."""
+    """First non-finite iteration; on several ranks the minimum over ranks
+    (each rank checks the pixels it computed: its slab, or its rows of a
+    sharded prox), so every rank raises together."""
     bad = state.session.bad_iteration()
-    if state.zslab is None and state.rowslab is None:
+    if not state.sharded:
         return bad
     import torch.distributed as dist
     t = torch.tensor([INT64_MAX if bad is None else bad], device="cuda", dtype=torch.int64)

@@ -1,6 +1,7 @@
 /* Test infrastructure: a host-staged stand-in for libnccl.so.2 that lets the
  * library's real multi-rank code (angle sectors, image rows, z-slabs: the
- * ncclAllReduce / ncclSend / ncclRecv call sequences on the session stream)
+ * ncclAllReduce / ncclSend / ncclRecv / ncclBroadcast call sequences on the
+ * session stream)
  * run as several processes on ONE GPU.  Every collective synchronises the
  * caller's stream, copies the device buffer to the host, exchanges it through
  * files in a rendezvous directory (the "unique id" is its path) and copies the
@@ -29,16 +30,18 @@ typedef struct {
     int rank, nranks;
     long ar_seq;
     long *p2p_send, *p2p_recv; /* per peer sequence numbers */
+    long* bcast_seq;           /* per root */
 } shim_comm;
 
-enum { OP_SEND, OP_RECV };
+enum { OP_SEND, OP_RECV, OP_BCAST };
 typedef struct {
     int kind;
     void* buf;
     size_t bytes;
-    int peer;
+    int peer; /* the root of a broadcast */
     shim_comm* comm;
     CUstream stream;
+    const void* src; /* broadcast source on the root */
 } shim_op;
 
 static shim_op g_ops[4096];
@@ -109,6 +112,7 @@ int ncclCommInitRank(shim_comm** comm, int nranks, ncclUniqueId id, int rank)
     c->nranks = nranks;
     c->p2p_send = (long*)calloc((size_t)nranks, sizeof(long));
     c->p2p_recv = (long*)calloc((size_t)nranks, sizeof(long));
+    c->bcast_seq = (long*)calloc((size_t)nranks, sizeof(long));
     *comm = c;
     return 0;
 }
@@ -118,6 +122,7 @@ int ncclCommDestroy(shim_comm* c)
     if (c) {
         free(c->p2p_send);
         free(c->p2p_recv);
+        free(c->bcast_seq);
         free(c);
     }
     return 0;
@@ -177,6 +182,25 @@ static int run_op(const shim_op* o)
 {
     char path[320];
     shim_comm* c = o->comm;
+    if (o->kind == OP_BCAST) {
+        snprintf(path, sizeof path, "%s/bc_%d_%ld", c->dir, o->peer, c->bcast_seq[o->peer]++);
+        char* h = (char*)malloc(o->bytes ? o->bytes : 1);
+        int rc = 0;
+        if (c->rank == o->peer) {
+            if (o->bytes && cuMemcpyDtoH(h, (CUdeviceptr)o->src, o->bytes) != CUDA_SUCCESS) rc = 1;
+            if (!rc) rc = write_file(path, h, o->bytes);
+            if (!rc && o->src != o->buf && o->bytes &&
+                cuMemcpyHtoD((CUdeviceptr)o->buf, h, o->bytes) != CUDA_SUCCESS)
+                rc = 1;
+        } else {
+            wait_file(path);
+            rc = read_file(path, h, o->bytes);
+            if (!rc && o->bytes && cuMemcpyHtoD((CUdeviceptr)o->buf, h, o->bytes) != CUDA_SUCCESS)
+                rc = 1;
+        }
+        free(h);
+        return rc;
+    }
     if (o->kind == OP_SEND) {
         char* h = (char*)malloc(o->bytes ? o->bytes : 1);
         if (o->bytes && cuMemcpyDtoH(h, (CUdeviceptr)o->buf, o->bytes) != CUDA_SUCCESS) return 1;
@@ -199,34 +223,45 @@ static int run_op(const shim_op* o)
 
 static int flush_ops(void)
 {
-    /* sends first (they never block), then the receives */
+    /* what this rank publishes first (sends, broadcasts it roots; they never
+       block), then what it waits for (receives, the other roots' broadcasts) */
     for (int i = 0; i < g_nops; ++i)
         if (cuStreamSynchronize(g_ops[i].stream) != CUDA_SUCCESS) return 1;
     for (int k = 0; k < 2; ++k)
-        for (int i = 0; i < g_nops; ++i)
-            if (g_ops[i].kind == (k == 0 ? OP_SEND : OP_RECV) && run_op(&g_ops[i])) return 1;
+        for (int i = 0; i < g_nops; ++i) {
+            const shim_op* o = &g_ops[i];
+            const int publishes = o->kind == OP_SEND ||
+                                  (o->kind == OP_BCAST && o->comm->rank == o->peer);
+            if (publishes == (k == 0) && run_op(o)) return 1;
+        }
     g_nops = 0;
     return 0;
 }
 
 static int queue_op(int kind, void* buf, size_t count, int dtype, int peer, shim_comm* c,
-                    CUstream stream)
+                    CUstream stream, const void* src)
 {
     const size_t es = elem_size(dtype);
     if (!es || g_nops >= (int)(sizeof g_ops / sizeof g_ops[0])) return 5;
-    shim_op o = {kind, buf, count * es, peer, c, stream};
+    shim_op o = {kind, buf, count * es, peer, c, stream, src};
     g_ops[g_nops++] = o;
     return g_group ? 0 : flush_ops();
 }
 
 int ncclSend(const void* buf, size_t count, int dtype, int peer, shim_comm* c, CUstream stream)
 {
-    return queue_op(OP_SEND, (void*)buf, count, dtype, peer, c, stream);
+    return queue_op(OP_SEND, (void*)buf, count, dtype, peer, c, stream, NULL);
 }
 
 int ncclRecv(void* buf, size_t count, int dtype, int peer, shim_comm* c, CUstream stream)
 {
-    return queue_op(OP_RECV, buf, count, dtype, peer, c, stream);
+    return queue_op(OP_RECV, buf, count, dtype, peer, c, stream, NULL);
+}
+
+int ncclBroadcast(const void* send, void* recv, size_t count, int dtype, int root, shim_comm* c,
+                  CUstream stream)
+{
+    return queue_op(OP_BCAST, recv, count, dtype, root, c, stream, send);
 }
 
 int ncclGroupStart(void)

@@ -135,7 +135,7 @@ else:
 """
 
 
-def _launch(shim, tmp_path, world, kind, arg):
+def _launch(shim, tmp_path, world, kind, arg, extra_env=None):
     """Run `world` rank processes on cuda:0 and the single-device reference;
     returns (per-rank outputs, reference output) paths."""
     port = _free_port()
@@ -146,7 +146,8 @@ def _launch(shim, tmp_path, world, kind, arg):
     for r in range(world):
         path = str(tmp_path / f"{kind}_{arg}_w{world}_r{r}{ext}")
         env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), PORT=str(port),
-                   MASTER_ADDR="127.0.0.1", PT_NCCL_LIB=shim, PT_NCCL_SHIM_DIR=str(shim_dir))
+                   MASTER_ADDR="127.0.0.1", PT_NCCL_LIB=shim, PT_NCCL_SHIM_DIR=str(shim_dir),
+                   **(extra_env or {}))
         procs.append(subprocess.Popen([sys.executable, "-c", _RANK.format(repo=REPO), path,
                                        kind, arg], env=env))
         outs.append(path)
@@ -166,12 +167,17 @@ def _launch(shim, tmp_path, world, kind, arg):
     return outs, ref
 
 
-@pytest.mark.parametrize("est,world", [("svrg", 2), ("saga", 3), ("full", 2), ("fista", 3)])
-def test_angle_sectors_multirank_match_emulation_bitwise(shim, tmp_path, est, world):
+@pytest.mark.parametrize("est,world,prox", [("svrg", 2, "1"), ("saga", 3, "1"), ("full", 2, "1"),
+                                            ("fista", 3, "1"), ("svrg", 3, "0")])
+def test_angle_sectors_multirank_match_emulation_bitwise(shim, tmp_path, est, world, prox):
     """Real sector ranks (own angles, partial A_i^T r, rank-order allreduce,
-    shared epilogue and prox on every rank): every rank's iterate equals the
-    single-device emulation of the same sectors bit for bit."""
-    outs, ref = _launch(shim, tmp_path, world, "sectors", est)
+    shared epilogue; the TV prox sharded by image rows with ghost-row
+    exchanges and the new rows broadcast to every rank, or replicated with
+    PT_SECTOR_PROX=0): every rank's iterate equals the single-device emulation
+    of the same sectors bit for bit."""
+    outs, ref = _launch(shim, tmp_path, world, "sectors", est, {"PT_SECTOR_PROX": prox})
+    # the sharded prox ran exactly when enabled (its row broadcasts; FISTA keeps it replicated)
+    assert bool(list((tmp_path / "rdv").glob("shim_*/bc_*"))) == (prox == "1" and est != "fista")
     want = np.load(ref)
     for path in outs:
         assert np.array_equal(np.load(path), want)

@@ -23,5 +23,5 @@ def test_shim_builds_and_exports_what_the_library_resolves(tmp_path):
                                                          capture_output=True, text=True).stdout))
     src = open(os.path.join(REPO, "paper_2602_09527_b200", "csrc", "session.cu")).read()
     resolved = set(re.findall(r'dlsym\(api->so, "(nccl\w+)"\)', src))
-    assert len(resolved) == 9
+    assert len(resolved) == 10
     assert resolved <= exported
