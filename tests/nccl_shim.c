@@ -65,7 +65,7 @@ static void wait_file(const char* path)
     long spins = 0;
     while (stat(path, &st) != 0) {
         usleep(50);
-        if (++spins > 20L * 1000 * 1000 / 50) { /* 20 s: a peer is gone */
+        if (++spins > 300L * 1000 * 1000 / 50) { /* 300 s: a peer is gone */
             fprintf(stderr, "nccl_shim: timeout waiting for %s\n", path);
             abort();
         }
