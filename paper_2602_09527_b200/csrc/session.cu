@@ -447,20 +447,24 @@ int gather_sector_rows(pt_session* s, float* a, cudaStream_t st)
 // ranks g -+ 1, bitwise the whole-image prox -- then the new iterate and the
 // control variate rows gathered on every rank.  The dual state keeps only the
 // own rows current (gathered at the end of a run call, see pt_session_run).
+// FISTA (fista = true): x+ = prox(v) only -- no control variate, and the
+// momentum kernel checks x+ for finiteness.
 int sector_rows_tv_prox(pt_session* s, double lam, float pog, float* xn, int64_t k,
-                        cudaStream_t st)
+                        cudaStream_t st, bool fista)
 {
     pt_plan* P = s->plan;
     const size_t off = (size_t)s->sr0 * P->W;
     pt::Fgp2Slab a;
     a.Hl = s->sHl; a.r0 = s->sr0;
     a.v = s->v + off; a.p = s->dp + off; a.q = s->dq + off;
-    a.x_out = xn + off; a.xhat = s->xhat + off; a.h = s->h + off; a.work = s->rows_work;
-    int rc = pt::fgp2d_rows_run(&a, 1, P->H, P->W, lam, s->d.tv_inner, s->d.tv_nonneg, pog, k,
-                                s->bad, &s->rhalo, st);
+    a.x_out = xn + off; a.work = s->rows_work;
+    a.xhat = fista ? nullptr : s->xhat + off;
+    a.h = fista ? nullptr : s->h + off;
+    int rc = pt::fgp2d_rows_run(&a, 1, P->H, P->W, lam, s->d.tv_inner, s->d.tv_nonneg,
+                                fista ? 0.f : pog, k, fista ? nullptr : s->bad, &s->rhalo, st);
     s->duals_sharded = true;
     if (!rc) rc = gather_sector_rows(s, xn, st);
-    if (!rc) rc = gather_sector_rows(s, s->h, st);
+    if (!rc && !fista) rc = gather_sector_rows(s, s->h, st);
     return rc;
 }
 
@@ -804,7 +808,9 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
                     PT_CHECK_CUDA(cudaMemsetAsync(s->dq, 0, s->n * 4, st));
                     if (dw) PT_CHECK_CUDA(cudaMemsetAsync(dw, 0, s->n * 4, st));
                 }
-                if (fista)  // x+ = prox(v); no control variate (the momentum kernel checks x+)
+                if (fista && s->sector_rows)
+                    rc = sector_rows_tv_prox(s, lam, pog, xn, k, st, true);
+                else if (fista)  // x+ = prox(v); no control variate (the momentum kernel checks x+)
                     rc = pt::launch_tv_prox(P, s->v, lam, d.tv_inner, d.tv_nonneg, s->dp, s->dq,
                                             s->dw, xn, nullptr, nullptr, 0.f, k, nullptr,
                                             s->fgp_work, st);
@@ -813,7 +819,7 @@ int pt_session_run(pt_session* s, int32_t n_steps, const int32_t* host_subset,
                 else if (s->rows)
                     rc = rows_tv_prox(s, lam, pog, xn, k, st);
                 else if (s->sector_rows)
-                    rc = sector_rows_tv_prox(s, lam, pog, xn, k, st);
+                    rc = sector_rows_tv_prox(s, lam, pog, xn, k, st, false);
                 else
                     rc = pt::launch_tv_prox(P, s->v, lam, d.tv_inner, d.tv_nonneg, s->dp, s->dq,
                                             s->dw, xn, s->xhat, s->h, pog, k, s->bad,
@@ -1014,7 +1020,7 @@ int attach_sector(pt_session* s, const NcclApi& api, nccl_comm comm, int rank, i
         return !(e && e[0] == '0');
     }();
     if (env && world > 1 && P->Z == 1 && P->Hg == P->H && s->d.prox_kind == 1 &&
-        s->d.estimator != PT_EST_FISTA && api.send && api.recv && api.group_start &&
+        api.send && api.recv && api.group_start &&
         api.group_end && api.bcast && P->H / world >= pt::kRowGhost) {
         s->sr0 = sector_row(P->H, rank, world);
         s->sHl = sector_row(P->H, rank + 1, world) - s->sr0;

@@ -176,8 +176,8 @@ def test_angle_sectors_multirank_match_emulation_bitwise(shim, tmp_path, est, wo
     PT_SECTOR_PROX=0): every rank's iterate equals the single-device emulation
     of the same sectors bit for bit."""
     outs, ref = _launch(shim, tmp_path, world, "sectors", est, {"PT_SECTOR_PROX": prox})
-    # the sharded prox ran exactly when enabled (its row broadcasts; FISTA keeps it replicated)
-    assert bool(list((tmp_path / "rdv").glob("shim_*/bc_*"))) == (prox == "1" and est != "fista")
+    # the sharded prox ran exactly when enabled (its row broadcasts)
+    assert bool(list((tmp_path / "rdv").glob("shim_*/bc_*"))) == (prox == "1")
     want = np.load(ref)
     for path in outs:
         assert np.array_equal(np.load(path), want)
