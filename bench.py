@@ -55,8 +55,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--decomposition", default="sectors", choices=["sectors", "rows"],
-                    help="2D multi-GPU layout: angle sectors with a replicated image and prox "
-                         "(north_star's layout, default) or image rows")
+                    help="2D multi-GPU layout: angle sectors with a replicated image "
+                         "(north_star's layout, default; the TV prox sharded by rows, "
+                         "PT_SECTOR_PROX=0 replicates it) or image rows")
     ap.add_argument("--dry-run", action="store_true",
                     help="test hook: form the N-rank process group (gloo, no GPU work) and "
                          "print its size; used by tests/test_bench_cli.py")
@@ -302,6 +303,13 @@ def build_gpu_problem(cfg, torch):
 # launch category -> (kernel, ncu kernel-name key) as in profiles/ncu_roofline_*.json
 KERNEL_OF = {"fwd_band": "fwd_band_kernel", "gather": "adj_gather_kernel",
              "fgp": "fgp2d_kernel", "fgp3": "fgp3d_col_kernel"}
+
+
+def sector_prox_sharded(world):
+    """Whether the sector layout's TV prox runs sharded by image rows (the
+    library's rule: > 1 rank, PT_SECTOR_PROX not 0; >= 9 rows per rank holds
+    for every 2D config)."""
+    return world > 1 and os.environ.get("PT_SECTOR_PROX", "1") != "0"
 
 
 def owned_angles(cfg, rank, world, sectors):
@@ -647,7 +655,9 @@ def gpu_arm(args, cfg, rank, world, local):
             "parallelism": ("1 GPU" if not dp else
                             f"z-slab dp{world}" if zs else
                             f"image-row dp{world}" if rs else
-                            f"angle-sector dp{world} (replicated image and prox)"),
+                            f"angle-sector dp{world} (replicated image, "
+                            f"{'row-sharded' if sector_prox_sharded(world) else 'replicated'} "
+                            f"prox)"),
             "timed": {"epochs": args.steps, "iterations": n_iter, "prox_calls": n_prox,
                       "snapshots": int(np.count_nonzero(refr))},
             "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
