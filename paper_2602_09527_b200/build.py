@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libproxtomo_b200.so")
 SOURCES = ["capi.cu", "projector.cu", "fgp.cu", "reduce.cu", "session.cu", "pdhg.cu"]
-HEADERS = ["pt_internal.cuh", "pt_simd.cuh", os.path.join("..", "..", "include", "proxtomo_b200.h")]
+HEADERS = ["pt_internal.cuh", "pt_simd.cuh", "pt_joseph.cuh", os.path.join("..", "..", "include", "proxtomo_b200.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

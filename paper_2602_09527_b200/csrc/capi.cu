@@ -32,7 +32,9 @@ void workspace_sizes(const pt_plan* plan, size_t* partial_floats, size_t* red_do
     *partial_floats =
         (size_t)plan->n_bands * plan->Z * plan->B * (size_t)plan->max_angles_per_launch;
     const size_t chunks = (plan->A + plan->max_angles_per_launch - 1) / plan->max_angles_per_launch;
-    *red_doubles = ((size_t)plan->A * plan->Z * plan->B + 255) / 256 + chunks + 16;
+    // block sums of the residual norm: one per 256 rows (band reduction) or
+    // one per 32 rays (small-image forward)
+    *red_doubles = ((size_t)plan->A * plan->Z * plan->B + 31) / 32 + chunks + 16;
     *image_floats = (size_t)plan->Z * plan->H * plan->W;
 }
 

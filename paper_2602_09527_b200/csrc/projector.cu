@@ -14,45 +14,9 @@
 
 #include "pt_internal.cuh"
 #include "pt_simd.cuh"
+#include "pt_joseph.cuh"
 
 namespace pt {
-
-// floor() on the fma pipe: x + 1.5*2^23 rounded toward -inf leaves floor(x)
-// in the low mantissa bits (valid for |x| < 2^22).
-static constexpr float kMagic = 12582912.0f;
-static constexpr int kMagicBits = 0x4B400000;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p)
-{
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ float lds(uint32_t a)
-{
-    float v;
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
-    return v;
-}
-// (x[a], x[a+1]) of a shared-memory address: one IMAD-formed address, two
-// loads with an immediate offset
-__device__ __forceinline__ void lds_pair(uint32_t a, float& v0, float& v1)
-{
-    asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+4];"
-                 : "=f"(v0), "=f"(v1)
-                 : "r"(a));
-}
-// a*4 + base as one IMAD; `base` is made opaque so the compiler cannot
-// re-associate the folded constants back out of it
-__device__ __forceinline__ uint32_t mad4(uint32_t a, uint32_t base)
-{
-    uint32_t r;
-    asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(r) : "r"(a), "r"(base));
-    return r;
-}
-__device__ __forceinline__ uint32_t opaque(uint32_t v)
-{
-    asm volatile("" : "+r"(v));
-    return v;
-}
 
 // ---------------------------------------------------------------------------
 // Forward: a work item = one band of TY consecutive steps (image rows for
@@ -118,20 +82,6 @@ struct FwdTile {
     static constexpr int BUF = (TY * PITCH_R > NL * PITCH_C) ? TY * PITCH_R : NL * PITCH_C;
     static constexpr int SMEM = BUF * 4;
 };
-
-__device__ __forceinline__ void cp_async4(uint32_t dst, const float* src, bool valid)
-{
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src),
-                 "r"(valid ? 4 : 0));
-}
-__device__ __forceinline__ void cp_async16(uint32_t dst, const float* src, int valid_bytes)
-{
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-                 "r"(valid_bytes));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-__device__ __forceinline__ void cp_async_wait_one() { asm volatile("cp.async.wait_group 1;"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;"); }
 
 struct FwdItem {
     int z, branch, band, tile, group;
@@ -257,65 +207,6 @@ __device__ __forceinline__ void stage_tile(const FwdArgs& P, const FwdItem& it, 
             }
         }
     }
-}
-
-// Sum of the Joseph samples st in [st_a, st_b) of one ray inside the tile.
-// LS / SS: byte strides of one lane / one step in the staged tile.
-template <int LS, int SS>
-__device__ __forceinline__ float ray_band_sum(uint32_t tile_u32, int st_a, int st_b, float pl,
-                                              float mf)
-{
-    // shared byte address of lane 0 at step st_a, minus the floor-trick
-    // magic offset folded in (mod 2^32)
-    uint32_t sbase = tile_u32 + (uint32_t)(st_a * SS) - (uint32_t)kMagicBits * (uint32_t)LS;
-    const f2 pl2 = pk(pl, pl), m2 = pk(mf, mf), mg2 = pk(kMagic, kMagic);
-    const f2 eight2 = pk(8.f, 8.f);
-    // a trip = 8 samples as 4 packed pairs (s + u, s + u + 4), u = 0..3: the
-    // pair's positions are u*m + (pos(s), pos(s + 4)), so one FFMA2 per pair
-    // with a broadcast immediate and no per-pair step counter
-    f2 st2 = pk((float)st_a, (float)st_a + 4.f);
-    f2 acc2 = pk(0.f, 0.f);
-    const int n = st_b - st_a;
-    int i = 0;
-    for (; i + 8 <= n; i += 8) {
-        const uint32_t sb = opaque(sbase);
-        const f2 base2 = fma2(st2, m2, pl2);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const f2 pos = u == 0 ? base2 : fma2(pk((float)u, (float)u), m2, base2);
-            const f2 t = add2_rm(pos, mg2);
-            const f2 fr = sub2(pos, sub2(t, mg2));
-            float ta, tb, a0, a1, b0, b1;
-            upk(t, ta, tb);
-            const uint32_t aa = __float_as_uint(ta) * (uint32_t)LS + sb + u * SS;
-            const uint32_t ab = __float_as_uint(tb) * (uint32_t)LS + sb + (u + 4) * SS;
-            asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+%3];"
-                         : "=f"(a0), "=f"(a1) : "r"(aa), "n"(LS));
-            asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+%3];"
-                         : "=f"(b0), "=f"(b1) : "r"(ab), "n"(LS));
-            const f2 x0 = pk(a0, b0), x1 = pk(a1, b1);
-            acc2 = add2(acc2, fma2(fr, sub2(x1, x0), x0));
-        }
-        st2 = add2(st2, eight2);
-        sbase += 8 * SS;
-    }
-    float acc0, acc1;
-    upk(acc2, acc0, acc1);
-    float sa, sb_;
-    upk(st2, sa, sb_);
-    for (; i < n; ++i) {
-        const float pa = fmaf(sa, mf, pl);
-        const float ta = __fadd_rd(pa, kMagic);
-        const float fa = pa - (ta - kMagic);
-        const uint32_t aa = __float_as_uint(ta) * (uint32_t)LS + opaque(sbase);
-        float a0, a1;
-        asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+%3];"
-                     : "=f"(a0), "=f"(a1) : "r"(aa), "n"(LS));
-        acc0 += fmaf(fa, a1 - a0, a0);
-        sa += 1.f;
-        sbase += SS;
-    }
-    return acc0 + acc1;
 }
 
 // Row-branch tile by TMA: the image as a 4D tensor (4, W/4, H, Z) and one box
@@ -570,6 +461,135 @@ __global__ void __launch_bounds__(256) fwd_reduce_kernel(RedArgs P)
     pdl_trigger();
 }
 
+// ---------------------------------------------------------------------------
+// Small images (pt_joseph.cuh): one launch writes finished residual rows --
+// no band partials, no reduction launch.  Every CTA stages the whole image
+// and sums 32 * RW consecutive rays of the selection, one warp per segment
+// (lanes = adjacent rays); the segment sums are combined in float64 in
+// segment order, then scaled, and the data rows subtracted, exactly as
+// fwd_reduce_kernel does.  A ray's value does not depend on which CTA
+// computes it, so subsets and the full selection agree bitwise (and the
+// cluster-resident executor, cluster.cu, reproduces it bit for bit).
+// ---------------------------------------------------------------------------
+struct SmallArgs {
+    const float* x;
+    const AngleTab* tab;
+    const int32_t* sel_angle;
+    int32_t n_k, H, W, B;
+    const float* data;
+    const float* data2;
+    float* y;
+    double* block_sums;
+    double* y64;  // row-slab partial: s * step_len in float64, no data, no y
+};
+
+__global__ void __launch_bounds__(1024) fwd_small_kernel(SmallArgs a)
+{
+    extern __shared__ __align__(16) float img[];
+    __shared__ float part[kSmallNseg][64];
+    __shared__ double red[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nw = blockDim.x >> 5;
+    const int rw = warp / kSmallNseg, seg = warp - rw * kSmallNseg;
+    const int rays_cta = 32 * (nw / kSmallNseg);
+    const int rl = rw * 32 + lane;  // ray within the CTA
+    const uint32_t buf = smem_u32(img);
+
+    // ray tables first (static data: overlaps the predecessor's tail)
+    const int total = a.n_k * a.B;
+    const int ray = blockIdx.x * rays_cta + rl;
+    const bool live = ray < total;
+    const int k = live ? ray / a.B : 0;
+    const int b = live ? ray - k * a.B : 0;
+    const int ang = a.sel_angle[k];
+    const AngleTab t = a.tab[ang];
+    const SmallRay sr = small_ray(t, b, a.H, a.W);
+
+    pdl_wait();  // the image is the predecessor's output
+    small_stage(a.x, a.H, a.W, buf, 0, blockDim.x);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    const float acc = live ? small_segment(buf, sr, seg) : 0.f;
+    part[seg][rl] = acc;
+    __syncthreads();
+    double sq = 0.0;
+    if (seg == 0 && live) {
+        const double yd = small_line_integral(&part[0][rl], 64, t.step_len);
+        const size_t o = (size_t)k * a.B + b;
+        if (a.y64) {
+            a.y64[o] = yd;
+        } else {
+            const float yv = residual_value(yd, a.data, a.data2, (size_t)ang * a.B + b);
+            a.y[o] = yv;
+            sq = (double)yv * (double)yv;
+        }
+    }
+    if (a.block_sums) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, o);
+        if (lane == 0) red[warp] = sq;
+        __syncthreads();
+        if (tid == 0) {
+            double s = 0.0;
+            for (int i = 0; i < nw; ++i) s += red[i];
+            a.block_sums[blockIdx.x] = s;
+        }
+    }
+    pdl_trigger();
+}
+
+static bool forward_small_ok(const pt_plan* plan)
+{
+    static const bool on = [] {
+        const char* e = getenv("PT_FWD_SMALL");
+        return !(e && e[0] == '0');
+    }();
+    return on && plan->Z == 1 && plan->H <= kSmallMax && plan->W <= kSmallMax;
+}
+
+static int run_forward_small(pt_plan* plan, Workspace* ws, const pt_selection* sel,
+                             const float* x, const float* data, float* y, double* sumsq,
+                             cudaStream_t st, const float* data2, double* y64)
+{
+    {
+        const int rc = ensure_smem((const void*)fwd_small_kernel, kSmallSmem);
+        if (rc) return rc;
+    }
+    const long long total = (long long)sel->n * plan->B;
+    // rays per CTA: 32 (subsets: more CTAs) up to 128 (long selections: fewer
+    // whole-image stagings)
+    const long long per = total / (64LL * plan->sm_count);
+    const int rw = (int)std::max(1LL, std::min(2LL, per));
+    const int rays_cta = 32 * rw;
+    const long long nblk = (total + rays_cta - 1) / rays_cta;
+    if (nblk > INT32_MAX || (sumsq && (size_t)nblk > ws->red_doubles)) {
+        set_error("forward launch too large");
+        return PT_EINVAL;
+    }
+    SmallArgs a;
+    a.x = x;
+    a.tab = plan->d_tab;
+    a.sel_angle = sel->d_angle;
+    a.n_k = sel->n;
+    a.H = plan->H;
+    a.W = plan->W;
+    a.B = plan->B;
+    a.data = data;
+    a.data2 = data2;
+    a.y = y;
+    a.block_sums = sumsq ? ws->red : nullptr;
+    a.y64 = y64;
+    {
+        ProfScope ps(ws, PT_PROF_FWD_BAND, st);
+        PT_CHECK_CUDA(launch_pdl(fwd_small_kernel, dim3((unsigned)nblk), dim3(32 * kSmallNseg * rw),
+                                 (size_t)kSmallSmem, st, a));
+        PT_CHECK_LAUNCH();
+    }
+    if (sumsq) return launch_sum_doubles(ws->red, nblk, sumsq, 0, st);
+    return PT_OK;
+}
+
 template <int TY, int TX, int NT, int MINB>
 static int run_forward_cfg(pt_plan* plan, Workspace* ws, const pt_selection* sel,
                            const float* x, const float* x2, const float* data, float* y,
@@ -728,6 +748,18 @@ int launch_forward(pt_plan* plan, Workspace* ws, const pt_selection* sel, const 
         return PT_OK;
     }
     if (y64 && sumsq) { set_error("partial forward has no residual norm"); return PT_EINVAL; }
+    if (forward_small_ok(plan)) {
+        if (x2) {
+            // A (x - x2): difference image first (standalone API path)
+            const size_t n = (size_t)plan->H * plan->W;
+            if (ws->image_floats < n) { set_error("workspace image too small"); return PT_EINVAL; }
+            sub_images_kernel<<<(int)std::min<size_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(
+                x, x2, ws->image, n);
+            PT_CHECK_LAUNCH();
+            x = ws->image;
+        }
+        return run_forward_small(plan, ws, sel, x, data, y, sumsq, st, data2, y64);
+    }
     switch (plan->fwd_cfg) {
 #define PT_FWD_CASE(id, TY, TX, NT, MB) \
     case id: return run_forward_cfg<TY, TX, NT, MB>(plan, ws, sel, x, x2, data, y, sumsq, st, data2, y64);
@@ -825,41 +857,6 @@ __device__ __forceinline__ void step_epilogue_vals(const pt_step_epilogue& ep, s
             break;
         }
         default: est = ep.n_scale * g + a0v; break;  // svrg / lsvrg
-    }
-    const float base = xv - ep.gamma * est;
-    const float xh = base + ep.gamma * hv;
-    if (ep.theta) {
-        ep.v_out[p] = base + ep.hcoef * hv;
-        ep.xhat_out[p] = xh;
-    } else {
-        ep.x_out[p] = xh;
-        if (!isfinite(xh) && ep.bad_iter)
-            atomicMin((long long*)ep.bad_iter, (long long)ep.iteration);
-    }
-}
-
-// Gather epilogue kinds (compile-time): 0 plain adjoint, 1 full/sgd, 2 saga,
-// 3 svrg/lsvrg; the number of operand planes prefetched for each
-__host__ __device__ constexpr int epi_planes(int epi)
-{
-    return epi == 0 ? 0 : epi == 1 ? 2 : epi == 2 ? 4 : 3;
-}
-
-// step_epilogue_vals with the estimator class fixed at compile time (the
-// per-pixel epilogue of the gather; same expressions, same operation order)
-template <int EPI>
-__device__ __forceinline__ void step_epilogue_k(const pt_step_epilogue& ep, size_t p, float g,
-                                                float xv, float hv, float a0v, float a1v)
-{
-    float est;
-    if (EPI == 1) {
-        est = ep.estimator == PT_EST_FULL ? g : ep.n_scale * g;
-    } else if (EPI == 2) {
-        est = ep.n_scale * g + (a1v - ep.n_scale * a0v);
-        ep.aux1[p] = (a1v - a0v) + g;
-        ep.aux0[p] = g;
-    } else {
-        est = ep.n_scale * g + a0v;
     }
     const float base = xv - ep.gamma * est;
     const float xh = base + ep.gamma * hv;
@@ -978,18 +975,17 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
             const AngleTab& t = P.tab[P.sel_angle[kb + a]];
             const double gbr = t.gbr, gbc = t.gbc;
             // crossing bin b_f(r, c) = gbr r + gbc c + gg (pos(b_f) == lane)
-            const double bf00 = gbr * r0 + gbc * c0 + t.gg;
-            const double bref = floor(bf00);
-            const double e0 = bf00 - bref;
-            const double lo = e0 + fmin(0.0, gbr) * (TR - 1) + fmin(0.0, gbc) * (TC - 1);
+            double bref;
+            float e0f;
+            gather_origin(t, r0, c0, &bref, &e0f);
+            const double lo = (double)e0f + fmin(0.0, gbr) * (TR - 1) + fmin(0.0, gbc) * (TC - 1);
             const int jlo = (int)floor(lo) - P.cand_half - 1;
             const int bb = (int)bref + jlo;
             // vec: the staged row starts at the 4-aligned bin below bb
             const int shift = P.vec ? bb - (bb & ~3) : 0;
             if (lane == 0) {
                 const float stp = t.step_len;
-                s_p4[buf][a] = make_float4((float)gbr, (float)gbc, (float)e0,
-                                           (float)fabs(t.sigma));
+                s_p4[buf][a] = make_float4((float)gbr, (float)gbc, e0f, (float)fabs(t.sigma));
                 // shared byte address of local bin 0 minus the floor-trick offset
                 const uint32_t ya = stage_u32 +
                                     (uint32_t)((buf * NA + a) * P.slot - jlo + shift) * 4u -
@@ -1191,7 +1187,7 @@ __global__ void epilogue_kernel(const float* g, size_t n, pt_step_epilogue ep)
     pdl_trigger();
 }
 
-static constexpr int kNT = 256, kNA = 32;
+static constexpr int kNT = 256, kNA = kGatherNA;
 
 template <int TR, int TC, bool TWO, int EPI>
 static int run_gather_e(pt_plan* plan, const AdjArgs& a, cudaStream_t st)

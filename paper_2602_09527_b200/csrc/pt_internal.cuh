@@ -106,6 +106,8 @@ namespace pt {
 // images: enough CTAs).  The plan picks one and sizes its staged-bin slot per
 // angle for that tile (capi.cu).
 constexpr int kGatherTiles[4][2] = {{32, 128}, {32, 64}, {16, 64}, {8, 64}};
+constexpr int kGatherNA = 32;  // angles per staged gather chunk
+
 
 // Per-caller scratch for the forward band partials and reductions.  The plan
 // owns one (used by the standalone C-ABI calls, which must therefore be

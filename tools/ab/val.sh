@@ -1,4 +1,5 @@
-O=gpurun_out
+#!/bin/bash
+O=gpurun_out; mkdir -p $O
+timeout 2400 python -m pytest tests -m gpu -q -rf > $O/gpu_tests.log 2>&1
+echo "pytest rc=$?" >> $O/gpu_tests.log
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
-timeout 2400 python -m pytest tests -m gpu -q -rf --durations=10 > $O/gpu_tests.log 2>&1; echo "pytest rc=$?" >> $O/gpu_tests.log
-timeout 900 python bench.py --config c3 --steps 20 --warmup 5 --no-cpu-baseline > $O/bench_c3.json 2> $O/bench_c3.err

@@ -15,7 +15,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2602_09527_b200 import ParallelGeometry, Projector, TvProxConfig, problems, tv_prox  # noqa
 from paper_2602_09527_b200 import _native as N  # noqa: E402
 
-want = set(sys.argv[1:]) or {"fwd", "gather", "fgp", "fgp3"}
+want = set(sys.argv[1:]) or {"fwd", "gather", "fgp", "fgp3", "fwd3"}
 
 
 def timed(fn, n, warm=3):
@@ -87,6 +87,13 @@ for name, (size, A, B, NS) in {"c2": (2048, 1800, 2900, 60), "c1": (512, 720, 76
         out, st = tv_prox(x, 1.0, cfg)
         print(f"{name} fgp{cfg.inner_iterations} {timed(lambda: tv_prox(x, 1.0, cfg, warm=st), 10) / 1e3:.3f} ms",
               flush=True)
+if "fwd3" in want:
+    Z = 256
+    vol = torch.tensor(problems.ellipsoid_phantom(Z, 40, 0), device="cuda", dtype=torch.float32)
+    p3 = Projector(ParallelGeometry.uniform(360, 384), Z, Z, n_slices=Z)
+    sub = tuple(range(0, 360, 40))
+    y3 = torch.empty((len(sub), Z, 384), device="cuda")
+    print(f"c3 subset fwd {timed(lambda: p3.plan.forward_into(vol, y3, sub), 30):.1f} us", flush=True)
 if "fgp3" in want:
     Z = 256
     vol = torch.tensor(problems.ellipsoid_phantom(Z, 40, 0), device="cuda")
