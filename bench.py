@@ -388,6 +388,8 @@ def roofline_record(cfg, msa, cnt, alg, peak, peak_kind):
     top = max(cands, key=lambda k: ms[k])
     achieved = alg[top] / (ms[top] / 1e3) / 1e9
     kernel = KERNEL_OF["fgp3" if (top == "fgp" and cfg.depth > 1) else top]
+    if top == "fwd_band" and cfg.depth == 1 and cfg.size <= 128:
+        kernel = "fwd_small_kernel"  # images <= 128^2: one-launch forward (projector.cu)
     rec = {"kernel": kernel, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
            "frac": round(achieved / peak, 4), "peak_source": peak_kind,
            "algorithmic_bytes_timed": int(alg[top]), "ms_timed": round(ms[top], 3),

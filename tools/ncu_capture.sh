@@ -24,6 +24,6 @@ cap c3 fwd_band 5 fwd_band_kernel 1
 cap c1 fwd_band 5 fwd_band_kernel 1
 cap c1 adj_gather 5 adj_gather_kernel 1
 cap c1 fgp2d 3 fgp2d_kernel 15
-cap c0 fwd_band 5 fwd_band_kernel 1
+cap c0 fwd_small 5 fwd_small_kernel 1
 cap c0 adj_gather 5 adj_gather_kernel 1
 cap c0 fgp2d 3 fgp2d_kernel 7
