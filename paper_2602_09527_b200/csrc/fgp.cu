@@ -713,6 +713,7 @@ struct Fgp3Args {
     float* Rn;          // P_{k+2} (two-iteration pass)
     float lam, eta, beta;  // beta = beta_k (momentum of the output)
     float beta_r;          // R_k = P_k + beta_r (P_k - P_{k-1}) formed on chip
+    float beta1 = 0.f;     // beta_{k+1} (three-iteration pass: R_{k+2})
     int nonneg;
     // register-column pass on a z-slab: planes -2, -1 / Zl, Zl + 1 come from
     // 2-plane ghost buffers [side][P_k: 2 x 3 planes, P_{k-1}: 2 x 3, v: 2]
@@ -1500,6 +1501,332 @@ static int fgp3d_col_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
     return PT_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Three inner iterations per HBM pass (one slab holding the whole volume):
+// fgp3d_col_kernel with a third lagged phase.  At step s phase 0 turns the
+// staged P_k, P_{k-1}, v of plane s + 1 into u_k(s + 1) and P_{k+1}(s),
+// phase 1 turns R_{k+1}(s - 1) into u_{k+1}(s - 1) and P_{k+2}(s - 2), phase 2
+// turns R_{k+2}(s - 3) into u_{k+2}(s - 3) and P_{k+3}(s - 4); the next pass
+// reads {P_{k+2}, P_{k+3}} as its {P_{k-1}, P_k}.  R_{k+2} needs P_{k+1} two
+// planes back (a two-step register delay), phase 2 needs v three planes back.
+// Three iterations make a 3-point ring of the tile inexact; the tile origin
+// keeps 4 columns on the left so that boxes and point pairs stay aligned
+// (16-byte TMA origins, 8-byte pair loads): a 32 x 32-point tile has a
+// 24 x 26 exact core.  Every value is the one-iteration kernel's expression
+// in its operation order (the same u_of / dual as the two-iteration pass), so
+// the pass is bitwise equal to three fgp3d_iter_kernel launches.
+// ---------------------------------------------------------------------------
+template <int BX2, int BY, int NS_ = 3>
+struct Fgp3Col3 {
+    static constexpr int NT = BX2 * BY;
+    static constexpr int BXP = 2 * BX2;       // tile width in points (= box width)
+    static constexpr int NS = NS_;            // TMA ring stages (planes)
+    static constexpr int BW = BXP;            // staged box: the tile itself
+    static constexpr int PL = BW * BY;        // one staged array plane (floats)
+    static constexpr int STAGE = 7 * PL;      // P_k (3), P_{k-1} (3), v
+    static constexpr int XPL = 2 * (NT + 1);  // exchange plane: float2 per thread + zero slot
+    static constexpr int XR = NS * STAGE;     // [2 parity][R_y, R_x of phases 0, 1, 2][XPL]
+    static constexpr int XU = XR + 12 * XPL;  // [2 parity][u of phases 0, 1, 2][XPL]
+    static constexpr int SMEM_FLOATS = XU + 6 * XPL;
+    static constexpr uint32_t TMA_BYTES = (uint32_t)STAGE * 4u;
+    static constexpr int CX = BXP - 8, CY = BY - 6;  // exact core
+    static_assert(CX % 4 == 0 && BW % 4 == 0, "16-byte aligned tile origins (TMA)");
+    static_assert((STAGE * 4) % 128 == 0 && (PL * 4) % 128 == 0, "128-byte aligned TMA boxes");
+};
+
+template <int BX2, int BY, int NS = 3>
+__global__ void __launch_bounds__(BX2 * BY, 1)
+    fgp3d_col3_kernel(Fgp3Args a, const __grid_constant__ Fgp3Maps m)
+{
+    using T = Fgp3Col3<BX2, BY, NS>;
+    constexpr int NT = T::NT, XPL = T::XPL;
+    extern __shared__ __align__(128) float fsm[];
+    __shared__ __align__(8) uint64_t mbar[T::NS];
+    const int tid = threadIdx.x;
+    const int tx = tid % BX2, ty = tid / BX2;
+    const int j0 = blockIdx.x * T::CX - 4, i0 = blockIdx.y * T::CY - 3;
+    const int zb = blockIdx.z * a.zchunk;
+    const int ze = min(a.Zl, zb + a.zchunk);
+    const int H = a.H, W = a.W;  // W even: a pair is inside or outside the image as a whole
+    const size_t HW = (size_t)H * W;
+    const int i = i0 + ty, ja = j0 + 2 * tx;
+    const bool inimg = i >= 0 && i < H && ja >= 0 && ja < W;
+    const bool i_lt = i < H - 1, i_gt = i > 0;
+    const bool jgt_a = ja > 0, jlt_b = ja + 1 < W - 1;
+    const bool core = tx >= 2 && tx < BX2 - 2 && ty >= 3 && ty < BY - 3 && inimg;
+    const bool interior = i0 >= 1 && i0 + BY <= H - 1 && j0 >= 1 && j0 + T::BXP <= W - 1;
+    const int n_up = ty > 0 ? tid - BX2 : NT, n_down = ty < BY - 1 ? tid + BX2 : NT;
+    const int n_left = tx > 0 ? tid - 1 : NT, n_right = tx < BX2 - 1 ? tid + 1 : NT;
+    const int own = ty * T::BW + 2 * tx;  // this pair in a staged plane
+    const f2 br2 = pk(a.beta_r, a.beta_r), bk2 = pk(a.beta, a.beta), bk12 = pk(a.beta1, a.beta1);
+    const f2 eta2 = pk(a.eta, a.eta), nlam2 = pk(-a.lam, -a.lam);
+    const f2 z2 = pk(0.f, 0.f), nz2 = pk(-0.f, -0.f);
+    const bool nonneg = a.nonneg != 0;
+    const int Zg = a.Zg;
+    const uint32_t fsm_u32 = (uint32_t)__cvta_generic_to_shared(fsm);
+    float* XR = fsm + T::XR;
+    float* XU = fsm + T::XU;
+
+    if (tid == 0) {
+        for (int k = 0; k < T::NS; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                (uint32_t)__cvta_generic_to_shared(&mbar[k])));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    if (tid < 18) {  // zero slots of the eighteen exchange planes
+        float* pl = (tid < 12 ? XR + tid * XPL : XU + (tid - 12) * XPL) + 2 * NT;
+        pl[0] = 0.f;
+        pl[1] = 0.f;
+    }
+    __syncthreads();
+    pdl_wait();  // the dual sets are the predecessor's output
+    const int pfirst = zb - 3, plast = ze + 4;  // input planes of this run
+    auto issue = [&](int p, int st) {
+        const uint32_t sb = fsm_u32 + (uint32_t)(st * T::STAGE) * 4u;
+        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&mbar[st]);
+        // planes outside the volume: the sets' zero ghost planes, or zero fill
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"(T::TMA_BYTES));
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb),
+            "l"(&m.R), "r"(j0), "r"(i0), "r"(0), "r"(p + 1), "r"(bar) : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb + (uint32_t)(3 * T::PL) * 4u),
+            "l"(&m.P), "r"(j0), "r"(i0), "r"(0), "r"(p + 1), "r"(bar) : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(sb + (uint32_t)(6 * T::PL) * 4u),
+            "l"(&m.V), "r"(j0), "r"(i0), "r"(p), "r"(bar) : "memory");
+    };
+    if (tid == 0)
+        for (int k = 0; k < T::NS; ++k) issue(pfirst + k, k);
+
+    // carried state (zeros before the run: they only feed planes outside the
+    // exact cone of [zb, ze))
+    f2 r0a[3] = {z2, z2, z2}, r0b[3] = {z2, z2, z2};  // R_k(s), R_k(s + 1)
+    f2 r1a[3] = {z2, z2, z2}, r1b[3] = {z2, z2, z2};  // R_{k+1}(s - 2), R_{k+1}(s - 1)
+    f2 r2a[3] = {z2, z2, z2}, r2b[3] = {z2, z2, z2};  // R_{k+2}(s - 4), R_{k+2}(s - 3)
+    f2 pka[3] = {z2, z2, z2}, pkb[3] = {z2, z2, z2};  // P_k(s), P_k(s + 1)
+    f2 pda[3] = {z2, z2, z2}, pdb[3] = {z2, z2, z2};  // P_{k+1} two steps back (by parity)
+    f2 u0a = z2, u0b = z2, u1a = z2, u1b = z2, u2a = z2, u2b = z2;
+    f2 va = z2, vb = z2, wa = z2, wb = z2;            // v(s - 1), v(s - 3) (by parity)
+    const ptrdiff_t plane3 = 3 * (ptrdiff_t)HW;
+    const size_t gij = core ? (size_t)i * W + ja : 0;
+    float* o2 = a.Pn + plane3 * (zb - 6) + gij;  // P_{k+2}(s - 2): set index s - 1
+    float* o3 = a.Rn + plane3 * (zb - 8) + gij;  // P_{k+3}(s - 4): set index s - 3
+
+    auto u_of = [&](auto XYI, auto ZI, const f2 (&r)[3], f2 rup, f2 rleft, f2 r2low, f2 v,
+                    bool zhi, bool zlo) {
+        f2 x;
+        if constexpr (decltype(XYI)::value) {
+            x = add2(sub2(add2(sub2(nz2, r[0]), rup), r[1]), rleft);
+        } else {
+            x = i_lt ? sub2(nz2, r[0]) : z2;
+            x = i_gt ? add2(x, rup) : x;
+            x = sel2(true, jlt_b, sub2(x, r[1]), x);
+            x = sel2(jgt_a, true, add2(x, rleft), x);
+        }
+        if constexpr (decltype(ZI)::value) {
+            x = add2(sub2(x, r[2]), r2low);
+        } else {
+            x = zhi ? sub2(x, r[2]) : x;
+            x = zlo ? add2(x, r2low) : x;
+        }
+        float ua, ub;
+        upk(fma2(x, nlam2, v), ua, ub);
+        ua = (nonneg && ua < 0.f) ? 0.f : ua;
+        ub = (nonneg && ub < 0.f) ? 0.f : ub;
+        if constexpr (!decltype(XYI)::value) {
+            ua = inimg ? ua : 0.f;
+            ub = inimg ? ub : 0.f;
+        }
+        return pk(ua, ub);
+    };
+    auto dual = [&](auto XYI, auto ZI, const f2 (&r)[3], f2 uo, f2 udown, f2 uright, f2 uz,
+                    bool top, bool zlive, f2 (&pn)[3]) {
+        f2 gv = sub2(udown, uo), gh = sub2(uright, uo);
+        if constexpr (!decltype(XYI)::value) {
+            gv = i_lt ? gv : z2;
+            gh = sel2(true, jlt_b, gh, z2);
+        }
+        f2 gz;
+        if constexpr (decltype(ZI)::value) gz = sub2(uz, uo);
+        else gz = top ? sub2(uz, uo) : z2;
+        const f2 ph = fma2(gv, eta2, r[0]);
+        const f2 qh = fma2(gh, eta2, r[1]);
+        const f2 wh = fma2(gz, eta2, r[2]);
+        const f2 inv = inv_norm2(fma2(wh, wh, fma2(qh, qh, mul2(ph, ph))));  // pinned order
+        pn[0] = mul2(ph, inv);
+        pn[1] = mul2(qh, inv);
+        pn[2] = mul2(wh, inv);
+        if constexpr (!(decltype(XYI)::value && decltype(ZI)::value)) {
+            const bool live = zlive && inimg;
+            pn[0] = live ? pn[0] : z2;
+            pn[1] = live ? pn[1] : z2;
+            pn[2] = live ? pn[2] : z2;
+        }
+    };
+
+    int stg = 0;         // stage of plane s + 1
+    uint32_t phase = 0;  // bit k: parity of stage k's next completion
+    // One plane step; the two-deep registers are passed by role (prev / cur),
+    // the parity-indexed delays (P_{k+1}, v) by their slot of this parity.
+    auto step = [&](auto XYI, auto ZI, int s, f2 (&r0_prev)[3], f2 (&r0_cur)[3],
+                    f2 (&r1_prev)[3], f2 (&r1_in)[3], f2 (&r2_prev)[3], f2 (&r2_in)[3],
+                    f2 (&pk_prev)[3], f2 (&pk_cur)[3], f2 (&pd)[3], f2& u0_prev, f2& u0_cur,
+                    f2& u1_prev, f2& u1_cur, f2& u2_prev, f2& u2_cur, f2& v_m1, f2& v_m3) {
+        const int par = s & 1;
+        mbar_wait((uint32_t)__cvta_generic_to_shared(&mbar[stg]), (phase >> stg) & 1u);
+        phase ^= 1u << stg;
+        const float* sp = fsm + stg * T::STAGE + own;
+        const f2 v1 = ldx2(sp + 6 * T::PL);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            pk_cur[c] = ldx2(sp + c * T::PL);
+            r0_cur[c] = fma2(sub2(pk_cur[c], ldx2(sp + (3 + c) * T::PL)), br2, pk_cur[c]);  // R_k(s + 1)
+        }
+        float* xr = XR + par * 6 * XPL;
+        st2s(xr + 2 * tid, r0_cur[0]);
+        st2s(xr + XPL + 2 * tid, r0_cur[1]);
+        st2s(xr + 2 * XPL + 2 * tid, r1_in[0]);
+        st2s(xr + 3 * XPL + 2 * tid, r1_in[1]);
+        st2s(xr + 4 * XPL + 2 * tid, r2_in[0]);
+        st2s(xr + 5 * XPL + 2 * tid, r2_in[1]);
+        __syncthreads();  // exchange planes of step s written; step s - 1 fully read
+        // the stage of plane s (read at step s - 1) takes plane s + NS
+        if (tid == 0 && s >= pfirst && s + T::NS <= plast)
+            issue(s + T::NS, stg == 0 ? T::NS - 1 : stg - 1);
+        stg = stg + 1 == T::NS ? 0 : stg + 1;
+        const float* xu_prev = XU + (par ^ 1) * 3 * XPL;
+        float* xu = XU + par * 3 * XPL;
+        const int z = a.z0 + s;
+        // ---- phase 0: u_k(s + 1), P_{k+1}(s)
+        u0_cur = u_of(XYI, ZI, r0_cur, ldx2(xr + 2 * n_up),
+                      pk(xr[XPL + 2 * n_left + 1], lo_of(r0_cur[1])), r0_prev[2], v1,
+                      z + 1 < Zg - 1, z + 1 > 0);
+        st2s(xu + 2 * tid, u0_cur);
+        f2 p1[3];
+        dual(XYI, ZI, r0_prev, u0_prev, ldx2(xu_prev + 2 * n_down),
+             pk(hi_of(u0_prev), xu_prev[2 * n_right]), u0_cur, z < Zg - 1, z >= 0 && z < Zg, p1);
+        // ---- phase 1: u_{k+1}(s - 1), P_{k+2}(s - 2)
+        u1_cur = u_of(XYI, ZI, r1_in, ldx2(xr + 2 * XPL + 2 * n_up),
+                      pk(xr[3 * XPL + 2 * n_left + 1], lo_of(r1_in[1])), r1_prev[2], v_m1,
+                      z - 1 < Zg - 1, z - 1 > 0);
+        st2s(xu + XPL + 2 * tid, u1_cur);
+        f2 p2[3];
+        dual(XYI, ZI, r1_prev, u1_prev, ldx2(xu_prev + XPL + 2 * n_down),
+             pk(hi_of(u1_prev), xu_prev[XPL + 2 * n_right]), u1_cur, z - 2 < Zg - 1,
+             z - 2 >= 0 && z - 2 < Zg, p2);
+        // ---- phase 2: u_{k+2}(s - 3), P_{k+3}(s - 4)
+        u2_cur = u_of(XYI, ZI, r2_in, ldx2(xr + 4 * XPL + 2 * n_up),
+                      pk(xr[5 * XPL + 2 * n_left + 1], lo_of(r2_in[1])), r2_prev[2], v_m3,
+                      z - 3 < Zg - 1, z - 3 > 0);
+        st2s(xu + 2 * XPL + 2 * tid, u2_cur);
+        f2 p3[3];
+        dual(XYI, ZI, r2_prev, u2_prev, ldx2(xu_prev + 2 * XPL + 2 * n_down),
+             pk(hi_of(u2_prev), xu_prev[2 * XPL + 2 * n_right]), u2_cur, z - 4 < Zg - 1,
+             z - 4 >= 0 && z - 4 < Zg, p3);
+        // ---- outputs of the run's own planes (exact core only)
+        o2 += plane3;
+        o3 += plane3;
+        if (core && s - 2 >= zb && s - 2 < ze) {
+            st2s(o2, p2[0]); st2s(o2 + HW, p2[1]); st2s(o2 + 2 * HW, p2[2]);
+        }
+        if (core && s - 4 >= zb && s - 4 < ze) {
+            st2s(o3, p3[0]); st2s(o3 + HW, p3[1]); st2s(o3 + 2 * HW, p3[2]);
+        }
+        // R_{k+2}(s - 2) for phase 2 takes the slot of R_{k+2}(s - 4), R_{k+1}(s)
+        // for phase 1 that of R_{k+1}(s - 2) (both consumed above); P_{k+1}(s)
+        // enters the two-step delay; v(s + 1) and v(s - 1) shift in
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            r2_prev[c] = fma2(sub2(p2[c], pd[c]), bk12, p2[c]);
+            r1_prev[c] = fma2(sub2(p1[c], pk_prev[c]), bk2, p1[c]);
+            pd[c] = p1[c];
+        }
+        v_m3 = v_m1;
+        v_m1 = v1;
+    };
+    // roles: even steps (A) and odd steps (B); steps whose planes s - 4 .. s + 1
+    // are all inside [1, Zg - 2] pass every z guard (ZI)
+    auto march = [&](auto XYI) {
+        const std::true_type zi{};
+        const std::false_type zg{};
+        int s = zb - 4;
+        for (; s + 1 <= ze + 3; s += 2) {
+            const int g0 = a.z0 + s;
+            if (g0 - 4 >= 1 && g0 + 2 <= Zg - 2) {
+                step(XYI, zi, s, r0a, r0b, r1a, r1b, r2a, r2b, pka, pkb, pda, u0a, u0b, u1a, u1b,
+                     u2a, u2b, va, wa);
+                step(XYI, zi, s + 1, r0b, r0a, r1b, r1a, r2b, r2a, pkb, pka, pdb, u0b, u0a, u1b,
+                     u1a, u2b, u2a, vb, wb);
+            } else {
+                step(XYI, zg, s, r0a, r0b, r1a, r1b, r2a, r2b, pka, pkb, pda, u0a, u0b, u1a, u1b,
+                     u2a, u2b, va, wa);
+                step(XYI, zg, s + 1, r0b, r0a, r1b, r1a, r2b, r2a, pkb, pka, pdb, u0b, u0a, u1b,
+                     u1a, u2b, u2a, vb, wb);
+            }
+        }
+        if (s <= ze + 3)
+            step(XYI, zg, s, r0a, r0b, r1a, r1b, r2a, r2b, pka, pkb, pda, u0a, u0b, u1a, u1b, u2a,
+                 u2b, va, wa);
+    };
+    if (interior) march(std::true_type{});
+    else march(std::false_type{});
+    pdl_trigger();
+}
+
+template <int BX2, int BY, int NS = 3>
+static int fgp3d_col3_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
+{
+    using T = Fgp3Col3<BX2, BY, NS>;
+    const size_t smem = (size_t)T::SMEM_FLOATS * 4;
+    {
+        const int rc = ensure_smem((const void*)fgp3d_col3_kernel<BX2, BY, NS>, smem);
+        if (rc) return rc;
+    }
+    int per_sm = 0;
+    PT_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, fgp3d_col3_kernel<BX2, BY, NS>, T::NT, smem));
+    Fgp3Maps m;
+    memset(&m, 0, sizeof(m));
+    const cuuint64_t W = a.W, H = a.H;
+    const cuuint64_t d4[4] = {W, H, 3, (cuuint64_t)a.Zl + 2};
+    const cuuint32_t b4[4] = {(cuuint32_t)T::BW, (cuuint32_t)BY, 3, 1};
+    const cuuint64_t d3[3] = {W, H, (cuuint64_t)a.Zl};
+    const cuuint32_t b3[3] = {(cuuint32_t)T::BW, (cuuint32_t)BY, 1};
+    int rc = make_map(&m.R, a.R, 4, d4, b4);
+    if (!rc) rc = make_map(&m.P, a.P, 4, d4, b4);
+    if (!rc) rc = make_map(&m.V, a.v, 3, d3, b3);
+    if (rc) return rc;
+    static const int zc_env = [] {
+        const char* e = getenv("PT_FGP3_ZCHUNK");
+        return e ? std::max(0, atoi(e)) : 0;
+    }();
+    const int tiles = ((a.W + T::CX - 1) / T::CX) * ((a.H + T::CY - 1) / T::CY);
+    // z-runs: each re-marches 8 planes; as few runs as fill whole waves
+    int zc = zc_env;
+    if (!zc) {
+        const int slots = sm_count * std::max(1, per_sm);
+        int best_cost = INT32_MAX;
+        zc = a.Zl;
+        for (int c = 1; c <= std::max(1, a.Zl / 8); ++c) {
+            const int run = (a.Zl + c - 1) / c;
+            const int waves = (tiles * c + slots - 1) / slots;
+            const int cost = waves * (run + 8);
+            if (cost < best_cost) { best_cost = cost; zc = run; }
+        }
+    }
+    a.zchunk = zc;
+    const dim3 grid((a.W + T::CX - 1) / T::CX, (a.H + T::CY - 1) / T::CY,
+                    (a.Zl + a.zchunk - 1) / a.zchunk);
+    PT_CHECK_CUDA(launch_pdl(fgp3d_col3_kernel<BX2, BY, NS>, grid, dim3(T::NT), smem, st, a, m));
+    PT_CHECK_LAUNCH();
+    return PT_OK;
+}
+
 int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int inner,
               int nonneg, float pog, int64_t iteration, int64_t* bad_iter, const ZHalo* halo,
               int sm_count, cudaStream_t st)
@@ -1547,6 +1874,33 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
         int rc = PT_OK;
         int sp = 0, sk = 0;  // sets of P_{k-1}, P_k
         int kk = 0;
+        // three iterations per pass (PT_FGP3_TRIPLE=0: two), then a two-
+        // iteration pass or a single iteration for the remainder
+        static const bool triple = [] {
+            const char* e = getenv("PT_FGP3_TRIPLE");
+            return !(e && e[0] == '0');
+        }();
+        for (; triple && pair_env == 6 && kk + 3 <= inner; kk += 3) {
+            const int o1 = (sk == 2 || sk == 3) ? 0 : 2;  // the pair not being read
+            Fgp3Args a;
+            a.Zl = Zl; a.H = H; a.W = W; a.z0 = 0; a.Zg = Zg;
+            a.v = sl[0].v;
+            a.vtop = nullptr;
+            a.P = fgp3d_set(sl[0].work, sp, Zl, H, W);
+            a.R = fgp3d_set(sl[0].work, sk, Zl, H, W);
+            a.Pn = fgp3d_set(sl[0].work, o1, Zl, H, W);      // P_{k+2}
+            a.Rn = fgp3d_set(sl[0].work, o1 + 1, Zl, H, W);  // P_{k+3}
+            a.lam = (float)lam;
+            a.eta = (float)(1.0 / (12.0 * lam));
+            a.beta = (float)betas[kk];
+            a.beta1 = (float)betas[kk + 1];
+            a.beta_r = kk == 0 ? 0.f : (float)betas[kk - 1];
+            a.nonneg = nonneg;
+            rc = fgp3d_col3_launch<16, 32, 3>(a, sm_count, st);
+            if (rc) return rc;
+            sp = o1;
+            sk = o1 + 1;
+        }
         for (; kk + 2 <= inner; kk += 2) {
             const int o1 = (sk == 2 || sk == 3) ? 0 : 2;  // the pair not being read
             Fgp3Args a;

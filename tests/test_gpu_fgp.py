@@ -128,7 +128,7 @@ import torch
 from paper_2602_09527_b200 import TvProxConfig, tv_prox
 out = []
 for shape, inner, nn in [((37, 44, 68), 11, True), ((64, 64, 64), 30, True), ((5, 16, 200), 2, False),
-                         ((17, 9, 8), 7, True), ((40, 33, 132), 16, False)]:
+                         ((17, 9, 8), 7, True), ((40, 33, 132), 16, False), ((23, 70, 96), 9, False)]:
     rng = np.random.default_rng(sum(shape))
     v = rng.standard_normal(shape).cumsum(axis=0) * 0.1 + 0.2
     x, st = tv_prox(v, 1.0, TvProxConfig(alpha=0.25, inner_iterations=inner, nonneg=nn))
@@ -140,19 +140,22 @@ np.save(sys.argv[1], np.concatenate(out))
 
 
 def test_fgp_3d_pair_pass_bitwise(tmp_path):
-    """Two iterations per HBM pass -- the register-column kernel (default 6,
-    5 / 7 / 8: other tile shapes, explicit z-run lengths) -- give the same
-    values as one iteration per pass (0); odd counts, ragged tiles, image-edge
-    and interior tiles and z-runs included."""
+    """Three and two iterations per HBM pass -- the register-column kernels
+    (default: three-iteration passes, PT_FGP3_TRIPLE=0 two-iteration passes;
+    PT_FGP3_PAIR 5 / 7 / 8: other two-iteration tile shapes; explicit z-run
+    lengths) -- give the same values as one iteration per pass (0); counts
+    with every remainder, ragged tiles, image-edge and interior tiles and
+    z-runs included."""
     import os
     import subprocess
     import sys
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
-    for flag, zc in (("", ""), ("0", ""), ("0", "16"), ("5", ""), ("6", "19"), ("6", "7"),
-                     ("7", ""), ("8", "")):
-        path = tmp_path / f"pair{flag}_{zc}.npy"
-        env = dict(os.environ, PT_FGP3_PAIR=flag, PT_FGP3_ZCHUNK=zc)
+    for flag, zc, tri in (("", "", ""), ("0", "", ""), ("0", "16", ""), ("5", "", ""),
+                          ("6", "19", "0"), ("6", "7", "0"), ("6", "19", ""), ("6", "7", ""),
+                          ("6", "5", ""), ("7", "", ""), ("8", "", "")):
+        path = tmp_path / f"pair{flag}_{zc}_{tri}.npy"
+        env = dict(os.environ, PT_FGP3_PAIR=flag, PT_FGP3_ZCHUNK=zc, PT_FGP3_TRIPLE=tri)
         subprocess.run([sys.executable, "-c", _PAIR_SNIPPET.format(repo=repo), str(path)],
                        check=True, env=env, timeout=300)
         outs.append(np.load(path))
