@@ -1857,13 +1857,15 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
                 PT_CHECK_CUDA(cudaMemsetAsync(set + (size_t)(Zl + 1) * plane3, 0, plane3 * 4, st));
         }
     }
-    // One slab holding the whole volume: two iterations per pass (sets 0/1 and
-    // 2/3 alternate as {P_{k-1}, P_k} -> {P_{k+1}, P_{k+2}}; the first pass
-    // reads set 0 twice, P_{-1} = P_0 with beta_r = 0), an odd last iteration
-    // by the one-iteration kernel.  PT_FGP3_PAIR selects the pass kernel: 6
-    // (default) the register-column kernel with 32 x 16-point tiles; 5 / 7 / 8
-    // other column tiles; 0 none (one iteration per pass).  256^3 FGP-100:
-    // 9.2 ms (6), 14.0 ms (0); the windowed pair kernel this replaced: 11.7 ms.
+    // One slab holding the whole volume: three iterations per pass (sets 0/1
+    // and 2/3 alternate as {P_{k-1}, P_k} -> {P_{k+2}, P_{k+3}}; the first pass
+    // reads set 0 twice, P_{-1} = P_0 with beta_r = 0), the remainder by a
+    // two-iteration pass or the one-iteration kernel.  PT_FGP3_PAIR selects the
+    // two-iteration kernel: 6 (default) the register-column kernel with
+    // 32 x 16-point tiles; 5 / 7 / 8 other column tiles; 0 none (one iteration
+    // per pass, no three-iteration passes either); PT_FGP3_TRIPLE=0 keeps two
+    // iterations per pass.  256^3 FGP-100: 8.0 ms (three), 9.2 ms (two),
+    // 14.0 ms (one); the windowed pair kernel of round 1: 11.7 ms.
     static const int pair_env = [] {
         const char* e = getenv("PT_FGP3_PAIR");
         return (e && *e) ? atoi(e) : 6;
@@ -1896,6 +1898,8 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
             a.beta1 = (float)betas[kk + 1];
             a.beta_r = kk == 0 ? 0.f : (float)betas[kk - 1];
             a.nonneg = nonneg;
+            // 32 x 32-point tiles, 3-stage ring: 256^3 FGP-100 8.0 ms (40 x 24 / 48 x 20 /
+            // 32 x 24 points: 8.3 / 8.7 / 9.6 ms; a 4-stage ring 8.0 ms)
             rc = fgp3d_col3_launch<16, 32, 3>(a, sm_count, st);
             if (rc) return rc;
             sp = o1;
