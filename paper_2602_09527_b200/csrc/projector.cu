@@ -464,7 +464,9 @@ __global__ void __launch_bounds__(256) fwd_reduce_kernel(RedArgs P)
 // ---------------------------------------------------------------------------
 // Small images (pt_joseph.cuh): one launch writes finished residual rows --
 // no band partials, no reduction launch.  Every CTA stages the whole image
-// and sums 32 * RW consecutive rays of the selection, one warp per segment
+// (one TMA box into a dense [132][136] layout when W % 4 == 0, else cp.async
+// into the odd-pitch [132][133] one; 4-byte cp.async of 70 KB per CTA took
+// ~4 us, the box ~1.5 us) and sums 32 * RW consecutive rays of the selection, one warp per segment
 // (lanes = adjacent rays); the segment sums are combined in float64 in
 // segment order, then scaled, and the data rows subtracted, exactly as
 // fwd_reduce_kernel does.  A ray's value does not depend on which CTA
@@ -483,9 +485,12 @@ struct SmallArgs {
     double* y64;  // row-slab partial: s * step_len in float64, no data, no y
 };
 
-__global__ void __launch_bounds__(1024) fwd_small_kernel(SmallArgs a)
+template <int PITCH>
+__global__ void __launch_bounds__(1024) fwd_small_kernel(SmallArgs a,
+                                                         const __grid_constant__ CUtensorMap tmap)
 {
-    extern __shared__ __align__(16) float img[];
+    extern __shared__ __align__(128) float img[];
+    __shared__ __align__(8) uint64_t s_bar;
     __shared__ float part[kSmallNseg][64];
     __shared__ double red[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -505,12 +510,25 @@ __global__ void __launch_bounds__(1024) fwd_small_kernel(SmallArgs a)
     const AngleTab t = a.tab[ang];
     const SmallRay sr = small_ray(t, b, a.H, a.W);
 
+    const uint32_t bar = smem_u32(&s_bar);
+    if (PITCH == kSmallPitchT) {
+        if (tid == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+            asm volatile("fence.mbarrier_init.release.cluster;");
+        }
+        __syncthreads();  // the barrier is initialised before anyone waits on it
+    }
     pdl_wait();  // the image is the predecessor's output
-    small_stage(a.x, a.H, a.W, buf, 0, blockDim.x);
-    cp_async_commit();
-    cp_async_wait_all();
-    __syncthreads();
-    const float acc = live ? small_segment(buf, sr, seg) : 0.f;
+    if (PITCH == kSmallPitchT) {
+        if (tid == 0) small_stage_tma(&tmap, buf, bar);
+        small_mbar_wait(bar, 0);
+    } else {
+        small_stage(a.x, a.H, a.W, buf, 0, blockDim.x);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncthreads();
+    }
+    const float acc = live ? small_segment<PITCH>(buf, sr, seg) : 0.f;
     part[seg][rl] = acc;
     __syncthreads();
     double sq = 0.0;
@@ -552,8 +570,19 @@ static int run_forward_small(pt_plan* plan, Workspace* ws, const pt_selection* s
                              const float* x, const float* data, float* y, double* sumsq,
                              cudaStream_t st, const float* data2, double* y64)
 {
+    // the whole image by one TMA box when its rows are 16-byte granular
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof(tmap));
+    const bool tma = (plan->W % 4) == 0 && (((uintptr_t)x & 15) == 0) && tma_available();
+    if (tma) {
+        const cuuint64_t dims[2] = {(cuuint64_t)plan->W, (cuuint64_t)plan->H};
+        const cuuint32_t box[2] = {(cuuint32_t)kSmallPitchT, (cuuint32_t)kSmallRows};
+        const int rc = make_map(&tmap, x, 2, dims, box);
+        if (rc) return rc;
+    }
+    auto* kern = tma ? fwd_small_kernel<kSmallPitchT> : fwd_small_kernel<kSmallPitch>;
     {
-        const int rc = ensure_smem((const void*)fwd_small_kernel, kSmallSmem);
+        const int rc = ensure_smem((const void*)kern, kSmallSmem);
         if (rc) return rc;
     }
     const long long total = (long long)sel->n * plan->B;
@@ -582,8 +611,8 @@ static int run_forward_small(pt_plan* plan, Workspace* ws, const pt_selection* s
     a.y64 = y64;
     {
         ProfScope ps(ws, PT_PROF_FWD_BAND, st);
-        PT_CHECK_CUDA(launch_pdl(fwd_small_kernel, dim3((unsigned)nblk), dim3(32 * kSmallNseg * rw),
-                                 (size_t)kSmallSmem, st, a));
+        PT_CHECK_CUDA(launch_pdl(kern, dim3((unsigned)nblk), dim3(32 * kSmallNseg * rw),
+                                 (size_t)kSmallSmem, st, a, tmap));
         PT_CHECK_LAUNCH();
     }
     if (sumsq) return launch_sum_doubles(ws->red, nblk, sumsq, 0, st);

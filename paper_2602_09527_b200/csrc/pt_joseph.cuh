@@ -133,8 +133,14 @@ __device__ __forceinline__ float ray_band_sum(uint32_t tile_u32, int st_a, int s
 // ---------------------------------------------------------------------------
 constexpr int kSmallMax = 128, kSmallMargin = 2;
 constexpr int kSmallRows = kSmallMax + 2 * kSmallMargin;       // 132
-constexpr int kSmallPitch = (kSmallMax + 2 * kSmallMargin) | 1;  // 133
-constexpr int kSmallSmem = kSmallRows * kSmallPitch * 4;
+constexpr int kSmallPitch = (kSmallMax + 2 * kSmallMargin) | 1;  // 133 (cp.async staging)
+// one TMA box: x origin -4 (a box's innermost coordinate must be 16-byte
+// aligned), so 4 zero columns on the left; 136 columns cover -4 .. 131
+constexpr int kSmallPitchT = kSmallMax + 8;                      // 136
+constexpr int kSmallSmem = kSmallRows * kSmallPitchT * 4;       // either layout fits
+// columns left of image column 0 in a layout of this pitch
+template <int PITCH>
+constexpr int small_mx() { return PITCH == kSmallPitchT ? 4 : kSmallMargin; }
 constexpr int kSmallSeg = 8, kSmallNseg = kSmallMax / kSmallSeg;
 
 // Threads [t0, t0 + nthr) (whole warps) copy the image into the staged buffer.
@@ -156,6 +162,27 @@ __device__ __forceinline__ void small_stage(const float* x, int H, int W, uint32
     }
 }
 
+// The whole image by one TMA box (136 x 132 from (-4, -2): the copy engine
+// zero-fills outside the image) into the dense [132][136] layout, completion
+// on `bar` (initialised by the caller); one thread issues.  W % 4 == 0.
+__device__ __forceinline__ void small_stage_tma(const CUtensorMap* map, uint32_t buf, uint32_t bar)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"((uint32_t)(kSmallRows * kSmallPitchT * 4)) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(buf),
+        "l"(map), "r"(-4), "r"(-kSmallMargin), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void small_mbar_wait(uint32_t bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "SW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra SW_%=;\n}" ::"r"(bar), "r"(parity) : "memory");
+}
+
 // One ray of one angle: lane position at step 0 (float64 -> float32), slope.
 struct SmallRay {
     float pl, mf, im;
@@ -175,6 +202,7 @@ __device__ __forceinline__ SmallRay small_ray(const AngleTab& t, int b, int H, i
 // Float32 sum of segment `seg` of the ray over the staged buffer: the steps
 // of the segment where pos in [-1.5, n_lanes + 0.5] (outside, both taps are
 // zero, as in fwd_band_kernel).
+template <int PITCH>
 __device__ __forceinline__ float small_segment(uint32_t buf, const SmallRay& r, int seg)
 {
     int st_a = seg * kSmallSeg, st_b = min(r.n_steps, st_a + kSmallSeg);
@@ -188,10 +216,10 @@ __device__ __forceinline__ float small_segment(uint32_t buf, const SmallRay& r, 
         st_b = min(st_b, (int)floorf(fminf(fmaxf(hi, -2.f), (float)kSmallMax + 1.f)) + 1);
     }
     if (st_a >= st_b) return 0.f;
-    // image (0, 0) at buffer (margin, margin)
-    const uint32_t org = buf + (uint32_t)(kSmallMargin * kSmallPitch + kSmallMargin) * 4u;
-    return r.branch == 0 ? ray_band_sum<4, kSmallPitch * 4>(org, st_a, st_b, r.pl, r.mf)
-                         : ray_band_sum<kSmallPitch * 4, 4>(org, st_a, st_b, r.pl, r.mf);
+    // image (0, 0) at buffer row kSmallMargin, column small_mx<PITCH>()
+    const uint32_t org = buf + (uint32_t)(kSmallMargin * PITCH + small_mx<PITCH>()) * 4u;
+    return r.branch == 0 ? ray_band_sum<4, PITCH * 4>(org, st_a, st_b, r.pl, r.mf)
+                         : ray_band_sum<PITCH * 4, 4>(org, st_a, st_b, r.pl, r.mf);
 }
 // Line integral of a ray from its segments' sums (float64, in segment
 // order), and its residual row value (operations pinned: no contraction)
