@@ -108,8 +108,6 @@ namespace pt {
 constexpr int kGatherTiles[4][2] = {{32, 128}, {32, 64}, {16, 64}, {8, 64}};
 constexpr int kGatherNA = 32;  // angles per staged gather chunk
 
-
-
 // Per-caller scratch for the forward band partials and reductions.  The plan
 // owns one (used by the standalone C-ABI calls, which must therefore be
 // stream-serialised per plan, like a cuFFT plan); every session owns its own.
