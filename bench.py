@@ -302,7 +302,7 @@ def build_gpu_problem(cfg, torch):
 
 # launch category -> (kernel, ncu kernel-name key) as in profiles/ncu_roofline_*.json
 KERNEL_OF = {"fwd_band": "fwd_band_kernel", "gather": "adj_gather_kernel",
-             "fgp": "fgp2d_kernel", "fgp3": "fgp3d_col_kernel"}
+             "fgp": "fgp2d_kernel", "fgp3": "fgp3d_col3_kernel"}
 
 
 def sector_prox_sharded(world):

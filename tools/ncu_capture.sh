@@ -19,7 +19,7 @@ done
 cap c2 fwd_band 5 fwd_band_kernel 1
 cap c2 adj_gather 5 adj_gather_kernel 1
 cap c2 fgp2d 3 fgp2d_kernel 13
-cap c3 fgp3d_col 3 fgp3d_col_kernel 50
+cap c3 fgp3d_col3 3 fgp3d_col3_kernel 33
 cap c3 fwd_band 5 fwd_band_kernel 1
 cap c1 fwd_band 5 fwd_band_kernel 1
 cap c1 adj_gather 5 adj_gather_kernel 1
