@@ -477,6 +477,8 @@ static int run_fgp2d(pt_plan* plan, const float* v, double lam, int inner, int n
         betas[k] = (t - 1.0) / tn;
         t = tn;
     }
+    // at least two exact points per region side on the final launch (halo T + 1)
+    tmax = std::max(1, std::min(tmax, (std::min(RW, RH) - 3) / 2));
     const int n_launch = (inner + tmax - 1) / tmax;
     const float *sp = p, *sq = q, *sr = nullptr, *ss = nullptr;
     if (n_launch == 1) {

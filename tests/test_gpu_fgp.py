@@ -168,7 +168,7 @@ import sys, numpy as np, torch
 sys.path.insert(0, {repo!r})
 from paper_2602_09527_b200 import TvProxConfig, tv_prox
 out = []
-for (h, w, inner) in ((2048, 2048, 100), (300, 701, 37), (1000, 130, 13), (128, 128, 50),
+for (h, w, inner) in ((2048, 2048, 100), (300, 701, 37), (1000, 130, 13), (128, 128, 50), (45, 110, 31),
                       (77, 200, 23)):
     rng = np.random.default_rng(h + w)
     v = torch.tensor(rng.standard_normal((h, w)).cumsum(axis=0) * 0.05 + 0.2, device="cuda",
