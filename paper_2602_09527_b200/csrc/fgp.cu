@@ -1021,15 +1021,24 @@ __global__ void fgp3d_final_kernel(Fgp3Args a, float* p_out, float* q_out, float
     pdl_trigger();
 }
 
+// Ghost buffers of the multi-iteration passes on z-slabs: per side up to
+// kGhostD planes of P_k (3 components each), of P_{k-1} and of v; a pass with
+// D <= kGhostD iterations uses the first D plane slots of each region.
+constexpr int kGhostD = 3;
+constexpr int kGhostSide = 7 * kGhostD;  // planes per side
+constexpr int kGhostPm = 3 * kGhostD;    // P_{k-1} region (planes from the side start)
+constexpr int kGhostV = 6 * kGhostD;     // v region
+
 int64_t fgp3d_slab_floats(int Zl, int H, int W)
 {
-    // four sets (P, R ping-pong) + the ghost plane of v + the column pass's
-    // 2-plane ghosts (2 sides x (2 x 3 + 2 x 3 + 2) planes)
-    return 12 * (int64_t)(Zl + 2) * H * W + (int64_t)H * W + 28 * (int64_t)H * W;
+    // four sets (P, R ping-pong) + the ghost plane of v + the column passes'
+    // ghosts (2 sides x kGhostSide planes)
+    return 12 * (int64_t)(Zl + 2) * H * W + (int64_t)H * W + 2 * kGhostSide * (int64_t)H * W;
 }
 static inline float* fgp3d_ghost(float* work, int side, int Zl, int H, int W)
 {
-    return work + 12 * (size_t)(Zl + 2) * H * W + (size_t)H * W + (size_t)side * 14 * H * W;
+    return work + 12 * (size_t)(Zl + 2) * H * W + (size_t)H * W +
+           (size_t)side * kGhostSide * H * W;
 }
 
 // set k of a slab workspace: 0 / 1 = P, R of the even iterations, 2 / 3 = odd
@@ -1089,16 +1098,17 @@ static int fgp3d_exchange(const Fgp3Slab* sl, int G, int H, int W, int which, bo
 // device copies between local slabs and the halo callback (ncclSend /
 // ncclRecv) between ranks.  Buffers on the global boundary stay zero.
 static int fgp3d_ghost_exchange(const Fgp3Slab* sl, int G, int H, int W, int set_k, int set_m,
-                                bool with_v, const ZHalo* halo, cudaStream_t st)
+                                bool with_v, const ZHalo* halo, cudaStream_t st, int D = 2)
 {
     const size_t HW = (size_t)H * W, plane3 = 3 * HW;
-    // (source of the two planes [lo, lo + 1] of slab g, offset in a ghost side, count)
+    // (source of the D planes [lo, lo + D) of slab g, offset in a ghost side, count)
     struct Arr { int kind; size_t goff, count; };  // kind 0: set k, 1: set m, 2: v
-    const Arr arrs[3] = {{0, 0, 2 * plane3}, {1, 6 * HW, 2 * plane3}, {2, 12 * HW, 2 * HW}};
+    const Arr arrs[3] = {{0, 0, D * plane3}, {1, kGhostPm * HW, D * plane3},
+                         {2, kGhostV * HW, D * HW}};
     auto src = [&](const Fgp3Slab& q, const Arr& ar, bool top) -> const float* {
-        if (ar.kind == 2) return q.v + (top ? (size_t)(q.Zl - 2) * HW : 0);
+        if (ar.kind == 2) return q.v + (top ? (size_t)(q.Zl - D) * HW : 0);
         const float* set = fgp3d_set(q.work, ar.kind == 0 ? set_k : set_m, q.Zl, H, W);
-        return set + (top ? (size_t)(q.Zl - 1) * plane3 : plane3);  // set index = plane + 1
+        return set + (top ? (size_t)(q.Zl - D + 1) * plane3 : plane3);  // set index = plane + 1
     };
     for (const Arr& ar : arrs) {
         if (ar.kind == 2 && !with_v) continue;
@@ -1470,10 +1480,10 @@ static int fgp3d_col_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
         const cuuint64_t g4[4] = {W, H, 3, 2};
         const cuuint64_t g3[3] = {W, H, 2};
         for (int side = 0; side < 2 && !rc; ++side) {
-            const float* gb = a.ghost + (size_t)side * 14 * HW;
+            const float* gb = a.ghost + (size_t)side * kGhostSide * HW;
             rc = make_map(&m.Rg[side], gb, 4, g4, b4);
-            if (!rc) rc = make_map(&m.Pg[side], gb + 6 * HW, 4, g4, b4);
-            if (!rc) rc = make_map(&m.Vg[side], gb + 12 * HW, 3, g3, b3);
+            if (!rc) rc = make_map(&m.Pg[side], gb + kGhostPm * HW, 4, g4, b4);
+            if (!rc) rc = make_map(&m.Vg[side], gb + kGhostV * HW, 3, g3, b3);
         }
     }
     if (rc) return rc;
@@ -1586,21 +1596,29 @@ __global__ void __launch_bounds__(BX2 * BY, 1)
     auto issue = [&](int p, int st) {
         const uint32_t sb = fsm_u32 + (uint32_t)(st * T::STAGE) * 4u;
         const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&mbar[st]);
+        // a slab's planes outside [0, Zl) come from its 3-plane ghost buffers;
         // planes outside the volume: the sets' zero ghost planes, or zero fill
+        const bool gh = a.ghost && (p < 0 || p >= a.Zl);
+        const int side = p < 0 ? 0 : 1;
+        const CUtensorMap* mr = gh ? &m.Rg[side] : &m.R;
+        const CUtensorMap* mp = gh ? &m.Pg[side] : &m.P;
+        const CUtensorMap* mv = gh ? &m.Vg[side] : &m.V;
+        const int pz = gh ? (p < 0 ? p + 3 : p - a.Zl) : p + 1;  // set / ghost plane index
+        const int vz = gh ? pz : p;
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
                      "r"(T::TMA_BYTES));
         asm volatile(
             "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
             " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb),
-            "l"(&m.R), "r"(j0), "r"(i0), "r"(0), "r"(p + 1), "r"(bar) : "memory");
+            "l"(mr), "r"(j0), "r"(i0), "r"(0), "r"(pz), "r"(bar) : "memory");
         asm volatile(
             "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
             " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(sb + (uint32_t)(3 * T::PL) * 4u),
-            "l"(&m.P), "r"(j0), "r"(i0), "r"(0), "r"(p + 1), "r"(bar) : "memory");
+            "l"(mp), "r"(j0), "r"(i0), "r"(0), "r"(pz), "r"(bar) : "memory");
         asm volatile(
             "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
             " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(sb + (uint32_t)(6 * T::PL) * 4u),
-            "l"(&m.V), "r"(j0), "r"(i0), "r"(p), "r"(bar) : "memory");
+            "l"(mv), "r"(j0), "r"(i0), "r"(vz), "r"(bar) : "memory");
     };
     if (tid == 0)
         for (int k = 0; k < T::NS; ++k) issue(pfirst + k, k);
@@ -1802,6 +1820,17 @@ static int fgp3d_col3_launch(Fgp3Args& a, int sm_count, cudaStream_t st)
     int rc = make_map(&m.R, a.R, 4, d4, b4);
     if (!rc) rc = make_map(&m.P, a.P, 4, d4, b4);
     if (!rc) rc = make_map(&m.V, a.v, 3, d3, b3);
+    if (a.ghost) {  // z-slab: 3-plane ghosts of P_k, P_{k-1}, v a side
+        const size_t HW = (size_t)a.W * a.H;
+        const cuuint64_t g4[4] = {W, H, 3, 3};
+        const cuuint64_t g3[3] = {W, H, 3};
+        for (int side = 0; side < 2 && !rc; ++side) {
+            const float* gb = a.ghost + (size_t)side * kGhostSide * HW;
+            rc = make_map(&m.Rg[side], gb, 4, g4, b4);
+            if (!rc) rc = make_map(&m.Pg[side], gb + kGhostPm * HW, 4, g4, b4);
+            if (!rc) rc = make_map(&m.Vg[side], gb + kGhostV * HW, 3, g3, b3);
+        }
+    }
     if (rc) return rc;
     static const int zc_env = [] {
         const char* e = getenv("PT_FGP3_ZCHUNK");
@@ -1978,15 +2007,53 @@ int fgp3d_run(const Fgp3Slab* sl, int G, int H, int W, int Zg, double lam, int i
         for (int g = 0; g < G; ++g) {  // the volume's own boundary: zero ghosts
             if (sl[g].z0 == 0)
                 PT_CHECK_CUDA(cudaMemsetAsync(fgp3d_ghost(sl[g].work, 0, sl[g].Zl, H, W), 0,
-                                              14 * (size_t)H * W * 4, st));
+                                              kGhostSide * (size_t)H * W * 4, st));
             if (sl[g].z0 + sl[g].Zl == Zg)
                 PT_CHECK_CUDA(cudaMemsetAsync(fgp3d_ghost(sl[g].work, 1, sl[g].Zl, H, W), 0,
-                                              14 * (size_t)H * W * 4, st));
+                                              kGhostSide * (size_t)H * W * 4, st));
         }
         int sp = 0, sk = 0;  // sets of P_{k-1}, P_k (P_{-1} = P_0 with beta_r = 0)
         int kk = 0;
+        // three iterations per pass with 3-plane ghosts when every slab holds
+        // >= 3 planes (decided from the global plane count: all ranks agree)
+        static const bool triple = [] {
+            const char* e = getenv("PT_FGP3_TRIPLE");
+            return !(e && e[0] == '0');
+        }();
+        bool tri = triple && pair_env == 6 && Zg / (ranks * G) >= 3;
+        for (int g = 0; g < G; ++g) tri = tri && sl[g].Zl >= 3;
+        for (; tri && kk + 3 <= inner; kk += 3) {
+            rc = fgp3d_ghost_exchange(sl, G, H, W, sk, sp, kk == 0, halo, st, 3);
+            if (rc) return rc;
+            const int o1 = (sk == 2 || sk == 3) ? 0 : 2;
+            for (int g = 0; g < G; ++g) {
+                const int Zl = sl[g].Zl;
+                Fgp3Args a;
+                a.Zl = Zl; a.H = H; a.W = W; a.z0 = sl[g].z0; a.Zg = Zg;
+                a.v = sl[g].v;
+                a.vtop = nullptr;
+                a.P = fgp3d_set(sl[g].work, sp, Zl, H, W);
+                a.R = fgp3d_set(sl[g].work, sk, Zl, H, W);
+                a.Pn = fgp3d_set(sl[g].work, o1, Zl, H, W);      // P_{k+2}
+                a.Rn = fgp3d_set(sl[g].work, o1 + 1, Zl, H, W);  // P_{k+3}
+                a.lam = (float)lam;
+                a.eta = (float)(1.0 / (12.0 * lam));
+                a.beta = (float)betas[kk];
+                a.beta1 = (float)betas[kk + 1];
+                a.beta_r = kk == 0 ? 0.f : (float)betas[kk - 1];
+                a.nonneg = nonneg;
+                a.ghost = fgp3d_ghost(sl[g].work, 0, Zl, H, W);
+                rc = fgp3d_col3_launch<16, 32, 3>(a, sm_count, st);
+                if (rc) return rc;
+            }
+            sp = o1;
+            sk = o1 + 1;
+        }
+        // two iterations per pass (the remainder, or slabs of 2 planes); the
+        // lower ghost slots of v hold planes -2, -1 only after a 2-plane exchange
+        const int k2 = kk;
         for (; kk + 2 <= inner; kk += 2) {
-            rc = fgp3d_ghost_exchange(sl, G, H, W, sk, sp, kk == 0, halo, st);
+            rc = fgp3d_ghost_exchange(sl, G, H, W, sk, sp, kk == k2, halo, st);
             if (rc) return rc;
             const int o1 = (sk == 2 || sk == 3) ? 0 : 2;
             for (int g = 0; g < G; ++g) {
