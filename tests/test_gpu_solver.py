@@ -333,24 +333,28 @@ def _problem_3d(Z=10, size=32, seed=4):
     return TomoProblem(proj, data, tv=TvProxConfig(alpha=0.05, inner_iterations=12)), proj
 
 
-@pytest.mark.parametrize("slabs", [2, 3, 5, 10])
-def test_zslab_decomposition_is_bitwise_identical(slabs):
+@pytest.mark.parametrize("slabs,inner", [(2, 12), (3, 12), (5, 12), (10, 12), (2, 13), (3, 14),
+                                         (5, 13)])
+def test_zslab_decomposition_is_bitwise_identical(slabs, inner):
     """3D z-slab data path emulated on one device: every virtual slab sees its
     neighbours only through the ghost planes the halo exchange fills; the
     trajectory must equal the single-volume run bit for bit (the projector is
-    slice-local, the slab FGP recomputes the same values).  Slabs of >= 2
-    planes (2, 3, 5 of 10) run the two-iteration column pass with 2-plane
-    ghosts exchanged once per pass; 1-plane slabs (10) the one-iteration
-    kernel with a halo round per iteration."""
+    slice-local, the slab FGP recomputes the same values).  Slabs of >= 3
+    planes (2, 3 of 10) run the three-iteration column pass with 3-plane
+    ghosts exchanged once per pass, the remainder of the iteration count (12,
+    13, 14: 0, 1, 2) a single iteration or a two-iteration pass; 2-plane slabs
+    (5) the two-iteration pass with 2-plane ghosts; 1-plane slabs (10) the
+    one-iteration kernel with a halo round per iteration."""
     from paper_2602_09527_b200 import distributed as D
     from paper_2602_09527_b200.solvers import _init_state, _plan_segment
     problem, proj = _problem_3d()
+    tv = TvProxConfig(alpha=problem.tv.alpha, inner_iterations=inner)
     lip = proj.norm_sq(20, 0)
     outs = []
     for g in (1, slabs):
         cfg = SolverConfig(gamma=1.0 / lip, skip_probability=0.5, n_subsets=5, estimator="svrg",
                            max_data_passes=1e9, seed=7)
-        st = _init_state(cfg, TomoProblem(proj, problem.data, tv=problem.tv), None)
+        st = _init_state(cfg, TomoProblem(proj, problem.data, tv=tv), None)
         if g > 1:
             D.emulate_zslabs(st.session, g)
         subs, th, rf, _, _ = _plan_segment(st, cfg, 1 << 40, max_steps=30)
