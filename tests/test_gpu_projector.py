@@ -283,3 +283,25 @@ def test_small_forward_tma_and_cp_async_staging_agree_bitwise(oracle, size, A, B
         assert torch.equal(ya, ym)
         y_ref = oracle.forward_project(x, g, s)
         assert rel_l2(cpu(ya), y_ref) <= TOL
+
+
+def test_random_small_geometries_match_oracle(oracle):
+    """Seeded random small problems (both sides <= 128: the one-launch
+    forward; odd and even widths: its TMA and cp.async staging; bin spacing
+    and pixel size != 1: two-tap and multi-candidate gathers) against the
+    float64 oracle, full and subset selections."""
+    rng = np.random.default_rng(20261021)
+    for _ in range(12):
+        H, W = int(rng.integers(3, 129)), int(rng.integers(3, 129))
+        A, B = int(rng.integers(1, 41)), int(rng.integers(3, 220))
+        ds = float(rng.choice([0.5, 0.7, 1.0, 1.3]))
+        h = float(rng.choice([0.8, 1.0, 1.5]))
+        g = ParallelGeometry.uniform(A, B, ds, h)
+        x = rng.standard_normal((H, W))
+        sub = tuple(sorted(rng.choice(A, size=max(1, A // 3), replace=False).tolist()))
+        for s in (None, sub):
+            y_ref = oracle.forward_project(x, g, s)
+            assert rel_l2(cpu(forward_project(x, g, s)), y_ref) <= TOL, (H, W, A, B, ds, h)
+            r = rng.standard_normal(y_ref.shape)
+            assert rel_l2(cpu(back_project(r, g, (H, W), s)),
+                          oracle.back_project(r, g, (H, W), s)) <= TOL, (H, W, A, B, ds, h)
