@@ -252,9 +252,13 @@ int pt_plan_create(const pt_geometry_desc* d, pt_plan** out)
         const char* e = getenv("PT_FWD_CFG");
         return e ? atoi(e) : -1;
     }();
-    if (mn >= 512) p->fwd_cfg = cfg_env >= 0 ? cfg_env : 3;
-    else if (mn >= 128) p->fwd_cfg = 100;
+    // slice stacks (config 3: 256 slices of 256^2) have CTAs to spare: 64-step
+    // bands on 128-lane tiles (c3 subset forward 122 -> 100 us against the
+    // 32 x 128 tiles a single 256^2 image needs to fill the GPU)
+    if (mn >= 512) p->fwd_cfg = 3;
+    else if (mn >= 128) p->fwd_cfg = p->Z > 1 ? 1 : 100;
     else p->fwd_cfg = 101;
+    if (cfg_env >= 0) p->fwd_cfg = cfg_env;  // PT_FWD_CFG overrides every size
     pt::forward_config(p->fwd_cfg, &p->fwd_ty, &p->fwd_tx);
     p->n_bands = (std::max(p->H, p->W) + p->fwd_ty - 1) / p->fwd_ty;
     const size_t per_angle = (size_t)p->n_bands * p->Z * p->B;
