@@ -174,34 +174,38 @@ def _slab_fgp(v_loc, z0, Zg, lam, inner, nonneg, rank, world):
     return np.maximum(x, 0.0) if nonneg else x
 
 
-def _slab_fgp_pass2(v_loc, z0, Zg, lam, inner, nonneg, rank, world):
-    """The native two-iteration column pass on z-slabs (csrc/fgp.cu,
-    fgp3d_ghost_exchange): before each pass of two iterations a slab receives
-    the two boundary planes of P_k and P_{k-1} of its neighbours (and of v
-    once), computes P_{k+1} on its planes and one plane into each ghost
-    region, then P_{k+2} on its own planes; an odd last iteration uses the
+def _slab_fgp_passes(v_loc, z0, Zg, lam, inner, nonneg, rank, world, D=2):
+    """The native multi-iteration column passes on z-slabs (csrc/fgp.cu,
+    fgp3d_ghost_exchange): before each pass of D iterations (D = 3 when every
+    slab holds >= 3 planes, else 2) a slab receives the D boundary planes of
+    P_k and P_{k-1} of its neighbours (and of v, once per pass depth) into
+    D-plane ghost regions, computes P_{k+1} on its planes and D - 1 planes into
+    each ghost region, ..., P_{k+D} on its own planes; the remainder of the
+    iteration count runs a two-iteration pass and / or one iteration with the
     one-plane protocol.  Restated in float64 numpy over gloo."""
     import torch
     zl, H, W = v_loc.shape
-    G = 2  # ghost planes per side; extended plane index e = z + G
+    G = 3  # ghost planes per side; extended plane index e = z + G
 
-    def exchange2(A):
-        """A: [zl + 2G, ...]; ghosts <- the neighbours' two boundary planes"""
+    def exchange(A, d):
+        """A: [zl + 2G, ...]; the d ghost planes nearest the slab <- the
+        neighbours' d boundary planes"""
         reqs, lo, hi = [], None, None
         if rank > 0:
-            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(A[G:2 * G])), rank - 1))
-            lo = torch.empty(A[:G].shape, dtype=torch.float64)
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(A[G:G + d])), rank - 1))
+            lo = torch.empty(A[:d].shape, dtype=torch.float64)
             reqs.append(dist.irecv(lo, rank - 1))
         if rank + 1 < world:
-            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(A[zl:zl + G])), rank + 1))
-            hi = torch.empty(A[:G].shape, dtype=torch.float64)
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(A[G + zl - d:G + zl])),
+                                   rank + 1))
+            hi = torch.empty(A[:d].shape, dtype=torch.float64)
             reqs.append(dist.irecv(hi, rank + 1))
         for r in reqs:
             r.wait()
         if lo is not None:
-            A[:G] = lo.numpy()
+            A[G - d:G] = lo.numpy()
         if hi is not None:
-            A[zl + G:] = hi.numpy()
+            A[G + zl:G + zl + d] = hi.numpy()
 
     def inside(z):
         return 0 <= z0 + z < Zg
@@ -246,7 +250,6 @@ def _slab_fgp_pass2(v_loc, z0, Zg, lam, inner, nonneg, rank, world):
 
     V = np.zeros((zl + 2 * G, H, W))
     V[G:G + zl] = v_loc
-    exchange2(V)
     P = np.zeros((zl + 2 * G, 3, H, W))
     Q = P.copy()
     t, betas = 1.0, []
@@ -254,21 +257,27 @@ def _slab_fgp_pass2(v_loc, z0, Zg, lam, inner, nonneg, rank, world):
         tn = (1.0 + np.sqrt(1.0 + 4.0 * t * t)) / 2.0
         betas.append((t - 1.0) / tn)
         t = tn
-    k = 0
-    while k + 2 <= inner:
-        exchange2(P)
-        exchange2(Q)
-        br = 0.0 if k == 0 else betas[k - 1]
-        P1 = step(P, Q, br, V, -1, zl + 1)   # own planes and one into each ghost region
-        P2 = step(P1, P, betas[k], V, 0, zl)
-        Q, P = P1, P2
-        k += 2
+    k, v_depth = 0, 0
+    for depth in (D, 2):
+        while depth > 1 and k + depth <= inner:
+            if v_depth != depth:  # v's ghosts, once per pass depth
+                exchange(V, depth)
+                v_depth = depth
+            exchange(P, depth)
+            exchange(Q, depth)
+            for i in range(depth):  # iteration k + i on planes [-(depth-1-i), zl + depth-1-i)
+                br = 0.0 if k + i == 0 else betas[k + i - 1]
+                r = depth - 1 - i
+                Q, P = P, step(P, Q, br, V, -r, zl + r)
+            k += depth
     if k < inner:
-        exchange2(P)
-        exchange2(Q)
+        exchange(P, 1)
+        exchange(Q, 1)
+        if v_depth == 0:
+            exchange(V, 1)
         br = 0.0 if k == 0 else betas[k - 1]
         Q, P = P, step(P, Q, br, V, 0, zl)
-    exchange2(P)
+    exchange(P, 1)
     R = P
     x = []
     for z in range(zl):
@@ -328,10 +337,21 @@ def _zworker(rank, world, port, q):
         # even and odd iteration counts
         if min(b - a for a, b in spans) >= 2:
             for inner in (12, 7):
-                xs = _slab_fgp_pass2(v[z0:z1], z0, Z, 0.3, inner, True, rank, world)
+                xs = _slab_fgp_passes(v[z0:z1], z0, Z, 0.3, inner, True, rank, world, 2)
                 xt = gather_zslabs(torch.from_numpy(xs), Z).numpy()
                 xo, _ = O.tv_prox(v, 1.0, 0.3, inner, True)
                 out[f"pass2_err_{inner}"] = float(np.abs(xt - xo).max())
+        # (6) the three-iteration pass protocol (3-plane ghosts once per pass,
+        # then a two-iteration pass and / or one iteration for the remainder)
+        # on a volume whose slabs hold >= 3 planes
+        Z3 = 3 * world + 1
+        a3, b3 = zslab_bounds(Z3, rank, world)
+        v3 = rng.standard_normal((Z3, H, W))
+        for inner in (12, 13, 14):
+            xs = _slab_fgp_passes(v3[a3:b3], a3, Z3, 0.3, inner, True, rank, world, 3)
+            xt = gather_zslabs(torch.from_numpy(xs), Z3).numpy()
+            xo, _ = O.tv_prox(v3, 1.0, 0.3, inner, True)
+            out[f"pass3_err_{inner}"] = float(np.abs(xt - xo).max())
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -356,6 +376,8 @@ def test_zslab_logic_and_halo_protocol_over_gloo(world):
         for inner in (12, 7):
             if f"pass2_err_{inner}" in res:
                 assert res[f"pass2_err_{inner}"] <= 1e-12, res
+        for inner in (12, 13, 14):
+            assert res[f"pass3_err_{inner}"] <= 1e-12, res
 
 
 # ---------------------------------------------------------------------------
@@ -506,3 +528,5 @@ def test_rows_logic_and_protocols_over_gloo(world):
         for inner in (12, 7):
             if f"pass2_err_{inner}" in res:
                 assert res[f"pass2_err_{inner}"] <= 1e-12, res
+        for inner in (12, 13, 14):
+            assert res[f"pass3_err_{inner}"] <= 1e-12, res
