@@ -72,71 +72,6 @@ __device__ __forceinline__ float max_nan(float a, float b)
     asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
     return r;
 }
-// One FGP inner iteration on the register strips.  EDGE = the region touches
-// the image border (masks needed); interior regions skip every boundary test.
-template <int RW, int RH, int STRIP, bool EDGE, bool NONNEG>
-__device__ __forceinline__ void fgp2d_iteration(
-    float (&v)[STRIP], float (&p)[STRIP], float (&q)[STRIP], float (&r)[STRIP],
-    float (&s)[STRIP], float (&u)[STRIP], float (*S_s)[RW + 2], float (*S_u)[RW + 2],
-    float (*S_r)[RW], float (*S_ut)[RW], int tx, int ty, int i0, int H, bool not_last_col,
-    unsigned in_mask, float lam, float eta, float beta)
-{
-    const int row0 = ty * STRIP;
-#pragma unroll
-    for (int k = 0; k < STRIP; ++k) S_s[row0 + k][tx + 1] = s[k];
-    S_r[ty + 1][tx] = r[STRIP - 1];
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < STRIP; ++k) {
-        const float r_up = k ? r[k - 1] : S_r[ty][tx];
-        const float s_left = S_s[row0 + k][tx];
-        // _diff_adjoint (regularizers.py:70-76), numpy statement order
-        float o;
-        if (EDGE) {
-            const int gi = i0 + row0 + k;
-            o = (gi < H - 1) ? -r[k] : 0.f;
-            o += r_up;
-            o = not_last_col ? o - s[k] : o;
-        } else {
-            o = -r[k];
-            o += r_up;
-            o = o - s[k];
-        }
-        o += s_left;
-        float uu = fmaf(-lam, o, v[k]);
-        if (NONNEG) uu = max_nan(uu, 0.f);
-        if (EDGE) uu = ((in_mask >> k) & 1u) ? uu : 0.f;
-        u[k] = uu;
-        S_u[row0 + k][tx + 1] = uu;
-    }
-    S_ut[ty][tx] = u[0];
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < STRIP; ++k) {
-        const float u_down = (k < STRIP - 1) ? u[k + 1] : S_ut[ty + 1][tx];
-        const float u_right = S_u[row0 + k][tx + 2];
-        float gv = u_down - u[k], gh = u_right - u[k];
-        if (EDGE) {
-            const int gi = i0 + row0 + k;
-            gv = (gi < H - 1) ? gv : 0.f;
-            gh = not_last_col ? gh : 0.f;
-        }
-        // the packed path's operations exactly (fma order, rsqrt of max(n2, 1)),
-        // so an edge region and an interior one give the same bits
-        const float ph = fmaf(eta, gv, r[k]);
-        const float qh = fmaf(eta, gh, s[k]);
-        const float n2 = fmaf(ph, ph, qh * qh);
-        const float inv = rsqrt_ftz(max_nan(n2, 1.f));
-        const float pn = ph * inv, qn = qh * inv;
-        if (!EDGE || ((in_mask >> k) & 1u)) {
-            r[k] = fmaf(beta, pn - p[k], pn);
-            s[k] = fmaf(beta, qn - q[k], qn);
-            p[k] = pn;
-            q[k] = qn;
-        }
-    }
-}
-
 // Interior iteration with packed f32x2 arithmetic.  A thread's strip rows are
 // held as pairs (j, j + H2), H2 = STRIP/2, so the up-neighbour of pair j is
 // pair j-1 and the down-neighbour of pair j is pair j+1 (one repack at the
@@ -154,15 +89,35 @@ __device__ __forceinline__ void st2(float2* p, f2 v)
     asm volatile("st.shared.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "l"(v.v));
 }
 
-template <int RW, int RH, int STRIP, bool NONNEG>
+// per-half select of two pairs: (clo ? lo(a) : lo(b), chi ? hi(a) : hi(b))
+__device__ __forceinline__ f2 sel2(f2 a, f2 b, bool clo, bool chi)
+{
+    float al, ah, bl, bh;
+    upk(a, al, ah);
+    upk(b, bl, bh);
+    return pk(clo ? al : bl, chi ? ah : bh);
+}
+
+// EDGE = the region touches the image border (or the arrays' row range): the
+// same packed arithmetic, with the boundary rules of fgp2d_iteration applied
+// by per-half selects -- lr_mask bit k: strip row k is above the image's last
+// row (D's vertical difference and D^T's -r term exist), in_mask bit k: the
+// point is inside the image, nlc: the column is not the image's last.  A point
+// inside the image and off its last row / column evaluates exactly the
+// interior expressions, so edge and interior regions agree bitwise.
+template <int RW, int RH, int STRIP, bool NONNEG, bool EDGE = false>
 __device__ __forceinline__ void fgp2d_iteration_packed(
     f2 (&V)[STRIP / 2], f2 (&Pp)[STRIP / 2], f2 (&Q)[STRIP / 2], f2 (&R)[STRIP / 2],
     f2 (&S)[STRIP / 2], f2 (&U)[STRIP / 2], float2 (*S_s2)[RW + 2], float2 (*S_u2)[RW + 2],
-    float (*S_r)[RW], float (*S_ut)[RW], int tx, int ty, float lam, float eta, float beta)
+    float (*S_r)[RW], float (*S_ut)[RW], int tx, int ty, float lam, float eta, float beta,
+    unsigned in_mask = 0u, unsigned lr_mask = 0u, bool nlc = true)
 {
     constexpr int H2 = STRIP / 2;
     const int prow0 = ty * H2;
     const f2 nlam2 = pk(-lam, -lam), eta2 = pk(eta, eta), beta2 = pk(beta, beta);
+    const f2 z2 = pk(0.f, 0.f);
+    auto in_ = [&](int k) { return ((in_mask >> k) & 1u) != 0u; };
+    auto lr_ = [&](int k) { return ((lr_mask >> k) & 1u) != 0u; };
 #pragma unroll
     for (int j = 0; j < H2; ++j) st2(&S_s2[prow0 + j][tx + 1], S[j]);
     S_r[ty + 1][tx] = hi_of(R[H2 - 1]);
@@ -173,13 +128,18 @@ __device__ __forceinline__ void fgp2d_iteration_packed(
         const f2 r_up = j ? R[j - 1] : pk(S_r[ty][tx], lo_of(R[H2 - 1]));
         const f2 s_left = ld2(&S_s2[prow0 + j][tx]);
         // _diff_adjoint (regularizers.py:70-76): ((-r + r_up) - s) + s_left
-        const f2 o = add2(sub2(sub2(r_up, R[j]), S[j]), s_left);
+        f2 o = sub2(r_up, R[j]);
+        if (EDGE) o = sel2(o, r_up, lr_(j), lr_(j + H2));
+        const f2 os = sub2(o, S[j]);
+        o = (!EDGE || nlc) ? os : o;
+        o = add2(o, s_left);
         f2 u = fma2(nlam2, o, V[j]);
         if (NONNEG) {
             float ua, ub;
             upk(u, ua, ub);
             u = pk(max_nan(ua, 0.f), max_nan(ub, 0.f));  // NaN propagates
         }
+        if (EDGE) u = sel2(u, z2, in_(j), in_(j + H2));
         U[j] = u;
         st2(&S_u2[prow0 + j][tx + 1], u);
     }
@@ -190,8 +150,12 @@ __device__ __forceinline__ void fgp2d_iteration_packed(
         // rows (j+1, j+1+H2); for the last pair: (pair 0 hi, next strip's first row)
         const f2 u_down = (j < H2 - 1) ? U[j + 1] : pk(hi_of(U[0]), S_ut[ty + 1][tx]);
         const f2 u_right = ld2(&S_u2[prow0 + j][tx + 2]);
-        const f2 gv = sub2(u_down, U[j]);
-        const f2 gh = sub2(u_right, U[j]);
+        f2 gv = sub2(u_down, U[j]);
+        f2 gh = sub2(u_right, U[j]);
+        if (EDGE) {
+            gv = sel2(gv, z2, lr_(j), lr_(j + H2));
+            gh = nlc ? gh : z2;
+        }
         const f2 ph = fma2(eta2, gv, R[j]);
         const f2 qh = fma2(eta2, gh, S[j]);
         const f2 n2 = fma2(ph, ph, mul2(qh, qh));
@@ -200,10 +164,20 @@ __device__ __forceinline__ void fgp2d_iteration_packed(
         // 1 / max(1, |.|): rsqrt of max(n2, 1) (exactly 1 at 1; NaN propagates)
         const f2 inv = pk(rsqrt_ftz(max_nan(na, 1.f)), rsqrt_ftz(max_nan(nb, 1.f)));
         const f2 pn = mul2(ph, inv), qn = mul2(qh, inv);
-        R[j] = fma2(beta2, sub2(pn, Pp[j]), pn);
-        S[j] = fma2(beta2, sub2(qn, Q[j]), qn);
-        Pp[j] = pn;
-        Q[j] = qn;
+        const f2 rn = fma2(beta2, sub2(pn, Pp[j]), pn);
+        const f2 sn = fma2(beta2, sub2(qn, Q[j]), qn);
+        if (EDGE) {
+            const bool a = in_(j), b = in_(j + H2);
+            R[j] = sel2(rn, R[j], a, b);
+            S[j] = sel2(sn, S[j], a, b);
+            Pp[j] = sel2(pn, Pp[j], a, b);
+            Q[j] = sel2(qn, Q[j], a, b);
+        } else {
+            R[j] = rn;
+            S[j] = sn;
+            Pp[j] = pn;
+            Q[j] = qn;
+        }
     }
 }
 
@@ -255,7 +229,7 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
             }
         }
     };
-    zero_pads(!edge);
+    zero_pads(true);
     if (tid < RW) {
         S_r[0][tid] = 0.f;
         S_ut[NS][tid] = 0.f;
@@ -336,31 +310,16 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
         if (it < P.n_iter)
             fgp2d_iteration_packed<RW, RH, STRIP, NONNEG>(V, Pp, Q, R, S, U, S_s2, S_u2, S_r, S_ut,
                                                           tx, ty, P.lam, P.eta, P.beta[it]);
-    }
-    for (int it = 0; edge && it < P.n_iter; ++it) {
-        {
-            float v[STRIP], p[STRIP], q[STRIP], r[STRIP], s[STRIP], u[STRIP];
-#pragma unroll
-            for (int j = 0; j < H2; ++j) {
-                upk(V[j], v[j], v[j + H2]);
-                upk(Pp[j], p[j], p[j + H2]);
-                upk(Q[j], q[j], q[j + H2]);
-                upk(R[j], r[j], r[j + H2]);
-                upk(S[j], s[j], s[j + H2]);
-                upk(U[j], u[j], u[j + H2]);
-            }
-            fgp2d_iteration<RW, RH, STRIP, true, NONNEG>(v, p, q, r, s, u, S_s, S_u, S_r, S_ut, tx,
-                                                         ty, gi0, P.H, not_last_col, in_mask, P.lam,
-                                                         P.eta, P.beta[it]);
-#pragma unroll
-            for (int j = 0; j < H2; ++j) {
-                Pp[j] = pk(p[j], p[j + H2]);
-                Q[j] = pk(q[j], q[j + H2]);
-                R[j] = pk(r[j], r[j + H2]);
-                S[j] = pk(s[j], s[j + H2]);
-                U[j] = pk(u[j], u[j + H2]);
-            }
-        }
+    } else {
+        // the same packed iteration with the boundary rules as per-half selects
+        // (bit k of lr_mask: image row of strip row k below H - 1)
+        const int last_k = P.H - 1 - (gi0 + row0);  // strip rows k < last_k are above the last row
+        const unsigned lr_mask =
+            last_k <= 0 ? 0u : (last_k >= STRIP ? (1u << STRIP) - 1u : (1u << last_k) - 1u);
+        for (int it = 0; it < P.n_iter; ++it)
+            fgp2d_iteration_packed<RW, RH, STRIP, NONNEG, true>(
+                V, Pp, Q, R, S, U, S_s2, S_u2, S_r, S_ut, tx, ty, P.lam, P.eta, P.beta[it],
+                in_mask, lr_mask, not_last_col);
     }
 
     float v[STRIP], p[STRIP], q[STRIP], r[STRIP], s[STRIP];
@@ -383,7 +342,7 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
     if (P.final_) {
         // x = max(v - lam D^T(p, q), 0), then the ProxSkip h update
         __syncthreads();
-        if (!edge) zero_pads(false);
+        zero_pads(false);
 #pragma unroll
         for (int k = 0; k < STRIP; ++k) S_s[row0 + k][tx + 1] = q[k];
         S_r[ty + 1][tx] = p[STRIP - 1];
