@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
         S_ut[NS][tid] = 0.f;
     }
 
-    pdl_wait();
+    pdl_wait<PDL_FGP2D>();
     // packed state: pair j = strip rows (j, j + H2)
     f2 V[H2], Pp[H2], Q[H2], R[H2], S[H2], U[H2];
     unsigned in_mask = 0;
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(RW*(RH / STRIP), 2) fgp2d_kernel(FgpArgs P)
             P.s_out[idx] = s[k];
         }
     }
-    pdl_trigger();
+    pdl_trigger<PDL_FGP2D>();
 }
 
 int64_t fgp_workspace_floats(const pt_plan* plan)
@@ -750,7 +750,7 @@ __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
         }
         __syncthreads();
     }
-    pdl_wait();  // the dual sets are the predecessor's output
+    pdl_wait<PDL_FGP3D>();  // the dual sets are the predecessor's output
     // plane p (local; -1 / Zl are ghosts) into stage s
     auto stage = [&](int p, int s) {
         const uint32_t sb = fsm_u32 + (uint32_t)(s * T::STAGE) * 4u;
@@ -909,7 +909,7 @@ __global__ void __launch_bounds__(TX * TY / 2) fgp3d_iter_kernel(Fgp3Args a,
         }
     }
     if (!TMA) asm volatile("cp.async.wait_group 0;");
-    pdl_trigger();
+    pdl_trigger<PDL_FGP3D>();
 }
 
 __device__ __forceinline__ f2 ld2s(const float* p)
@@ -1223,7 +1223,7 @@ __global__ void __launch_bounds__(BX2 * BY, MINB)
         pl[1] = 0.f;
     }
     __syncthreads();
-    pdl_wait();  // the dual sets are the predecessor's output
+    pdl_wait<PDL_FGP3D>();  // the dual sets are the predecessor's output
     const int pfirst = zb - 2, plast = ze + 2;  // input planes of this run
     auto issue = [&](int p, int st) {
         const uint32_t sb = fsm_u32 + (uint32_t)(st * T::STAGE) * 4u;
@@ -1409,7 +1409,7 @@ __global__ void __launch_bounds__(BX2 * BY, MINB)
     };
     if (interior) march(std::true_type{});
     else march(std::false_type{});
-    pdl_trigger();
+    pdl_trigger<PDL_FGP3D>();
 }
 
 template <int BX2, int BY, int MINB, int NS = 3>
@@ -1550,7 +1550,7 @@ __global__ void __launch_bounds__(BX2 * BY, 1)
         pl[1] = 0.f;
     }
     __syncthreads();
-    pdl_wait();  // the dual sets are the predecessor's output
+    pdl_wait<PDL_FGP3D>();  // the dual sets are the predecessor's output
     const int pfirst = zb - 3, plast = ze + 4;  // input planes of this run
     auto issue = [&](int p, int st) {
         const uint32_t sb = fsm_u32 + (uint32_t)(st * T::STAGE) * 4u;
@@ -1754,7 +1754,7 @@ __global__ void __launch_bounds__(BX2 * BY, 1)
     };
     if (interior) march(std::true_type{});
     else march(std::false_type{});
-    pdl_trigger();
+    pdl_trigger<PDL_FGP3D>();
 }
 
 template <int BX2, int BY, int NS = 3>

@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P,
     const bool tma = P.tma && it.branch == 0;
     const uint32_t bar = smem_u32(&s_bar);
     if (stager) {
-        pdl_wait();  // the image is the predecessor's output
+        pdl_wait<PDL_FWD>();  // the image is the predecessor's output
         if (tma) {
             if (tid == 32)
                 fwd_tma_issue(&tmap, tile_u32, bar, it.tile * TX - T::HL, it.band * TY, it.z,
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P,
             if (tid == 0) s_pref[0] = 0;
         }
         if (!waited) {
-            if (!stager) pdl_wait();
+            if (!stager) pdl_wait<PDL_FWD>();
             else if (!tma) cp_async_wait_all();
         }
         __syncthreads();
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(NT, MINB) fwd_band_kernel(FwdArgs P,
         }
         if (cbeg + CH < a_end) __syncthreads();  // chunk tables are rewritten next
     }
-    pdl_trigger();
+    pdl_trigger<PDL_FWD>();
 }
 
 __global__ void sub_images_kernel(const float* a, const float* b, float* out, size_t n)
@@ -393,7 +393,7 @@ struct RedArgs {
 
 __global__ void __launch_bounds__(256) fwd_reduce_kernel(RedArgs P)
 {
-    pdl_wait();
+    pdl_wait<PDL_REDUCE>();
     // n_k * Z * B < 2^31 (checked on the host): 32-bit index math
     const unsigned total = (unsigned)P.n_k * P.Z * P.B;
     const unsigned idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(256) fwd_reduce_kernel(RedArgs P)
         double yd = s * (double)at.step_len;
         if (P.y64) {  // partial line integrals of a row slab (summed over ranks later)
             P.y64[((size_t)k * P.Z + z) * P.B + b] = yd;
-            pdl_trigger();
+            pdl_trigger<PDL_REDUCE>();
             return;
         }
         if (P.data) yd -= (double)P.data[((size_t)ang * P.Z + z) * P.B + b];
@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(256) fwd_reduce_kernel(RedArgs P)
             P.block_sums[blockIdx.x] = s;
         }
     }
-    pdl_trigger();
+    pdl_trigger<PDL_REDUCE>();
 }
 
 // ---------------------------------------------------------------------------
@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(1024) fwd_small_kernel(SmallArgs a,
         }
         __syncthreads();  // the barrier is initialised before anyone waits on it
     }
-    pdl_wait();  // the image is the predecessor's output
+    pdl_wait<PDL_FWD_SMALL>();  // the image is the predecessor's output
     if (PITCH == kSmallPitchT) {
         if (tid == 0) small_stage_tma(&tmap, buf, bar);
         small_mbar_wait(bar, 0);
@@ -554,7 +554,7 @@ __global__ void __launch_bounds__(1024) fwd_small_kernel(SmallArgs a,
             a.block_sums[blockIdx.x] = s;
         }
     }
-    pdl_trigger();
+    pdl_trigger<PDL_FWD_SMALL>();
 }
 
 static bool forward_small_ok(const pt_plan* plan)
@@ -1067,7 +1067,7 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
 
     const int n_chunks = (P.n_sel + NA - 1) / NA;
     if (n_chunks > 0) prepare_params(0, 0);
-    pdl_wait();  // the residual rows are the predecessor's output
+    pdl_wait<PDL_GATHER>();  // the residual rows are the predecessor's output
     if (n_chunks > 0) prepare_stage(0, 0);
     for (int ci = 0; ci < n_chunks; ++ci) {
         const int buf = (P.nbuf == 2) ? (ci & 1) : 0;
@@ -1183,7 +1183,7 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
 
     const int c = c0 + cl;
     if (c >= P.W) {
-        pdl_trigger();
+        pdl_trigger<PDL_GATHER>();
         return;
     }
     const float* epi = smem + P.nbuf * NA * P.slot;
@@ -1204,7 +1204,7 @@ __global__ void __launch_bounds__(NT, (TR * TC / NT > 8) ? 3 : 4) adj_gather_ker
                                  NEPI > 3 ? epi[3 * TR * TC + e] : 0.f);
         }
     }
-    pdl_trigger();
+    pdl_trigger<PDL_GATHER>();
 }
 
 __global__ void epilogue_kernel(const float* g, size_t n, pt_step_epilogue ep)

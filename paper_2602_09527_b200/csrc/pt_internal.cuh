@@ -57,14 +57,38 @@ extern std::atomic<long long> g_launches;  // kernels launched by this library
 // with programmatic stream serialisation: a kernel may start while its
 // predecessor drains, runs only predecessor-independent prologue work, then
 // pdl_wait() (griddepcontrol.wait: the predecessor grid has completed and its
-// writes are visible).  Every such kernel calls pdl_trigger() only after its
-// last global write, so when kernel N+1 is released, kernels <= N-1 are
-// complete -- N+1's prologue may read their outputs, never kernel N's.
+// writes are visible).  A kernel family releases its successor either at its
+// end, after its last global write (the default), or right after its own wait
+// (its bit set in PT_PDL_EARLY_MASK: the successor's CTAs become resident as
+// this grid's last CTAs retire and block at their own wait).  Either way, when
+// kernel N+1 is released some thread of kernel N has passed its wait, so
+// kernels <= N-1 are complete -- N+1's prologue may read their outputs, never
+// kernel N's (nor any buffer kernel N writes).  Measured per family
+// (tools/ab/pdl_mask.sh, profiles/ANALYSIS_r02.md): only the one-launch small
+// forward gains from the early release (config 0 +7.7%: its successor, the
+// gather, stages its operands while the forward's single wave drains); an
+// early release everywhere is slower (config 1 -17%: the successor's CTAs
+// pile onto the SMs that drain first instead of spreading over all of them).
 // Kernels launched without the attribute see both as no-ops.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#ifndef PT_PDL_EARLY_MASK
+#define PT_PDL_EARLY_MASK 2  // PDL_FWD_SMALL
+#endif
+enum : int {
+    PDL_FWD = 1, PDL_FWD_SMALL = 2, PDL_REDUCE = 4, PDL_GATHER = 8, PDL_FGP2D = 16,
+    PDL_FGP3D = 32, PDL_MISC = 64
+};
+template <int F = PDL_MISC>
+__device__ __forceinline__ void pdl_wait()
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if constexpr ((PT_PDL_EARLY_MASK & F) != 0)
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+template <int F = PDL_MISC>
 __device__ __forceinline__ void pdl_trigger()
 {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if constexpr ((PT_PDL_EARLY_MASK & F) == 0)
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 bool pdl_enabled();
 
