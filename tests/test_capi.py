@@ -76,3 +76,34 @@ def test_reference_binding_loads_standalone():
     src = open(RB.__file__, encoding="utf-8").read()
     # standalone: a maintainer copies this one file next to proxtomo/projector.py
     assert "from . import" not in src and "from .." not in src
+
+
+def test_every_pdl_launched_kernel_waits_before_it_releases():
+    """The launch chain's rule (csrc/pt_internal.cuh): a kernel launched with
+    programmatic stream serialisation must call pdl_wait() (else it would run
+    beside its predecessor), and releases its successor only after that wait --
+    either inside pdl_wait() (early families) or by a later pdl_trigger()."""
+    csrc = os.path.join(REPO, "paper_2602_09527_b200", "csrc")
+    bodies, launched = {}, set()
+    for f in os.listdir(csrc):
+        if not f.endswith(".cu"):
+            continue
+        src = open(os.path.join(csrc, f), encoding="utf-8").read()
+        parts = re.split(r"(?=__global__)", src)
+        for part in parts[1:]:
+            m = re.search(r"(\w+_kernel)\s*\(", part)
+            if m:
+                bodies[m.group(1)] = part
+        for m in re.finditer(r"launch_pdl\(([^;]*?);", src, flags=re.S):
+            launched.update(re.findall(r"\b(\w+_kernel)\b", m.group(1)))
+    assert launched, "no PDL launches found"
+    for name in sorted(launched):
+        body = bodies.get(name)
+        assert body is not None, name
+        wait = re.search(r"pdl_wait(<\w+>)?\(\)", body)
+        assert wait, f"{name} is launched with PDL but never waits"
+        first_trigger = re.search(r"pdl_trigger(<\w+>)?\(\)", body)
+        assert first_trigger and first_trigger.start() > wait.start(), name
+    hdr = open(os.path.join(csrc, "pt_internal.cuh"), encoding="utf-8").read()
+    w = hdr.index("void pdl_wait()")
+    assert hdr.index("griddepcontrol.wait", w) < hdr.index("griddepcontrol.launch_dependents", w)
